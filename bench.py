@@ -1,0 +1,348 @@
+"""Benchmark: Pauli rotations/s (and HBM GB/s) on a 30-qubit fp64 state (BASELINE.json configs[1]).
+
+One step = one ps_apply_rotations call applying a layer of 1000 random Pauli rotations of weight
+1-10 (the R10 generator of DESIGN.md "Input recipe") to the full 2^30-amplitude state, inputs
+resident in HBM; value = rotations / second (whole job).  N > 1 GPUs (torchrun): the same
+30-qubit state sharded over N ranks by its top qubits (strong scaling), exchanges over NCCL.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--n 30] [--layer 1000] [--kind R10] [--dtype c128] [--fusion 2]
+
+--impl reference times the CPU oracle (the slow from-definition program) on the host cores,
+on a bounded sample of the same workload (scaled to the 30-qubit metric), and prints the same
+line with "impl": "reference".
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import workloads  # noqa: E402
+
+METRIC = "Pauli rotations/sec and HBM GB/s at 30-36 qubits, 1/2/4/8 B200"
+UNIT = "rotations/s"
+FALLBACK_HBM_GBS = 6650.0
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", type=int, default=30)
+    ap.add_argument("--layer", type=int, default=1000)
+    ap.add_argument("--kind", default="R10")
+    ap.add_argument("--dtype", default="c128", choices=["c128", "c64"])
+    ap.add_argument("--fusion", type=int, default=2)
+    ap.add_argument("--tile-bits", type=int, default=0)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def workload_name(args):
+    return (f"{args.n}q {'fp64' if args.dtype == 'c128' else 'fp32'} random Pauli-rotation layer "
+            f"({args.kind}: weight 1-10, phi~U[-pi,pi)), {args.layer} rotations/step")
+
+
+def layers(args, count):
+    out = []
+    for s in range(count):
+        codes, ang = workloads.random_layer(args.n, args.layer, seed=1000 + s, kind=args.kind)
+        out.append((codes, ang))
+    return out
+
+
+# ------------------------------------------------------------------------------ clocks
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+               0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+        self.th = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+            return
+        self.th = threading.Thread(target=self._read, daemon=True)
+        self.th.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        if self.th:
+            self.th.join(timeout=2)
+        sm, mx, reasons = [], 0.0, set()
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 3:
+                continue
+            try:
+                s, m = float(parts[0]), float(parts[1])
+                bits = int(parts[2], 16) if parts[2].startswith("0x") else int(parts[2])
+            except ValueError:
+                continue
+            sm.append(s)
+            mx = max(mx, m)
+            for b, name in self.REASONS.items():
+                if bits & b and name != "gpu_idle":
+                    reasons.add(name)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, torch copy_)"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def traffic_for(kernel: str):
+    """dram bytes per launch from the committed ncu --set full summary, if any."""
+    path = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(path) as fh:
+            d = json.load(fh)
+        return d.get(kernel)
+    except Exception:
+        return None
+
+
+# ------------------------------------------------------------------------------ CPU oracle
+
+def cpu_oracle_sample(args, budget_s=15.0, n_sample=26):
+    """The oracle as it stands, on the host cores: apply the layer's rotations (restricted to the
+    low n_sample qubits, same weights/letters otherwise) at n_sample qubits until the time budget
+    is spent; rot/s is scaled by 2^(n_sample - n) to the n-qubit state (cost is linear in 2^n)."""
+    import oracle
+    n_s = min(n_sample, args.n)
+    codes, ang = workloads.random_layer(n_s, args.layer, seed=1000, kind=args.kind)
+    psi = oracle.random_state(workloads.BASE_SEED, n_s)
+    done, t0 = 0, time.perf_counter()
+    while done < len(ang):
+        psi = oracle.apply(n_s, psi, codes[done:done + 1], ang[done:done + 1])
+        done += 1
+        if time.perf_counter() - t0 > budget_s:
+            break
+    el = time.perf_counter() - t0
+    rate = done / el * 2.0 ** (n_s - args.n)
+    cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
+    return {"value": rate, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"{done} rotations of a {args.kind} layer on a {n_s}-qubit fp64 state in {el:.1f} s, "
+                      f"scaled by 2^({n_s}-{args.n}) to the {args.n}-qubit state"}
+
+
+def run_reference(args):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    steps = []
+    for s in range(args.warmup + args.steps):
+        r = cpu_oracle_sample(args, budget_s=8.0)
+        if s >= args.warmup:
+            steps.append(r)
+    value = statistics.mean(r["value"] for r in steps)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": args.layer / value * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": {"workload": workload_name(args), "n_qubits": args.n,
+                                        "rotations_per_step": args.layer},
+        "cpu_baseline": {k: steps[-1][k] for k in ("kind", "cores", "sample")} | {"value": value, "unit": UNIT},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------------------ ours
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2504_17881_b200 as P
+    from paper_2504_17881_b200 import ps
+
+    world, rank, local = dist_env()
+    if world != args.gpus:
+        args.gpus = world
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    st = P.State(args.n, args.dtype, world=world, rank=rank, torch_memory=True)
+    st.set_option(ps.OPT_FUSION, args.fusion)
+    if args.tile_bits:
+        st.set_option(ps.OPT_TILE_BITS, args.tile_bits)
+    st.set_option(ps.OPT_PROFILE, 1)
+    lay = layers(args, args.warmup + args.steps)
+    enc = [P.pauli_encode_codes(c) + (a,) for c, a in lay]
+    st.init_random(workloads.BASE_SEED)
+
+    stream = torch.cuda.current_stream()
+    for w in range(args.warmup):
+        x, z, a = enc[w]
+        st.apply_rotations(x, z, a)
+    st.synchronize()
+    st.reset_stats()
+    barrier()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for s in range(args.steps):
+        x, z, a = enc[args.warmup + s]
+        st.apply_rotations(x, z, a)
+    e1.record(stream)
+    st.synchronize()
+    torch.cuda.synchronize()
+    barrier()
+    ms = e0.elapsed_time(e1)
+    clk = clocks.stop()
+    stats = st.stats()
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_per_step = ms / args.steps
+    value = args.layer / (ms_per_step / 1e3)
+    amp_bytes = 16 if args.dtype == "c128" else 8
+    local_state = amp_bytes << (args.n - (world.bit_length() - 1))
+    hbm_alg = sum(stats["algo_bytes"][k] for k in ("stream", "tile", "coset")) / (ms / 1e3) / 1e9 * world
+
+    # dominant kernel roofline (CUDA events around each launch on the launching stream)
+    fam = max(("stream", "tile", "coset"), key=lambda k: stats["kernel_ms"][k])
+    launches = max(1, stats["launches"][fam])
+    kms = stats["kernel_ms"][fam]
+    bytes_per_launch = stats["algo_bytes"][fam] / launches
+    achieved = stats["algo_bytes"][fam] / (kms / 1e3) / 1e9 if kms > 0 else 0.0
+    peak, peak_src = peaks()
+    rotations = stats["rotations"]
+    passes = max(1, stats["passes"])
+    gpu_launches = sum(stats["launches"][k] for k in ("stream", "tile", "coset"))
+
+    # e2e through the public API with host buffers (pinned): H2D of the initial state + rotation
+    # arrays, the layer, D2H of the norm (the step's scalar result)
+    e2e = None
+    if not args.no_e2e:
+        tdt = torch.float64 if args.dtype == "c128" else torch.float32
+        host = torch.empty(local_state // (amp_bytes // 2), dtype=tdt, pin_memory=True)
+        st.init_random(workloads.BASE_SEED)
+        host.copy_(st._tensor)  # the seeded initial state, staged in pinned host memory (untimed)
+        h2d = local_state + 24 * args.layer
+        e_steps = min(args.steps, 2)
+        x, z, a = enc[0]
+        st.set_state_ptr(host.data_ptr(), 1 << (args.n - (world.bit_length() - 1)), first=rank << st.n_local)
+        st.apply_rotations(x, z, a)
+        st.norm()
+        barrier()
+        t0 = time.perf_counter()
+        for s in range(e_steps):
+            x, z, a = enc[(args.warmup + s) % len(enc)]
+            st.set_state_ptr(host.data_ptr(), 1 << st.n_local, first=rank << st.n_local)
+            st.apply_rotations(x, z, a)
+            st.norm()
+        barrier()
+        el = time.perf_counter() - t0
+        if world > 1:
+            t = torch.tensor([el], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            el = float(t.item())
+        e2e = {"value": args.layer * e_steps / el, "unit": UNIT, "h2d_bytes_per_step": h2d * world,
+               "d2h_bytes_per_step": 8, "steps": e_steps,
+               "path": "ps_set_state(pinned host) + ps_apply_rotations(host arrays) + ps_norm -> host"}
+        del host
+
+    if rank == 0:
+        cpu = None if args.no_cpu else cpu_oracle_sample(args)
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64" if args.dtype == "c128" else "f32",
+            "data": "synthetic",
+            "config": {"workload": workload_name(args), "n_qubits": args.n, "rotations_per_step": args.layer,
+                       "fusion": args.fusion, "parallelism": f"state sharded over {world} GPU(s) by top qubits",
+                       "l2": "inputs larger than L2 (state %.1f GiB per GPU)" % (local_state / 2 ** 30)},
+            "hbm_gbs": hbm_alg,
+            "bytes_per_rotation": stats["algo_bytes"]["stream"] / max(1, stats["rotations_by"]["stream"])
+            if fam == "stream" else sum(stats["algo_bytes"][k] for k in ("stream", "tile", "coset")) / max(1, rotations),
+            "rotations_per_pass": rotations / passes,
+            "passes": {k: stats["launches"][k] for k in ("stream", "tile", "coset")},
+            "exchanges": stats["exchanges"],
+            "roofline": {"bound": "hbm", "kernel": fam, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "peak_source": peak_src,
+                         "algorithmic_bytes_per_launch": bytes_per_launch,
+                         "avg_launch_ms": kms / launches, "traffic": traffic_for(fam)},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": gpu_launches,
+            "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+    st.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,243 @@
+/*
+ * ps.h -- C ABI of libps: full-state-vector simulation of Pauli-rotation layers on B200.
+ *
+ * The hot path of arXiv 2504.17881 ("phase2"): starting from a state |psi>, apply the sequence
+ * of Pauli rotations exp(i phi P) (Introduction), each by the closed form
+ * exp(i phi P) = cos(phi) I + i sin(phi) P, with P encoded as two 64-bit masks
+ * (P:116-121).  One process per GPU; the state is partitioned over G = 2^m GPUs by its
+ * top m qubits (Mathematical model).
+ *
+ * Citations "P:n" are PAPER.md line numbers; "S:n" SPEC.md line numbers; readings of ambiguous
+ * passages are numbered R1.. in DESIGN.md.
+ *
+ * Conventions (all entry points)
+ *   - Qubit q (0-based) is factor P_{q+1} of the string and bit q of the basis index.
+ *   - Pauli string masks: xmask bit q set iff P_{q+1} in {X, Y}  (the paper's p1);
+ *                         zmask bit q set iff P_{q+1} in {Y, Z}  (the paper's p2).
+ *   - Amplitude storage: interleaved (re, im) of the handle's element type:
+ *       PS_C128 -> two doubles per amplitude (the paper's C99 _Complex double),
+ *       PS_C64  -> two floats per amplitude.
+ *   - Rotation order: angle[0] is applied first: U = R_{count-1} ... R_1 R_0 (R7).
+ *   - Multi-GPU (world > 1): every call is SPMD-collective -- all ranks call it with identical
+ *     arguments (like MPI).  Index ranges are GLOBAL logical indices; rank r owns
+ *     [r*2^(n-m), (r+1)*2^(n-m)) at every call boundary.
+ *   - Errors: every entry point returns a ps_status (0 = PS_OK).  Arguments are validated before
+ *     any device work, so a call that fails validation leaves the state unchanged.  An
+ *     asynchronous CUDA or NCCL fault poisons the handle: later calls return PS_ESTATE.
+ *     ps_last_error() gives a thread-local message for the last failure.
+ *   - Ownership: the library owns handles and (unless ps_create_ex is given a buffer) the state
+ *     memory.  Input arrays are borrowed for the duration of the call only.  Output buffers are
+ *     caller-allocated.  One handle per host thread; no internal locking.
+ *   - Stream semantics: device work is enqueued on the handle's stream.  ps_apply_rotations and
+ *     ps_init_* return once the work is enqueued; ps_synchronize, ps_norm, ps_expectation,
+ *     ps_inner, ps_get_amplitudes block until their result is available.
+ */
+#ifndef PS_H
+#define PS_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct ps_state *ps_handle; /* opaque; owned by the library */
+
+typedef enum { PS_C128 = 0, PS_C64 = 1 } ps_dtype;
+
+typedef enum {
+    PS_OK = 0,
+    PS_EINVAL = -1,      /* bad argument: NULL with count > 0, n out of range, non-finite angle, bad letter */
+    PS_ERANGE = -2,      /* mask bit >= n, or index range beyond 2^n */
+    PS_ENOMEM = -3,      /* device or host allocation failed */
+    PS_ECUDA = -4,       /* CUDA runtime error */
+    PS_ENCCL = -5,       /* NCCL error */
+    PS_ESTATE = -6,      /* handle poisoned by an earlier asynchronous fault */
+    PS_EUNSUPPORTED = -7 /* valid request this build cannot serve (e.g. world > 1 without NCCL) */
+} ps_status;
+
+/* kernel families counted in ps_stats */
+enum {
+    PS_K_STREAM = 0,   /* K1: streaming pair-rotation pass (single rotation or same-x run)   */
+    PS_K_TILE = 1,     /* K2: low-qubit fused tile pass (contiguous 2^k tile through TMA)     */
+    PS_K_COSET = 2,    /* K7: coset-tile fused pass (gathered 2^k tile)                       */
+    PS_K_REDUCE = 3,   /* K5: norm / expectation / inner-product reductions                   */
+    PS_K_INIT = 4,     /* K6: state initialisation                                            */
+    PS_K_EXCHANGE = 5, /* K3: half-vector exchange (staging copies + NCCL send/recv)          */
+    PS_K_COUNT = 6
+};
+
+typedef struct ps_stats {
+    uint64_t rotations;                  /* rotations applied since the last reset */
+    uint64_t passes;                     /* HBM passes over the local state (all kernel families) */
+    uint64_t exchanges;                  /* half-vector exchanges, counting the swap-back */
+    uint64_t launches[PS_K_COUNT];       /* kernel launches per family */
+    uint64_t rotations_by[PS_K_COUNT];   /* rotations applied per family */
+    double algo_bytes[PS_K_COUNT];       /* algorithmic HBM bytes per family (2*2^n_l*s per pass) */
+    double nvlink_bytes;                 /* bytes sent to peers by exchanges */
+    double kernel_ms[PS_K_COUNT];        /* device time per family (CUDA events; PS_OPT_PROFILE=1 only) */
+} ps_stats;
+
+/* options for ps_set_option */
+enum {
+    PS_OPT_PROFILE = 0,       /* 1: time every launch with CUDA events on the handle's stream (default 0) */
+    PS_OPT_FUSION = 1,        /* 0: one rotation per pass (K1 only); 1: same-x runs; 2: + tiles (default 2) */
+    PS_OPT_TILE_BITS = 2,     /* log2 amplitudes per fused tile (default: 12 for C128, 13 for C64) */
+    PS_OPT_CHUNK_BYTES = 3,   /* exchange chunk size in bytes (default 256 MiB) */
+    PS_OPT_MAX_PASS_ROTS = 4, /* cap on rotations fused into one tile pass (default 64) */
+    PS_OPT_VEC256 = 5         /* 1: 256-bit LDG/STG in K1 (default 1); 0: 128-bit */
+};
+
+/* ------------------------------------------------------------------------------------------ */
+/* Lifetime                                                                                    */
+
+/* Single GPU on the current CUDA device.  n_qubits in [1, 40] (memory permitting).
+ * The state is allocated (2^n * 16 B for PS_C128) and set to |0>. */
+int ps_create(int n_qubits, int dtype, ps_handle *out);
+
+/* General constructor.
+ *   dev_buf/bytes: optional caller-owned device buffer holding the LOCAL slice
+ *                  (2^(n-m) amplitudes); NULL -> the library allocates.  The caller keeps it
+ *                  alive until ps_destroy.
+ *   stream:        optional cudaStream_t to enqueue on (e.g. torch's current stream); NULL ->
+ *                  the library creates a non-blocking stream.
+ *   rank, world:   this process's rank and the number of GPUs G = 2^m, 1 <= G, G | 2^(n-1)
+ *                  (M = 2^m tasks, one per GPU).
+ *   nccl_id:       128-byte ncclUniqueId from ps_get_unique_id on rank 0, broadcast by the
+ *                  caller (torch.distributed); ignored when world == 1.
+ * The state is set to |0>. */
+int ps_create_ex(int n_qubits, int dtype, void *dev_buf, size_t bytes, void *stream, int rank,
+                 int world, const void *nccl_id, ps_handle *out);
+
+/* Convenience: ps_create_ex with library-owned memory and stream. */
+int ps_create_dist(int n_qubits, int dtype, int rank, int world, const void *nccl_id,
+                   ps_handle *out);
+
+/* Writes a fresh 128-byte ncclUniqueId into out (host only; call on rank 0). */
+int ps_get_unique_id(void *out);
+
+int ps_destroy(ps_handle h);
+
+/* Introspection: qubits, local qubits n-m, rank, world, dtype, device pointer of the local slice. */
+int ps_info(ps_handle h, int *n_qubits, int *n_local, int *rank, int *world, int *dtype,
+            void **dev_ptr);
+
+int ps_set_option(ps_handle h, int option, int64_t value);
+
+/* ------------------------------------------------------------------------------------------ */
+/* State initialisation and access (a7 row; P:519 random init for benchmarks, P:625 basis
+ * states for guiding states)                                                                  */
+
+/* |index>: all amplitudes zero except a_index = 1.  PS_ERANGE if index >= 2^n. */
+int ps_init_basis(ps_handle h, uint64_t index);
+
+/* Unnormalised seeded amplitudes a_i = u(seed, 2i) + i u(seed, 2i+1) with the counter-based
+ * generator of DESIGN.md "Input recipe" (values in [-1, 1), exact in fp64; rounded once to fp32
+ * for PS_C64).  Identical for any world size. */
+int ps_init_random(ps_handle h, uint64_t seed);
+
+/* Scales the state to unit norm (one reduction + one scaling pass). */
+int ps_normalize(ps_handle h);
+
+/* Copies count amplitudes from host memory amps (interleaved, handle dtype) into global indices
+ * [first, first+count).  Every rank passes the same data; each keeps the part it owns.
+ * PS_ERANGE if first+count > 2^n.  Pinned host memory gives full PCIe bandwidth. */
+int ps_set_state(ps_handle h, uint64_t first, uint64_t count, const void *amps);
+
+/* Copies global indices [first, first+count) to host memory amps_out (interleaved, handle
+ * dtype).  With world > 1 the result appears on every rank.  Blocks. */
+int ps_get_amplitudes(ps_handle h, uint64_t first, uint64_t count, void *amps_out);
+
+/* ------------------------------------------------------------------------------------------ */
+/* The hot path                                                                                */
+
+/* Applies exp(i angle[l] P_l) for l = 0 .. count-1 in that order, P_l given by
+ * (xmask[l], zmask[l]).  Pairs (i, i xor xmask) are updated by
+ *   a'_i = cos(phi) a_i + i sin(phi) w(i xor x) a_(i xor x),
+ *   w(i) = i^(popc(x & z) mod 4) (-1)^(popc(z & i))            (R3),
+ * a direct sum of 2x2 blocks.  xmask = zmask = 0 is the global phase e^{i phi} (R5).
+ * Rotations are grouped into HBM passes (same-x runs, fused tiles) and, for
+ * world > 1, rotations whose xmask touches the top m qubits run after a pairwise half-vector
+ * exchange with rank r xor gx (Eq. (1)); z-only support on the top qubits
+ * becomes a per-rank sign.  The result equals the sequential product up to fp
+ * rounding.  PS_EINVAL on NULL arrays with count > 0 or a non-finite angle; PS_ERANGE on a mask
+ * bit >= n. */
+int ps_apply_rotations(ps_handle h, const uint64_t *xmask, const uint64_t *zmask,
+                       const double *angle, size_t count);
+
+/* out = sum_i |a_i|^2 over all ranks, fp64 accumulation.  Blocks. */
+int ps_norm(ps_handle h, double *out);
+
+/* out = sum_l coeff[l] * Re <psi|P_l|psi> over all ranks (P:560-566 H = sum h_l P_l),
+ * fp64 accumulation; terms sharing an xmask share one read pass.  Blocks. */
+int ps_expectation(ps_handle h, const uint64_t *xmask, const uint64_t *zmask,
+                   const double *coeff, size_t count, double *out);
+
+/* out[0] + i out[1] = <a|b> = sum_i conj(a_i) b_i (the overlap behind Z_m).
+ * a and b must have equal n, dtype and world.  Blocks. */
+int ps_inner(ps_handle a, ps_handle b, double *out_re_im);
+
+int ps_synchronize(ps_handle h);
+
+int ps_get_stats(ps_handle h, ps_stats *out);
+int ps_reset_stats(ps_handle h);
+
+const char *ps_status_string(int code);
+const char *ps_last_error(void);
+
+/* ------------------------------------------------------------------------------------------ */
+/* Host-only helpers (no GPU needed)                                                           */
+
+/* Pauli word (letters I, X, Y, Z; leftmost = P_1 = qubit 0; length 1..64) -> masks.
+ * "XIY" -> (5, 4).  PS_EINVAL on an empty word, a bad letter or length > 64. */
+int ps_pauli_encode(const char *word, uint64_t *xmask, uint64_t *zmask);
+
+/* Batch form: codes[l*n + q] in {0=I, 1=X, 2=Y, 3=Z} for qubit q of string l. */
+int ps_pauli_encode_codes(const uint8_t *codes, int n, size_t count, uint64_t *xmask,
+                          uint64_t *zmask);
+
+/* Standard gate -> Pauli rotations under the paper's exp(+i phi P) convention (R1), universality
+ * P:12.  gate: "H","S","T","X","Y","Z","RX","RY","RZ","CNOT"/"CX","CZ","SWAP",
+ * "CPHASE","RZZ" (case-insensitive); qubits[0] = control / first qubit; params: angle for
+ * RX/RY/RZ/CPHASE/RZZ.  The global phase is emitted as an identity-string rotation (x = z = 0), so
+ * the product of the emitted rotations equals the gate matrix exactly (up to rounding).
+ * Writes *n_out rotations (<= cap; 7 suffices) in application order.  PS_EINVAL on an unknown
+ * gate or bad qubits, PS_ERANGE if cap is too small. */
+int ps_gate_to_rotations(const char *gate, const int *qubits, int n_qubits_gate,
+                         const double *params, int n_params, uint64_t *xmask, uint64_t *zmask,
+                         double *angle, size_t cap, size_t *n_out);
+
+/* Planner dump (host only; for tests and plan inspection).  Plans `count` rotations for an
+ * n-qubit state on `world` GPUs as seen by `rank`, with the given fusion level and tile bits,
+ * and writes up to cap ops.  Each op is one HBM pass or one exchange; for a pass, the
+ * rotations it applies are given in PHYSICAL local coordinates. */
+typedef struct ps_plan_op {
+    int32_t kind;        /* PS_K_STREAM, PS_K_TILE, PS_K_COSET or PS_K_EXCHANGE */
+    int32_t first_rot;   /* index of the first input rotation covered */
+    int32_t n_rot;       /* input rotations covered */
+    int32_t exch_bit;    /* EXCHANGE: local pivot bit l swapped with the partner */
+    uint64_t exch_gx;    /* EXCHANGE: partner = rank xor exch_gx */
+    uint32_t tile_bits;  /* TILE/COSET: log2 tile size */
+    uint32_t pad;
+} ps_plan_op;
+
+/* Physical rotation record as executed (one per rotation per pass, in order). */
+typedef struct ps_plan_rot {
+    uint64_t x;   /* physical local xor mask */
+    uint64_t z;   /* physical local phase mask */
+    int32_t y;    /* i^y factor of the ORIGINAL string, popc(x & z) mod 4 of the logical masks */
+    int32_t sign; /* +1/-1: per-rank sign folded into sin(phi) */
+    double angle; /* phi */
+} ps_plan_rot;
+
+int ps_plan_describe(int n_qubits, int world, int rank, int fusion, int tile_bits,
+                     const uint64_t *xmask, const uint64_t *zmask, const double *angle,
+                     size_t count, ps_plan_op *ops, size_t ops_cap, size_t *n_ops,
+                     ps_plan_rot *rots, size_t rots_cap, size_t *n_rots);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PS_H */

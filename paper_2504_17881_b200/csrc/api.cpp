@@ -1,0 +1,846 @@
+// api.cpp -- the C ABI of libps (include/ps.h): handles, device memory, streams, NCCL, and the
+// execution of plans produced by planner.cpp.  Argument marshalling and orchestration only;
+// every step of the path runs in the kernels of kernels.cu (or NCCL for exchanges).
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "ps_internal.h"
+
+namespace ps {
+
+// kernels.cu
+int kernel_max_red_blocks();
+cudaError_t launch_stream(int dtype, void* a, int nl, const Pass& p, const DevRot* d_rots, int vec256,
+                          cudaStream_t s);
+cudaError_t launch_tile(int dtype, void* a, int nl, const Pass& p, const DevRot* d_rots, const uint64_t* d_offs,
+                        cudaStream_t s);
+cudaError_t launch_full_update(int dtype, void* a, const void* stage, uint64_t base, uint64_t count, uint64_t pbase,
+                               const DevRot* rec, cudaStream_t s);
+cudaError_t launch_norm(int dtype, const void* a, uint64_t n, double* d_partial, double* d_out, cudaStream_t s);
+cudaError_t launch_inner(int dtype, const void* a, const void* b, uint64_t n, double* d_partial, double* d_out,
+                         cudaStream_t s);
+cudaError_t launch_expect(int dtype, const void* a, uint64_t n, uint64_t x0, const DevTerm* terms, int nt,
+                          double* d_partial, double* d_out_slot, cudaStream_t s);
+cudaError_t launch_init_random(int dtype, void* a, uint64_t n, uint64_t seed, uint64_t goff, cudaStream_t s);
+cudaError_t launch_set_one(int dtype, void* a, uint64_t idx, cudaStream_t s);
+cudaError_t launch_scale(int dtype, void* a, uint64_t n, double f, cudaStream_t s);
+
+static thread_local std::string g_last_error;
+void set_last_error(const std::string& msg) { g_last_error = msg; }
+
+}  // namespace ps
+
+using namespace ps;
+
+struct PendingTiming {
+    int kind;
+    cudaEvent_t e0, e1;
+};
+
+struct ps_state {
+    int n = 0, nl = 0, rank = 0, world = 1, dtype = PS_C128;
+    size_t amp_bytes = 16;
+    int device = 0;
+    void* d_state = nullptr;
+    bool own_state = false;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    bool poisoned = false;
+    // per-call plan buffers
+    DevRot* d_rots = nullptr;
+    size_t d_rots_cap = 0;
+    uint64_t* d_offs = nullptr;
+    size_t d_offs_cap = 0;
+    void* h_stage[2] = {nullptr, nullptr};
+    size_t h_stage_cap[2] = {0, 0};
+    cudaEvent_t h_stage_ev[2] = {nullptr, nullptr};
+    int stage_flip = 0;
+    // reductions
+    double* d_partial = nullptr;
+    double* d_result = nullptr;  // 64 doubles
+    double* h_result = nullptr;  // pinned, 64 doubles
+    DevTerm* d_terms = nullptr;
+    size_t d_terms_cap = 0;
+    // multi-GPU
+    ncclComm_t comm = nullptr;
+    void* d_xstage[2] = {nullptr, nullptr};
+    size_t xstage_bytes = 0;
+    size_t chunk_bytes = 256ull << 20;
+    // options
+    int profile = 0, fusion = 2, tile_bits = 12, vec256 = 1, max_pass_rots = 1 << 30;
+    ps_stats stats{};
+    std::vector<PendingTiming> pending;
+    std::vector<cudaEvent_t> event_pool;
+    Plan plan;  // reused
+};
+
+// ------------------------------------------------------------------------------------------
+// error helpers
+
+static int fail(int code, const std::string& msg) {
+    set_last_error(msg);
+    return code;
+}
+
+#define CUDA_TRY(h, expr)                                                                          \
+    do {                                                                                           \
+        cudaError_t _e = (expr);                                                                   \
+        if (_e != cudaSuccess) {                                                                   \
+            if ((h) && _e != cudaErrorMemoryAllocation && _e != cudaErrorInvalidValue)             \
+                (h)->poisoned = true;                                                              \
+            return fail(_e == cudaErrorMemoryAllocation ? PS_ENOMEM : PS_ECUDA,                    \
+                        std::string(#expr) + ": " + cudaGetErrorString(_e));                       \
+        }                                                                                          \
+    } while (0)
+
+#define NCCL_TRY(h, expr)                                                                          \
+    do {                                                                                           \
+        ncclResult_t _r = (expr);                                                                  \
+        if (_r != ncclSuccess) {                                                                   \
+            if (h) (h)->poisoned = true;                                                           \
+            return fail(PS_ENCCL, std::string(#expr) + ": " + ncclGetErrorString(_r));             \
+        }                                                                                          \
+    } while (0)
+
+#define CHECK_HANDLE(h)                                                                            \
+    do {                                                                                           \
+        if (!(h)) return fail(PS_EINVAL, "NULL handle");                                           \
+        if ((h)->poisoned) return fail(PS_ESTATE, "handle poisoned by an earlier fault");          \
+        cudaSetDevice((h)->device);                                                                \
+    } while (0)
+
+static cudaEvent_t get_event(ps_state* h) {
+    if (!h->event_pool.empty()) {
+        cudaEvent_t e = h->event_pool.back();
+        h->event_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+}
+
+struct Timed {
+    ps_state* h;
+    int kind;
+    cudaEvent_t e0 = nullptr;
+    Timed(ps_state* hh, int k) : h(hh), kind(k) {
+        if (h->profile) {
+            e0 = get_event(h);
+            cudaEventRecord(e0, h->stream);
+        }
+    }
+    ~Timed() {
+        if (h->profile && e0) {
+            cudaEvent_t e1 = get_event(h);
+            cudaEventRecord(e1, h->stream);
+            h->pending.push_back({kind, e0, e1});
+        }
+    }
+};
+
+static void drain_timings(ps_state* h) {
+    for (auto& p : h->pending) {
+        float ms = 0.f;
+        if (cudaEventSynchronize(p.e1) == cudaSuccess && cudaEventElapsedTime(&ms, p.e0, p.e1) == cudaSuccess)
+            h->stats.kernel_ms[p.kind] += ms;
+        h->event_pool.push_back(p.e0);
+        h->event_pool.push_back(p.e1);
+    }
+    h->pending.clear();
+}
+
+template <typename T>
+static int ensure_dev(ps_state* h, T** buf, size_t* cap, size_t need) {
+    if (need <= *cap) return PS_OK;
+    size_t ncap = std::max(need, *cap * 2);
+    if (*buf) CUDA_TRY(h, cudaFreeAsync(*buf, h->stream));
+    *buf = nullptr;
+    CUDA_TRY(h, cudaMallocAsync((void**)buf, ncap * sizeof(T), h->stream));
+    *cap = ncap;
+    return PS_OK;
+}
+
+// ------------------------------------------------------------------------------------------
+// lifetime
+
+extern "C" int ps_get_unique_id(void* out) {
+    if (!out) return fail(PS_EINVAL, "NULL out");
+    ncclUniqueId id;
+    ncclResult_t r = ncclGetUniqueId(&id);
+    if (r != ncclSuccess) return fail(PS_ENCCL, std::string("ncclGetUniqueId: ") + ncclGetErrorString(r));
+    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+    std::memcpy(out, &id, 128);
+    return PS_OK;
+}
+
+static void free_state(ps_state* h) {
+    if (!h) return;
+    cudaSetDevice(h->device);
+    if (h->stream) cudaStreamSynchronize(h->stream);
+    drain_timings(h);
+    for (auto e : h->event_pool) cudaEventDestroy(e);
+    if (h->comm) ncclCommDestroy(h->comm);
+    for (int t = 0; t < 2; ++t) {
+        if (h->d_xstage[t]) cudaFree(h->d_xstage[t]);
+        if (h->h_stage[t]) cudaFreeHost(h->h_stage[t]);
+        if (h->h_stage_ev[t]) cudaEventDestroy(h->h_stage_ev[t]);
+    }
+    if (h->d_rots) cudaFree(h->d_rots);
+    if (h->d_offs) cudaFree(h->d_offs);
+    if (h->d_terms) cudaFree(h->d_terms);
+    if (h->d_partial) cudaFree(h->d_partial);
+    if (h->d_result) cudaFree(h->d_result);
+    if (h->h_result) cudaFreeHost(h->h_result);
+    if (h->own_state && h->d_state) cudaFree(h->d_state);
+    if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
+    delete h;
+}
+
+extern "C" int ps_init_basis(ps_handle h, uint64_t index);
+
+extern "C" int ps_create_ex(int n_qubits, int dtype, void* dev_buf, size_t bytes, void* stream, int rank,
+                            int world, const void* nccl_id, ps_handle* out) {
+    if (!out) return fail(PS_EINVAL, "NULL out");
+    *out = nullptr;
+    if (dtype != PS_C128 && dtype != PS_C64) return fail(PS_EINVAL, "dtype must be PS_C128 or PS_C64");
+    if (world < 1 || (world & (world - 1))) return fail(PS_EINVAL, "world must be a power of two");
+    if (rank < 0 || rank >= world) return fail(PS_EINVAL, "rank out of range");
+    const int m = __builtin_ctz((unsigned)world);
+    if (n_qubits < 1 || n_qubits > 62) return fail(PS_EINVAL, "n_qubits must be in [1, 62]");
+    if (n_qubits - m < 1) return fail(PS_EINVAL, "need at least one local qubit (n - log2(world) >= 1)");
+    if (world > 1 && !nccl_id) return fail(PS_EINVAL, "world > 1 needs an NCCL unique id");
+    ps_state* h = new ps_state();
+    h->n = n_qubits;
+    h->nl = n_qubits - m;
+    h->rank = rank;
+    h->world = world;
+    h->dtype = dtype;
+    h->amp_bytes = dtype == PS_C128 ? 16 : 8;
+    h->tile_bits = dtype == PS_C128 ? 12 : 13;
+    cudaError_t e = cudaGetDevice(&h->device);
+    if (e != cudaSuccess) {
+        delete h;
+        return fail(PS_ECUDA, std::string("cudaGetDevice: ") + cudaGetErrorString(e));
+    }
+    const size_t need = h->amp_bytes << h->nl;
+    int rc = PS_OK;
+    auto bail = [&](int code, const std::string& msg) {
+        free_state(h);
+        return fail(code, msg);
+    };
+    if (stream) {
+        h->stream = (cudaStream_t)stream;
+    } else {
+        e = cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking);
+        if (e != cudaSuccess) return bail(PS_ECUDA, std::string("cudaStreamCreate: ") + cudaGetErrorString(e));
+        h->own_stream = true;
+    }
+    if (dev_buf) {
+        if (bytes < need) return bail(PS_EINVAL, "dev_buf smaller than the local slice");
+        if (((uintptr_t)dev_buf) & 255) return bail(PS_EINVAL, "dev_buf must be 256-byte aligned");
+        h->d_state = dev_buf;
+    } else {
+        e = cudaMalloc(&h->d_state, need);
+        if (e != cudaSuccess) return bail(PS_ENOMEM, std::string("cudaMalloc state: ") + cudaGetErrorString(e));
+        h->own_state = true;
+    }
+    const int nred = kernel_max_red_blocks();
+    if ((e = cudaMalloc(&h->d_partial, sizeof(double) * 2 * (size_t)nred)) != cudaSuccess ||
+        (e = cudaMalloc(&h->d_result, sizeof(double) * 64)) != cudaSuccess ||
+        (e = cudaMallocHost(&h->h_result, sizeof(double) * 64)) != cudaSuccess)
+        return bail(PS_ENOMEM, std::string("scratch: ") + cudaGetErrorString(e));
+    for (int t = 0; t < 2; ++t) {
+        if ((e = cudaEventCreateWithFlags(&h->h_stage_ev[t], cudaEventDisableTiming)) != cudaSuccess)
+            return bail(PS_ECUDA, std::string("event: ") + cudaGetErrorString(e));
+    }
+    if (world > 1) {
+        ncclUniqueId id;
+        std::memcpy(&id, nccl_id, 128);
+        ncclResult_t r = ncclCommInitRank(&h->comm, world, id, rank);
+        if (r != ncclSuccess) return bail(PS_ENCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
+    }
+    rc = ps_init_basis(h, 0);
+    if (rc) {
+        std::string msg = ps_last_error();
+        free_state(h);
+        return fail(rc, msg);
+    }
+    *out = h;
+    return PS_OK;
+}
+
+extern "C" int ps_create_dist(int n_qubits, int dtype, int rank, int world, const void* nccl_id, ps_handle* out) {
+    return ps_create_ex(n_qubits, dtype, nullptr, 0, nullptr, rank, world, nccl_id, out);
+}
+
+extern "C" int ps_create(int n_qubits, int dtype, ps_handle* out) {
+    return ps_create_ex(n_qubits, dtype, nullptr, 0, nullptr, 0, 1, nullptr, out);
+}
+
+extern "C" int ps_destroy(ps_handle h) {
+    if (!h) return fail(PS_EINVAL, "NULL handle");
+    free_state(h);
+    return PS_OK;
+}
+
+extern "C" int ps_info(ps_handle h, int* n_qubits, int* n_local, int* rank, int* world, int* dtype, void** dev_ptr) {
+    if (!h) return fail(PS_EINVAL, "NULL handle");
+    if (n_qubits) *n_qubits = h->n;
+    if (n_local) *n_local = h->nl;
+    if (rank) *rank = h->rank;
+    if (world) *world = h->world;
+    if (dtype) *dtype = h->dtype;
+    if (dev_ptr) *dev_ptr = h->d_state;
+    return PS_OK;
+}
+
+extern "C" int ps_set_option(ps_handle h, int option, int64_t value) {
+    if (!h) return fail(PS_EINVAL, "NULL handle");
+    switch (option) {
+    case PS_OPT_PROFILE: h->profile = value ? 1 : 0; break;
+    case PS_OPT_FUSION:
+        if (value < 0 || value > 2) return fail(PS_EINVAL, "fusion must be 0, 1 or 2");
+        h->fusion = (int)value;
+        break;
+    case PS_OPT_TILE_BITS: {
+        const int maxb = h->dtype == PS_C128 ? 13 : 14;  // <= 128 KiB of shared memory per tile
+        if (value < 1 || value > maxb) return fail(PS_EINVAL, "tile bits out of range");
+        h->tile_bits = (int)value;
+        break;
+    }
+    case PS_OPT_CHUNK_BYTES:
+        if (value < 4096 || (value & (value - 1))) return fail(PS_EINVAL, "chunk bytes must be a power of two >= 4096");
+        h->chunk_bytes = (size_t)value;
+        break;
+    case PS_OPT_MAX_PASS_ROTS:
+        if (value < 1) return fail(PS_EINVAL, "max pass rotations must be >= 1");
+        h->max_pass_rots = (int)std::min<int64_t>(value, 1 << 30);
+        break;
+    case PS_OPT_VEC256: h->vec256 = value ? 1 : 0; break;
+    default: return fail(PS_EINVAL, "unknown option");
+    }
+    return PS_OK;
+}
+
+// ------------------------------------------------------------------------------------------
+// init / access
+
+static uint64_t local_amps(const ps_state* h) { return 1ull << h->nl; }
+
+extern "C" int ps_init_basis(ps_handle h, uint64_t index) {
+    CHECK_HANDLE(h);
+    if (h->n < 64 && index >> h->n) return fail(PS_ERANGE, "basis index >= 2^n");
+    Timed t(h, PS_K_INIT);
+    CUDA_TRY(h, cudaMemsetAsync(h->d_state, 0, h->amp_bytes * local_amps(h), h->stream));
+    if ((index >> h->nl) == (uint64_t)h->rank) CUDA_TRY(h, launch_set_one(h->dtype, h->d_state, index & (local_amps(h) - 1), h->stream));
+    h->stats.launches[PS_K_INIT] += 1;
+    return PS_OK;
+}
+
+extern "C" int ps_init_random(ps_handle h, uint64_t seed) {
+    CHECK_HANDLE(h);
+    Timed t(h, PS_K_INIT);
+    CUDA_TRY(h, launch_init_random(h->dtype, h->d_state, local_amps(h), seed, (uint64_t)h->rank << h->nl, h->stream));
+    h->stats.launches[PS_K_INIT] += 1;
+    return PS_OK;
+}
+
+static int reduce_norm(ps_state* h, double* out);
+
+extern "C" int ps_normalize(ps_handle h) {
+    CHECK_HANDLE(h);
+    double nrm = 0.0;
+    int rc = reduce_norm(h, &nrm);
+    if (rc) return rc;
+    if (!(nrm > 0.0)) return fail(PS_EINVAL, "cannot normalise a zero state");
+    Timed t(h, PS_K_INIT);
+    CUDA_TRY(h, launch_scale(h->dtype, h->d_state, local_amps(h), 1.0 / std::sqrt(nrm), h->stream));
+    return PS_OK;
+}
+
+static int check_range(const ps_state* h, uint64_t first, uint64_t count) {
+    if (h->n < 64) {
+        const uint64_t dim = 1ull << h->n;
+        if (first > dim || count > dim - first) return fail(PS_ERANGE, "index range beyond 2^n");
+    }
+    return PS_OK;
+}
+
+extern "C" int ps_set_state(ps_handle h, uint64_t first, uint64_t count, const void* amps) {
+    CHECK_HANDLE(h);
+    if (count && !amps) return fail(PS_EINVAL, "NULL amps with count > 0");
+    int rc = check_range(h, first, count);
+    if (rc) return rc;
+    const uint64_t lo = (uint64_t)h->rank << h->nl, hi = lo + local_amps(h);
+    const uint64_t a = std::max(lo, first), b = std::min(hi, first + count);
+    if (a < b) {
+        CUDA_TRY(h, cudaMemcpyAsync((char*)h->d_state + (a - lo) * h->amp_bytes,
+                                    (const char*)amps + (a - first) * h->amp_bytes, (b - a) * h->amp_bytes,
+                                    cudaMemcpyHostToDevice, h->stream));
+        CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+    }
+    return PS_OK;
+}
+
+static int ensure_xstage(ps_state* h, size_t bytes) {
+    if (h->xstage_bytes >= bytes) return PS_OK;
+    CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+    for (int t = 0; t < 2; ++t) {
+        if (h->d_xstage[t]) cudaFree(h->d_xstage[t]);
+        h->d_xstage[t] = nullptr;
+    }
+    h->xstage_bytes = 0;
+    for (int t = 0; t < 2; ++t) CUDA_TRY(h, cudaMalloc(&h->d_xstage[t], bytes));
+    h->xstage_bytes = bytes;
+    return PS_OK;
+}
+
+extern "C" int ps_get_amplitudes(ps_handle h, uint64_t first, uint64_t count, void* amps_out) {
+    CHECK_HANDLE(h);
+    if (count && !amps_out) return fail(PS_EINVAL, "NULL amps_out with count > 0");
+    int rc = check_range(h, first, count);
+    if (rc) return rc;
+    if (h->world == 1) {
+        if (count)
+            CUDA_TRY(h, cudaMemcpyAsync(amps_out, (const char*)h->d_state + first * h->amp_bytes, count * h->amp_bytes,
+                                        cudaMemcpyDeviceToHost, h->stream));
+        CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+        return PS_OK;
+    }
+    // world > 1: pieces broadcast from their owners (collective; all ranks pass the same range)
+    const size_t piece_amps = std::max<size_t>(1, h->chunk_bytes / h->amp_bytes);
+    rc = ensure_xstage(h, piece_amps * h->amp_bytes);
+    if (rc) return rc;
+    uint64_t done = 0;
+    while (done < count) {
+        const uint64_t g = first + done;
+        const int owner = (int)(g >> h->nl);
+        const uint64_t owner_end = ((uint64_t)owner + 1) << h->nl;
+        const uint64_t len = std::min<uint64_t>({count - done, piece_amps, owner_end - g});
+        if (owner == h->rank)
+            CUDA_TRY(h, cudaMemcpyAsync(h->d_xstage[0], (const char*)h->d_state + (g & (local_amps(h) - 1)) * h->amp_bytes,
+                                        len * h->amp_bytes, cudaMemcpyDeviceToDevice, h->stream));
+        NCCL_TRY(h, ncclBroadcast(h->d_xstage[0], h->d_xstage[0], len * h->amp_bytes, ncclChar, owner, h->comm, h->stream));
+        CUDA_TRY(h, cudaMemcpyAsync((char*)amps_out + done * h->amp_bytes, h->d_xstage[0], len * h->amp_bytes,
+                                    cudaMemcpyDeviceToHost, h->stream));
+        CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+        done += len;
+    }
+    return PS_OK;
+}
+
+// ------------------------------------------------------------------------------------------
+// exchanges (K3): half-vector swap of slots with bit ell == 1-keep with partner rank^gx
+
+static int exchange_half(ps_state* h, const Pass& p) {
+    const int partner = h->rank ^ (int)p.gx;
+    const size_t s = h->amp_bytes;
+    const uint64_t rows = 1ull << (h->nl - 1 - p.ell);
+    const size_t row_bytes = s << p.ell;
+    const size_t start = (size_t)(1 - p.keep) * row_bytes;
+    const size_t chunk = h->chunk_bytes;
+    int rc = ensure_xstage(h, std::min(chunk, row_bytes * rows));
+    if (rc) return rc;
+    char* base = (char*)h->d_state;
+    if (row_bytes >= chunk) {
+        for (uint64_t r = 0; r < rows; ++r) {
+            for (size_t off = 0; off < row_bytes; off += chunk) {
+                char* reg = base + start + r * 2 * row_bytes + off;
+                const size_t len = std::min(chunk, row_bytes - off);
+                CUDA_TRY(h, cudaMemcpyAsync(h->d_xstage[0], reg, len, cudaMemcpyDeviceToDevice, h->stream));
+                NCCL_TRY(h, ncclGroupStart());
+                NCCL_TRY(h, ncclSend(h->d_xstage[0], len, ncclChar, partner, h->comm, h->stream));
+                NCCL_TRY(h, ncclRecv(reg, len, ncclChar, partner, h->comm, h->stream));
+                NCCL_TRY(h, ncclGroupEnd());
+                h->stats.nvlink_bytes += (double)len;
+            }
+        }
+    } else {
+        const uint64_t rows_per = std::max<uint64_t>(1, chunk / row_bytes);
+        for (uint64_t r0 = 0; r0 < rows; r0 += rows_per) {
+            const uint64_t nr = std::min(rows_per, rows - r0);
+            char* reg = base + start + r0 * 2 * row_bytes;
+            CUDA_TRY(h, cudaMemcpy2DAsync(h->d_xstage[0], row_bytes, reg, 2 * row_bytes, row_bytes, nr,
+                                          cudaMemcpyDeviceToDevice, h->stream));
+            NCCL_TRY(h, ncclGroupStart());
+            NCCL_TRY(h, ncclSend(h->d_xstage[0], nr * row_bytes, ncclChar, partner, h->comm, h->stream));
+            NCCL_TRY(h, ncclRecv(h->d_xstage[1], nr * row_bytes, ncclChar, partner, h->comm, h->stream));
+            NCCL_TRY(h, ncclGroupEnd());
+            CUDA_TRY(h, cudaMemcpy2DAsync(reg, 2 * row_bytes, h->d_xstage[1], row_bytes, row_bytes, nr,
+                                          cudaMemcpyDeviceToDevice, h->stream));
+            h->stats.nvlink_bytes += (double)(nr * row_bytes);
+        }
+    }
+    h->stats.exchanges += 1;
+    h->stats.algo_bytes[PS_K_EXCHANGE] += (double)(rows * row_bytes) * 2.0;
+    return PS_OK;
+}
+
+// single-rotation full exchange (no free pivot): chunk pairs {t, t^delta}
+static int exchange_full(ps_state* h, const Pass& p, const DevRot* d_rec, const DevRot& rec) {
+    const int partner = h->rank ^ (int)p.gx;
+    const size_t s = h->amp_bytes;
+    const uint64_t N = local_amps(h);
+    uint64_t C = std::max<uint64_t>(1, h->chunk_bytes / s);
+    if (C > N) C = N;
+    // C must be a power of two
+    C = 1ull << highest_bit(C);
+    const uint64_t xl = rec.x;
+    const uint64_t delta = xl / C;
+    int rc = ensure_xstage(h, 2 * C * s);
+    if (rc) return rc;
+    char* st = (char*)h->d_xstage[0];
+    char* base = (char*)h->d_state;
+    const uint64_t nchunks = N / C;
+    for (uint64_t t = 0; t < nchunks; ++t) {
+        const uint64_t u = t ^ delta;
+        if (u < t) continue;
+        NCCL_TRY(h, ncclGroupStart());
+        NCCL_TRY(h, ncclSend(base + t * C * s, C * s, ncclChar, partner, h->comm, h->stream));
+        if (u != t) NCCL_TRY(h, ncclSend(base + u * C * s, C * s, ncclChar, partner, h->comm, h->stream));
+        NCCL_TRY(h, ncclRecv(st, C * s, ncclChar, partner, h->comm, h->stream));
+        if (u != t) NCCL_TRY(h, ncclRecv(st + C * s, C * s, ncclChar, partner, h->comm, h->stream));
+        NCCL_TRY(h, ncclGroupEnd());
+        // st holds partner chunk t, st + C*s partner chunk u
+        // own chunk t needs partner elements i^xl in chunk u; own chunk u needs partner chunk t
+        const char* pu = (u != t) ? st + C * s : st;
+        CUDA_TRY(h, launch_full_update(h->dtype, h->d_state, pu, t * C, C, u * C, d_rec, h->stream));
+        if (u != t) CUDA_TRY(h, launch_full_update(h->dtype, h->d_state, st, u * C, C, t * C, d_rec, h->stream));
+        h->stats.nvlink_bytes += (double)(C * s * (u != t ? 2 : 1));
+    }
+    h->stats.exchanges += 1;
+    h->stats.rotations_by[PS_K_EXCHANGE] += 1;
+    h->stats.algo_bytes[PS_K_EXCHANGE] += (double)(N * s) * 3.0;
+    return PS_OK;
+}
+
+// ------------------------------------------------------------------------------------------
+// the hot path
+
+static int upload_plan(ps_state* h, const Plan& plan) {
+    const size_t rb = plan.rots.size() * sizeof(DevRot);
+    const size_t ob = plan.offsets.size() * sizeof(uint64_t);
+    const size_t total = rb + ob;
+    if (total == 0) return PS_OK;
+    int rc = ensure_dev(h, &h->d_rots, &h->d_rots_cap, std::max<size_t>(plan.rots.size(), 1));
+    if (rc) return rc;
+    rc = ensure_dev(h, &h->d_offs, &h->d_offs_cap, std::max<size_t>(plan.offsets.size(), 1));
+    if (rc) return rc;
+    const int b = h->stage_flip;
+    h->stage_flip ^= 1;
+    CUDA_TRY(h, cudaEventSynchronize(h->h_stage_ev[b]));
+    if (h->h_stage_cap[b] < total) {
+        if (h->h_stage[b]) CUDA_TRY(h, cudaFreeHost(h->h_stage[b]));
+        h->h_stage[b] = nullptr;
+        const size_t cap = std::max(total, 2 * h->h_stage_cap[b]);
+        CUDA_TRY(h, cudaMallocHost(&h->h_stage[b], cap));
+        h->h_stage_cap[b] = cap;
+    }
+    char* hs = (char*)h->h_stage[b];
+    if (rb) std::memcpy(hs, plan.rots.data(), rb);
+    if (ob) std::memcpy(hs + rb, plan.offsets.data(), ob);
+    if (rb) CUDA_TRY(h, cudaMemcpyAsync(h->d_rots, hs, rb, cudaMemcpyHostToDevice, h->stream));
+    if (ob) CUDA_TRY(h, cudaMemcpyAsync(h->d_offs, hs + rb, ob, cudaMemcpyHostToDevice, h->stream));
+    CUDA_TRY(h, cudaEventRecord(h->h_stage_ev[b], h->stream));
+    return PS_OK;
+}
+
+static PlanConfig plan_config(const ps_state* h) {
+    PlanConfig cfg;
+    cfg.n = h->n;
+    cfg.n_local = h->nl;
+    cfg.world = h->world;
+    cfg.rank = h->rank;
+    cfg.fusion = h->fusion;
+    cfg.tile_bits = h->tile_bits;
+    cfg.min_chunk_bits = h->dtype == PS_C128 ? 4 : 5;  // >= 256-byte gathered chunks
+    cfg.max_pass_rots = h->max_pass_rots;
+    return cfg;
+}
+
+extern "C" int ps_apply_rotations(ps_handle h, const uint64_t* xmask, const uint64_t* zmask, const double* angle,
+                                  size_t count) {
+    CHECK_HANDLE(h);
+    std::string err;
+    int rc = validate_rotations(h->n, xmask, zmask, angle, count, &err);
+    if (rc) return fail(rc, "ps_apply_rotations: " + err);
+    if (count == 0) return PS_OK;
+    Plan& plan = h->plan;
+    make_plan(plan_config(h), xmask, zmask, angle, count, &plan);
+    rc = upload_plan(h, plan);
+    if (rc) return rc;
+    const double pass_bytes = 2.0 * (double)h->amp_bytes * (double)local_amps(h);
+    for (const Pass& p : plan.passes) {
+        switch (p.kind) {
+        case PASS_STREAM: {
+            Timed t(h, PS_K_STREAM);
+            CUDA_TRY(h, launch_stream(h->dtype, h->d_state, h->nl, p, h->d_rots, h->vec256, h->stream));
+            break;
+        }
+        case PASS_TILE:
+        case PASS_COSET: {
+            Timed t(h, p.kind);
+            CUDA_TRY(h, launch_tile(h->dtype, h->d_state, h->nl, p, h->d_rots, h->d_offs, h->stream));
+            break;
+        }
+        case PASS_EXCHANGE: {
+            Timed t(h, PS_K_EXCHANGE);
+            if (p.full)
+                rc = exchange_full(h, p, h->d_rots + p.rot_begin, plan.rots[p.rot_begin]);
+            else
+                rc = exchange_half(h, p);
+            if (rc) return rc;
+            h->stats.launches[PS_K_EXCHANGE] += 1;
+            continue;
+        }
+        default:
+            return fail(PS_EINVAL, "internal: unknown pass kind");
+        }
+        h->stats.launches[p.kind] += 1;
+        h->stats.rotations_by[p.kind] += (uint64_t)p.rot_count;
+        h->stats.algo_bytes[p.kind] += pass_bytes;
+        h->stats.passes += 1;
+    }
+    h->stats.rotations += count;
+    return PS_OK;
+}
+
+// ------------------------------------------------------------------------------------------
+// reductions
+
+static int allreduce_result(ps_state* h, int nvals) {
+    if (h->world > 1)
+        NCCL_TRY(h, ncclAllReduce(h->d_result, h->d_result, (size_t)nvals, ncclDouble, ncclSum, h->comm, h->stream));
+    CUDA_TRY(h, cudaMemcpyAsync(h->h_result, h->d_result, sizeof(double) * nvals, cudaMemcpyDeviceToHost, h->stream));
+    CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+    return PS_OK;
+}
+
+static int reduce_norm(ps_state* h, double* out) {
+    {
+        Timed t(h, PS_K_REDUCE);
+        CUDA_TRY(h, launch_norm(h->dtype, h->d_state, local_amps(h), h->d_partial, h->d_result, h->stream));
+        h->stats.launches[PS_K_REDUCE] += 1;
+        h->stats.algo_bytes[PS_K_REDUCE] += (double)h->amp_bytes * (double)local_amps(h);
+    }
+    int rc = allreduce_result(h, 1);
+    if (rc) return rc;
+    *out = h->h_result[0];
+    return PS_OK;
+}
+
+extern "C" int ps_norm(ps_handle h, double* out) {
+    CHECK_HANDLE(h);
+    if (!out) return fail(PS_EINVAL, "NULL out");
+    return reduce_norm(h, out);
+}
+
+extern "C" int ps_inner(ps_handle a, ps_handle b, double* out) {
+    CHECK_HANDLE(a);
+    CHECK_HANDLE(b);
+    if (!out) return fail(PS_EINVAL, "NULL out");
+    if (a->n != b->n || a->dtype != b->dtype || a->world != b->world || a->rank != b->rank || a->device != b->device)
+        return fail(PS_EINVAL, "ps_inner: handles differ in n, dtype, world, rank or device");
+    if (b->stream != a->stream) {
+        CUDA_TRY(b, cudaStreamSynchronize(b->stream));
+    }
+    {
+        Timed t(a, PS_K_REDUCE);
+        CUDA_TRY(a, launch_inner(a->dtype, a->d_state, b->d_state, local_amps(a), a->d_partial, a->d_result, a->stream));
+        a->stats.launches[PS_K_REDUCE] += 1;
+        a->stats.algo_bytes[PS_K_REDUCE] += 2.0 * (double)a->amp_bytes * (double)local_amps(a);
+    }
+    int rc = allreduce_result(a, 2);
+    if (rc) return rc;
+    out[0] = a->h_result[0];
+    out[1] = a->h_result[1];
+    return PS_OK;
+}
+
+// expectation: terms grouped by physical x; global-X terms evaluated after a half exchange
+extern "C" int ps_expectation(ps_handle h, const uint64_t* xmask, const uint64_t* zmask, const double* coeff,
+                              size_t count, double* out) {
+    CHECK_HANDLE(h);
+    if (!out) return fail(PS_EINVAL, "NULL out");
+    std::string err;
+    int rc = validate_rotations(h->n, xmask, zmask, coeff, count, &err);
+    if (rc) return fail(rc, "ps_expectation: " + err);
+    *out = 0.0;
+    if (count == 0) return PS_OK;
+    const int nl = h->nl;
+    const uint64_t lmask = (1ull << nl) - 1;
+    const uint64_t rank = (uint64_t)h->rank;
+    // segments: gx -> list of term indices (gx = 0 first), order of first appearance
+    std::vector<uint64_t> gorder;
+    std::map<uint64_t, std::vector<size_t>> bygx;
+    for (size_t l = 0; l < count; ++l) {
+        const uint64_t gx = xmask[l] >> nl;
+        if (!bygx.count(gx)) gorder.push_back(gx);
+        bygx[gx].push_back(l);
+    }
+    std::stable_sort(gorder.begin(), gorder.end(), [](uint64_t a, uint64_t b) { return (a == 0) > (b == 0); });
+    double total = 0.0;
+    const uint64_t N = local_amps(h);
+    for (uint64_t gx : gorder) {
+        std::vector<size_t> idx = bygx[gx];
+        // split into sub-groups whose local x-parts leave a free pivot (always true for gx == 0)
+        size_t pos = 0;
+        while (pos < idx.size()) {
+            size_t end = pos;
+            uint64_t U = 0;
+            if (gx == 0) {
+                end = idx.size();
+            } else {
+                while (end < idx.size() && (U | (xmask[idx[end]] & lmask)) != lmask) U |= xmask[idx[end++]] & lmask;
+                if (end == pos) return fail(PS_EUNSUPPORTED, "ps_expectation: global-X term without a free local pivot");
+            }
+            int ell = 0, keep = 0;
+            if (gx) {
+                ell = highest_bit(lmask & ~U);
+                keep = (int)((rank >> __builtin_ctzll(gx)) & 1);
+            }
+            // physical terms grouped by physical x
+            std::map<uint64_t, std::vector<DevTerm>> byx;
+            std::vector<uint64_t> xorder;
+            for (size_t q = pos; q < end; ++q) {
+                const size_t l = idx[q];
+                const uint64_t xh = xmask[l] >> nl, xl = xmask[l] & lmask, zh = zmask[l] >> nl, zl = zmask[l] & lmask;
+                uint64_t xp = xl, zp = zl;
+                int sgn = __builtin_parityll(zh & rank);
+                if (gx) {
+                    const int kappa = __builtin_parityll(zh & gx) ^ (int)((zl >> ell) & 1);
+                    xp = xl ^ (xh ? (1ull << ell) : 0);
+                    zp = zl ^ (kappa ? (1ull << ell) : 0);
+                    sgn ^= keep & kappa;
+                }
+                const int y = __builtin_popcountll(xmask[l] & zmask[l]) & 3;
+                // Re(i^y sigma t): y=0 -> tr, 1 -> -ti, 2 -> -tr, 3 -> ti ; pairs counted twice (i and j)
+                const double w = (xp ? 2.0 : 1.0) * coeff[l] * (sgn ? -1.0 : 1.0);
+                DevTerm t;
+                t.z = zp;
+                t.kr = (y == 0) ? w : (y == 2 ? -w : 0.0);
+                t.ki = (y == 1) ? -w : (y == 3 ? w : 0.0);
+                if (!byx.count(xp)) xorder.push_back(xp);
+                byx[xp].push_back(t);
+            }
+            if (gx) {
+                Pass ex;
+                ex.kind = PASS_EXCHANGE;
+                ex.gx = gx;
+                ex.ell = ell;
+                ex.keep = keep;
+                Timed t(h, PS_K_EXCHANGE);
+                rc = exchange_half(h, ex);
+                if (rc) return rc;
+            }
+            size_t nterms = 0;
+            for (auto& kv : byx) nterms += kv.second.size();
+            rc = ensure_dev(h, &h->d_terms, &h->d_terms_cap, nterms);
+            if (rc) return rc;
+            std::vector<DevTerm> flat;
+            flat.reserve(nterms);
+            std::vector<std::pair<size_t, size_t>> ranges;
+            for (uint64_t xp : xorder) {
+                ranges.push_back({flat.size(), byx[xp].size()});
+                flat.insert(flat.end(), byx[xp].begin(), byx[xp].end());
+            }
+            CUDA_TRY(h, cudaMemcpyAsync(h->d_terms, flat.data(), flat.size() * sizeof(DevTerm), cudaMemcpyHostToDevice,
+                                        h->stream));
+            const size_t ng = xorder.size();
+            for (size_t gi = 0; gi < ng; gi += 64) {
+                const size_t nb = std::min<size_t>(64, ng - gi);
+                for (size_t q = 0; q < nb; ++q) {
+                    Timed t(h, PS_K_REDUCE);
+                    CUDA_TRY(h, launch_expect(h->dtype, h->d_state, N, xorder[gi + q], h->d_terms + ranges[gi + q].first,
+                                              (int)ranges[gi + q].second, h->d_partial, h->d_result + q, h->stream));
+                    h->stats.launches[PS_K_REDUCE] += 1;
+                    h->stats.algo_bytes[PS_K_REDUCE] += (double)h->amp_bytes * (double)N;
+                }
+                if (h->world > 1)
+                    NCCL_TRY(h, ncclAllReduce(h->d_result, h->d_result, nb, ncclDouble, ncclSum, h->comm, h->stream));
+                CUDA_TRY(h, cudaMemcpyAsync(h->h_result, h->d_result, sizeof(double) * nb, cudaMemcpyDeviceToHost, h->stream));
+                CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+                for (size_t q = 0; q < nb; ++q) total += h->h_result[q];
+            }
+            if (gx) {
+                Pass ex;
+                ex.kind = PASS_EXCHANGE;
+                ex.gx = gx;
+                ex.ell = ell;
+                ex.keep = keep;
+                Timed t(h, PS_K_EXCHANGE);
+                rc = exchange_half(h, ex);
+                if (rc) return rc;
+            }
+            pos = end;
+        }
+    }
+    *out = total;
+    return PS_OK;
+}
+
+// ------------------------------------------------------------------------------------------
+
+extern "C" int ps_synchronize(ps_handle h) {
+    CHECK_HANDLE(h);
+    CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+    if (h->comm) {
+        ncclResult_t async_err = ncclSuccess;
+        ncclCommGetAsyncError(h->comm, &async_err);
+        if (async_err != ncclSuccess) {
+            h->poisoned = true;
+            return fail(PS_ENCCL, std::string("NCCL async error: ") + ncclGetErrorString(async_err));
+        }
+    }
+    drain_timings(h);
+    return PS_OK;
+}
+
+extern "C" int ps_get_stats(ps_handle h, ps_stats* out) {
+    if (!h || !out) return fail(PS_EINVAL, "NULL argument");
+    if (!h->poisoned) {
+        cudaSetDevice(h->device);
+        if (!h->pending.empty()) {
+            cudaStreamSynchronize(h->stream);
+            drain_timings(h);
+        }
+    }
+    *out = h->stats;
+    return PS_OK;
+}
+
+extern "C" int ps_reset_stats(ps_handle h) {
+    if (!h) return fail(PS_EINVAL, "NULL handle");
+    if (!h->poisoned) {
+        cudaSetDevice(h->device);
+        cudaStreamSynchronize(h->stream);
+        drain_timings(h);
+    }
+    std::memset(&h->stats, 0, sizeof(h->stats));
+    return PS_OK;
+}
+
+extern "C" const char* ps_status_string(int code) {
+    switch (code) {
+    case PS_OK: return "PS_OK";
+    case PS_EINVAL: return "PS_EINVAL: invalid argument";
+    case PS_ERANGE: return "PS_ERANGE: mask bit or index out of range";
+    case PS_ENOMEM: return "PS_ENOMEM: allocation failed";
+    case PS_ECUDA: return "PS_ECUDA: CUDA error";
+    case PS_ENCCL: return "PS_ENCCL: NCCL error";
+    case PS_ESTATE: return "PS_ESTATE: handle poisoned by an earlier fault";
+    case PS_EUNSUPPORTED: return "PS_EUNSUPPORTED: unsupported request";
+    default: return "unknown status";
+    }
+}
+
+extern "C" const char* ps_last_error(void) { return g_last_error.c_str(); }

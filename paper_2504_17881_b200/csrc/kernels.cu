@@ -1,0 +1,708 @@
+// kernels.cu -- sm_100a kernels of libps (all HBM-bound; no contraction, no tensor cores).
+//
+//   K1 k_stream     streaming pair-rotation pass: one rotation or a same-x run applied to each
+//                   pair {i, i xor x} in registers, 256-bit LDG/STG, pair indices by bit
+//                   insertion (P:96-101 direct sum of 2x2 blocks; P:119-121 AND/XOR/parity)
+//   K2/K7 k_tile    fused tile pass: a 2^k-amplitude tile (contiguous for K2, a gathered coset
+//                   i0 xor span{v_t} of contiguous chunks for K7) is staged in shared memory by
+//                   TMA bulk copies (cp.async.bulk + mbarrier), every rotation of the pass is
+//                   applied there, and the tile is written back by TMA bulk stores
+//                   (several rotations per traversal of the array)
+//   K5 k_norm/k_expect/k_inner   fp64-accumulating reductions
+//   K6 k_init_*     seeded counter-based init, basis states
+//   K3 k_full_update  single-rotation full-exchange update against a partner chunk
+//
+// Every kernel applies the SAME per-pair arithmetic (rot_pair / rot_diag below, explicit
+// round-to-nearest intrinsics, no contraction freedom) so fused and unfused passes, and 1-GPU
+// and G-GPU runs, are bitwise identical.
+#include <cuda_runtime.h>
+#include <cstdint>
+
+#include "ps_internal.h"
+
+namespace ps {
+namespace {
+
+// ------------------------------------------------------------------------------------------
+// per-pair arithmetic (DevRot in ps_internal.h):
+//   a'_i = c a_i + s*A a_j, A = (-br, bi);   a'_j = c a_j + s*B a_i, B = (br, bi);  s = +-1
+
+__device__ __forceinline__ void rot_pair(double& ir, double& ii, double& jr, double& ji, double c,
+                                         double br, double bi) {
+    const double ur = __fma_rn(-br, jr, __dmul_rn(-bi, ji));
+    const double ui = __fma_rn(-br, ji, __dmul_rn(bi, jr));
+    const double vr = __fma_rn(br, ir, __dmul_rn(-bi, ii));
+    const double vi = __fma_rn(br, ii, __dmul_rn(bi, ir));
+    const double nir = __fma_rn(c, ir, ur);
+    const double nii = __fma_rn(c, ii, ui);
+    const double njr = __fma_rn(c, jr, vr);
+    const double nji = __fma_rn(c, ji, vi);
+    ir = nir; ii = nii; jr = njr; ji = nji;
+}
+
+__device__ __forceinline__ void rot_pair(float& ir, float& ii, float& jr, float& ji, float c,
+                                         float br, float bi) {
+    const float ur = __fmaf_rn(-br, jr, __fmul_rn(-bi, ji));
+    const float ui = __fmaf_rn(-br, ji, __fmul_rn(bi, jr));
+    const float vr = __fmaf_rn(br, ir, __fmul_rn(-bi, ii));
+    const float vi = __fmaf_rn(br, ii, __fmul_rn(bi, ir));
+    const float nir = __fmaf_rn(c, ir, ur);
+    const float nii = __fmaf_rn(c, ii, ui);
+    const float njr = __fmaf_rn(c, jr, vr);
+    const float nji = __fmaf_rn(c, ji, vi);
+    ir = nir; ii = nii; jr = njr; ji = nji;
+}
+
+__device__ __forceinline__ void rot_diag(double& r, double& i, double c, double br, double bi) {
+    const double ur = __fma_rn(-br, r, __dmul_rn(-bi, i));
+    const double ui = __fma_rn(-br, i, __dmul_rn(bi, r));
+    r = __fma_rn(c, r, ur);
+    i = __fma_rn(c, i, ui);
+}
+
+__device__ __forceinline__ void rot_diag(float& r, float& i, float c, float br, float bi) {
+    const float ur = __fmaf_rn(-br, r, __fmul_rn(-bi, i));
+    const float ui = __fmaf_rn(-br, i, __fmul_rn(bi, r));
+    r = __fmaf_rn(c, r, ur);
+    i = __fmaf_rn(c, i, ui);
+}
+
+template <typename T>
+struct Coef {
+    T c, br, bi;
+};
+
+template <typename T>
+__device__ __forceinline__ Coef<T> load_coef(const DevRot* __restrict__ r) {
+    Coef<T> k;
+    k.c = (T)__ldg(&r->c);
+    k.br = (T)__ldg(&r->br);
+    k.bi = (T)__ldg(&r->bi);
+    return k;
+}
+
+template <typename T>
+__device__ __forceinline__ T flip(T v, int neg) {
+    return neg ? -v : v;
+}
+
+__device__ __forceinline__ int par64(uint64_t v) { return __popcll(v) & 1; }
+
+__device__ __forceinline__ uint64_t insert0(uint64_t t, int p) {
+    const uint64_t lo = t & ((1ull << p) - 1);
+    return ((t >> p) << (p + 1)) | lo;
+}
+
+// ------------------------------------------------------------------------------------------
+// vector global memory access: V amplitudes of type T per access (32 B = 256-bit when V*2*sizeof(T) == 32)
+
+template <typename T, int V>
+struct Vec {
+    T r[V], i[V];
+};
+
+template <typename T, int V>
+__device__ __forceinline__ void ld_vec(const T* p, Vec<T, V>& v);
+template <typename T, int V>
+__device__ __forceinline__ void st_vec(T* p, const Vec<T, V>& v);
+
+template <>
+__device__ __forceinline__ void ld_vec<double, 1>(const double* p, Vec<double, 1>& v) {
+    asm volatile("ld.global.L1::no_allocate.v2.f64 {%0,%1}, [%2];" : "=d"(v.r[0]), "=d"(v.i[0]) : "l"(p));
+}
+template <>
+__device__ __forceinline__ void st_vec<double, 1>(double* p, const Vec<double, 1>& v) {
+    asm volatile("st.global.v2.f64 [%0], {%1,%2};" ::"l"(p), "d"(v.r[0]), "d"(v.i[0]) : "memory");
+}
+template <>
+__device__ __forceinline__ void ld_vec<double, 2>(const double* p, Vec<double, 2>& v) {
+    asm volatile("ld.global.L1::no_allocate.v4.f64 {%0,%1,%2,%3}, [%4];"
+                 : "=d"(v.r[0]), "=d"(v.i[0]), "=d"(v.r[1]), "=d"(v.i[1])
+                 : "l"(p));
+}
+template <>
+__device__ __forceinline__ void st_vec<double, 2>(double* p, const Vec<double, 2>& v) {
+    asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(v.r[0]), "d"(v.i[0]), "d"(v.r[1]),
+                 "d"(v.i[1])
+                 : "memory");
+}
+template <>
+__device__ __forceinline__ void ld_vec<float, 1>(const float* p, Vec<float, 1>& v) {
+    asm volatile("ld.global.L1::no_allocate.v2.f32 {%0,%1}, [%2];" : "=f"(v.r[0]), "=f"(v.i[0]) : "l"(p));
+}
+template <>
+__device__ __forceinline__ void st_vec<float, 1>(float* p, const Vec<float, 1>& v) {
+    asm volatile("st.global.v2.f32 [%0], {%1,%2};" ::"l"(p), "f"(v.r[0]), "f"(v.i[0]) : "memory");
+}
+template <>
+__device__ __forceinline__ void ld_vec<float, 2>(const float* p, Vec<float, 2>& v) {
+    asm volatile("ld.global.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+                 : "=f"(v.r[0]), "=f"(v.i[0]), "=f"(v.r[1]), "=f"(v.i[1])
+                 : "l"(p));
+}
+template <>
+__device__ __forceinline__ void st_vec<float, 2>(float* p, const Vec<float, 2>& v) {
+    asm volatile("st.global.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(v.r[0]), "f"(v.i[0]), "f"(v.r[1]),
+                 "f"(v.i[1])
+                 : "memory");
+}
+template <>
+__device__ __forceinline__ void ld_vec<float, 4>(const float* p, Vec<float, 4>& v) {
+    asm volatile("ld.global.L1::no_allocate.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=f"(v.r[0]), "=f"(v.i[0]), "=f"(v.r[1]), "=f"(v.i[1]), "=f"(v.r[2]), "=f"(v.i[2]),
+                   "=f"(v.r[3]), "=f"(v.i[3])
+                 : "l"(p));
+}
+template <>
+__device__ __forceinline__ void st_vec<float, 4>(float* p, const Vec<float, 4>& v) {
+    asm volatile("st.global.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "f"(v.r[0]), "f"(v.i[0]),
+                 "f"(v.r[1]), "f"(v.i[1]), "f"(v.r[2]), "f"(v.i[2]), "f"(v.r[3]), "f"(v.i[3])
+                 : "memory");
+}
+
+// ------------------------------------------------------------------------------------------
+// K1: streaming pass.  mode 0: pairs across vectors (pivot >= log2 V); mode 1: pairs inside a
+// vector (x0 < V); mode 2: diagonal-only run.  One "unit" = one vector pair (mode 0) or one
+// vector (modes 1, 2).  Each thread handles UNROLL units per iteration, loads first.
+
+constexpr int kStreamThreads = 256;
+
+template <typename T, int V>
+__device__ __forceinline__ void apply_run_pair(Vec<T, V>& vi, Vec<T, V>& vj, uint64_t ibase, int xin,
+                                               uint64_t jbase, const DevRot* __restrict__ rec, int nrec) {
+    for (int r = 0; r < nrec; ++r) {
+        const uint64_t x = __ldg(&rec[r].x);
+        const uint64_t z = __ldg(&rec[r].z);
+        const Coef<T> k = load_coef<T>(&rec[r]);
+        if (x == 0) {
+#pragma unroll
+            for (int e = 0; e < V; ++e) {
+                const int si = par64(z & (ibase + e));
+                rot_diag(vi.r[e], vi.i[e], k.c, flip(k.br, si), flip(k.bi, si));
+                const int sj = par64(z & (jbase + e));
+                rot_diag(vj.r[e], vj.i[e], k.c, flip(k.br, sj), flip(k.bi, sj));
+            }
+        } else {
+#pragma unroll
+            for (int e = 0; e < V; ++e) {
+                const int s = par64(z & (ibase + e));
+                const int f = e ^ xin;
+                rot_pair(vi.r[e], vi.i[e], vj.r[f], vj.i[f], k.c, flip(k.br, s), flip(k.bi, s));
+            }
+        }
+    }
+}
+
+template <typename T, int V>
+__device__ __forceinline__ void apply_run_intra(Vec<T, V>& v, uint64_t base, int x0, int piv,
+                                                const DevRot* __restrict__ rec, int nrec) {
+    for (int r = 0; r < nrec; ++r) {
+        const uint64_t x = __ldg(&rec[r].x);
+        const uint64_t z = __ldg(&rec[r].z);
+        const Coef<T> k = load_coef<T>(&rec[r]);
+        if (x == 0) {
+#pragma unroll
+            for (int e = 0; e < V; ++e) {
+                const int s = par64(z & (base + e));
+                rot_diag(v.r[e], v.i[e], k.c, flip(k.br, s), flip(k.bi, s));
+            }
+        } else {
+#pragma unroll
+            for (int e = 0; e < V; ++e) {
+                if ((e >> piv) & 1) continue;
+                const int f = e ^ x0;
+                const int s = par64(z & (base + e));
+                rot_pair(v.r[e], v.i[e], v.r[f], v.i[f], k.c, flip(k.br, s), flip(k.bi, s));
+            }
+        }
+    }
+}
+
+template <typename T, int V, int UNROLL>
+__global__ void __launch_bounds__(kStreamThreads) k_stream(T* __restrict__ a, uint64_t units, int mode,
+                                                           int piv, uint64_t x0,
+                                                           const DevRot* __restrict__ rec, int nrec) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    const uint64_t t0 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (mode == 0) {
+        const uint64_t xv = x0 & ~(uint64_t)(V - 1);
+        const int xin = (int)(x0 & (V - 1));
+        for (uint64_t u = t0; u < units; u += stride * UNROLL) {
+            Vec<T, V> vi[UNROLL], vj[UNROLL];
+            uint64_t ib[UNROLL];
+#pragma unroll
+            for (int q = 0; q < UNROLL; ++q) {
+                const uint64_t uq = u + (uint64_t)q * stride;
+                ib[q] = insert0(uq * V, piv);
+                if (uq < units) {
+                    ld_vec<T, V>(a + 2 * ib[q], vi[q]);
+                    ld_vec<T, V>(a + 2 * (ib[q] ^ xv), vj[q]);
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < UNROLL; ++q) {
+                const uint64_t uq = u + (uint64_t)q * stride;
+                if (uq < units) apply_run_pair<T, V>(vi[q], vj[q], ib[q], xin, ib[q] ^ xv, rec, nrec);
+            }
+#pragma unroll
+            for (int q = 0; q < UNROLL; ++q) {
+                const uint64_t uq = u + (uint64_t)q * stride;
+                if (uq < units) {
+                    st_vec<T, V>(a + 2 * ib[q], vi[q]);
+                    st_vec<T, V>(a + 2 * (ib[q] ^ xv), vj[q]);
+                }
+            }
+        }
+    } else {
+        for (uint64_t u = t0; u < units; u += stride * UNROLL) {
+            Vec<T, V> v[UNROLL];
+#pragma unroll
+            for (int q = 0; q < UNROLL; ++q) {
+                const uint64_t uq = u + (uint64_t)q * stride;
+                if (uq < units) ld_vec<T, V>(a + 2 * uq * V, v[q]);
+            }
+#pragma unroll
+            for (int q = 0; q < UNROLL; ++q) {
+                const uint64_t uq = u + (uint64_t)q * stride;
+                if (uq < units) apply_run_intra<T, V>(v[q], uq * V, (int)x0, piv, rec, nrec);
+            }
+#pragma unroll
+            for (int q = 0; q < UNROLL; ++q) {
+                const uint64_t uq = u + (uint64_t)q * stride;
+                if (uq < units) st_vec<T, V>(a + 2 * uq * V, v[q]);
+            }
+        }
+    }
+}
+
+// ------------------------------------------------------------------------------------------
+// K2 / K7: tile pass through shared memory with TMA bulk copies.
+//
+// tile tau: i0 = pdep(tau, free_mask); chunk u (u < 2^h) = amplitudes [i0 ^ off[u], +2^c);
+// tile-local index l = (u << c) | w.  Rotation records are in tile-local coordinates; the
+// per-tile sign is parity(zt & i0).
+
+constexpr int kTileThreads = 512;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ uint64_t pdep64(uint64_t v, uint64_t mask) {
+    uint64_t out = 0;
+    for (uint64_t m = mask; m; m &= m - 1) {
+        const uint64_t low = m & (~m + 1);
+        if (v & 1) out |= low;
+        v >>= 1;
+    }
+    return out;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kTileThreads) k_tile(T* __restrict__ a, int cbits, int hbits,
+                                                       uint64_t free_mask,
+                                                       const uint64_t* __restrict__ offs,
+                                                       const DevRot* __restrict__ rec, int nrec) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    __shared__ __align__(8) uint64_t mbar;
+    T* tile = reinterpret_cast<T*>(smem_raw);
+    const int kbits = cbits + hbits;
+    const uint32_t tile_amps = 1u << kbits;
+    const uint32_t chunk_bytes = (2u * sizeof(T)) << cbits;
+    const uint32_t nchunks = 1u << hbits;
+    const uint64_t i0 = pdep64((uint64_t)blockIdx.x, free_mask);
+    const int tid = threadIdx.x;
+
+    if (tid == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&mbar)));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    // ---- TMA bulk loads of the 2^h chunks into smem (warp 0 issues)
+    if (tid < 32) {
+        if (tid == 0) {
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&mbar)),
+                         "r"(tile_amps * (uint32_t)(2 * sizeof(T)))
+                         : "memory");
+        }
+        __syncwarp();
+        for (uint32_t u = tid; u < nchunks; u += 32) {
+            const uint64_t g = i0 ^ __ldg(&offs[u]);
+            const T* src = a + 2 * g;
+            T* dst = tile + 2 * ((uint64_t)u << cbits);
+            asm volatile(
+                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                    smem_u32(dst)),
+                "l"(src), "r"(chunk_bytes), "r"(smem_u32(&mbar))
+                : "memory");
+        }
+    }
+    // ---- wait for the tile
+    {
+        uint32_t done = 0;
+        while (!done) {
+            asm volatile(
+                "{\n\t.reg .pred p;\n\t"
+                "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\n\t"
+                "selp.u32 %0, 1, 0, p;\n\t}"
+                : "=r"(done)
+                : "r"(smem_u32(&mbar))
+                : "memory");
+        }
+    }
+    // ---- every rotation of the pass, in order
+    for (int r = 0; r < nrec; ++r) {
+        const uint32_t X = (uint32_t)__ldg(&rec[r].x);
+        const uint32_t Z = (uint32_t)__ldg(&rec[r].z);
+        const int ts = par64(__ldg(&rec[r].zt) & i0);
+        const Coef<T> k = load_coef<T>(&rec[r]);
+        if (X == 0) {
+            for (uint32_t l = tid; l < tile_amps; l += kTileThreads) {
+                const int s = (__popc(Z & l) & 1) ^ ts;
+                T re = tile[2 * l], im = tile[2 * l + 1];
+                rot_diag(re, im, k.c, flip(k.br, s), flip(k.bi, s));
+                tile[2 * l] = re;
+                tile[2 * l + 1] = im;
+            }
+        } else {
+            const int piv = 31 - __clz(X);
+            const uint32_t lo = (1u << piv) - 1;
+            for (uint32_t p = tid; p < (tile_amps >> 1); p += kTileThreads) {
+                const uint32_t l = ((p >> piv) << (piv + 1)) | (p & lo);
+                const uint32_t m = l ^ X;
+                const int s = (__popc(Z & l) & 1) ^ ts;
+                T ir = tile[2 * l], ii = tile[2 * l + 1];
+                T jr = tile[2 * m], ji = tile[2 * m + 1];
+                rot_pair(ir, ii, jr, ji, k.c, flip(k.br, s), flip(k.bi, s));
+                tile[2 * l] = ir;
+                tile[2 * l + 1] = ii;
+                tile[2 * m] = jr;
+                tile[2 * m + 1] = ji;
+            }
+        }
+        __syncthreads();
+    }
+    // ---- TMA bulk stores back to HBM
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+    if (tid < 32) {
+        for (uint32_t u = tid; u < nchunks; u += 32) {
+            const uint64_t g = i0 ^ __ldg(&offs[u]);
+            T* dst = a + 2 * g;
+            const T* src = tile + 2 * ((uint64_t)u << cbits);
+            asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
+                         "r"(smem_u32(src)), "r"(chunk_bytes)
+                         : "memory");
+        }
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+    }
+}
+
+// ------------------------------------------------------------------------------------------
+// K3 fallback: own element i (local index base+t) updated against the partner's OLD value at
+// local index i ^ x, held in `stage` (partner chunk starting at local index pbase).
+//   a'_i = c a_i + s A b_(i^x)
+
+template <typename T>
+__global__ void k_full_update(T* __restrict__ a, const T* __restrict__ stage, uint64_t base,
+                              uint64_t count, uint64_t pbase, const DevRot* __restrict__ rec) {
+    const uint64_t x = __ldg(&rec->x);
+    const uint64_t z = __ldg(&rec->z);
+    const Coef<T> k = load_coef<T>(rec);
+    for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < count;
+         t += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t i = base + t;
+        const uint64_t j = (i ^ x) - pbase;
+        const int s = par64(z & i);
+        T ir = a[2 * i], ii = a[2 * i + 1];
+        T jr = stage[2 * j], ji = stage[2 * j + 1];
+        rot_pair(ir, ii, jr, ji, k.c, flip(k.br, s), flip(k.bi, s));
+        a[2 * i] = ir;
+        a[2 * i + 1] = ii;
+    }
+}
+
+// ------------------------------------------------------------------------------------------
+// reductions (fp64 accumulation, deterministic two-stage)
+
+constexpr int kRedThreads = 256;
+
+__device__ __forceinline__ double block_sum(double v) {
+    __shared__ double sh[kRedThreads / 32];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    if (l == 0) sh[w] = v;
+    __syncthreads();
+    double s = 0.0;
+    if (w == 0) {
+        s = (l < kRedThreads / 32) ? sh[l] : 0.0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    }
+    __syncthreads();
+    return s;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kRedThreads) k_norm(const T* __restrict__ a, uint64_t n, double* partial) {
+    double acc = 0.0;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        const double r = (double)a[2 * i], m = (double)a[2 * i + 1];
+        acc = __fma_rn(r, r, __fma_rn(m, m, acc));
+    }
+    const double s = block_sum(acc);
+    if (threadIdx.x == 0) partial[blockIdx.x] = s;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kRedThreads) k_inner(const T* __restrict__ a, const T* __restrict__ b, uint64_t n,
+                                                       double* partial) {
+    double re = 0.0, im = 0.0;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        const double ar = (double)a[2 * i], ai = (double)a[2 * i + 1];
+        const double br = (double)b[2 * i], bi = (double)b[2 * i + 1];
+        re = __fma_rn(ar, br, __fma_rn(ai, bi, re));
+        im = __fma_rn(ar, bi, __fma_rn(-ai, br, im));
+    }
+    const double s0 = block_sum(re);
+    const double s1 = block_sum(im);
+    if (threadIdx.x == 0) {
+        partial[2 * blockIdx.x] = s0;
+        partial[2 * blockIdx.x + 1] = s1;
+    }
+}
+
+// expectation over one x-group: terms[0..nt) share xor mask x0
+template <typename T>
+__global__ void __launch_bounds__(kRedThreads) k_expect(const T* __restrict__ a, uint64_t nl_amps, uint64_t x0,
+                                                        const DevTerm* __restrict__ terms, int nt,
+                                                        double* partial) {
+    double acc = 0.0;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    if (x0 == 0) {
+        for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nl_amps; i += stride) {
+            const double r = (double)a[2 * i], m = (double)a[2 * i + 1];
+            const double p = __fma_rn(r, r, __dmul_rn(m, m));
+            double w = 0.0;
+            for (int l = 0; l < nt; ++l) {
+                const double kr = __ldg(&terms[l].kr);
+                w += par64(__ldg(&terms[l].z) & i) ? -kr : kr;
+            }
+            acc = __fma_rn(w, p, acc);
+        }
+    } else {
+        const int piv = 63 - __clzll(x0);
+        for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < (nl_amps >> 1); t += stride) {
+            const uint64_t i = insert0(t, piv), j = i ^ x0;
+            const double ir = (double)a[2 * i], ii = (double)a[2 * i + 1];
+            const double jr = (double)a[2 * j], ji = (double)a[2 * j + 1];
+            // t = conj(a_j) a_i
+            const double tr = __fma_rn(jr, ir, __dmul_rn(ji, ii));
+            const double ti = __fma_rn(jr, ii, __dmul_rn(-ji, ir));
+            for (int l = 0; l < nt; ++l) {
+                const double v = __fma_rn(__ldg(&terms[l].kr), tr, __dmul_rn(__ldg(&terms[l].ki), ti));
+                acc += par64(__ldg(&terms[l].z) & i) ? -v : v;
+            }
+        }
+    }
+    const double s = block_sum(acc);
+    if (threadIdx.x == 0) partial[blockIdx.x] = s;
+}
+
+// sums partial[0..n) (stride `width`, component `comp`) in a fixed order into out[comp]
+__global__ void k_final_sum(const double* __restrict__ partial, int n, int width, int comp, double* out) {
+    double acc = 0.0;
+    for (int t = threadIdx.x; t < n; t += blockDim.x) acc += partial[(size_t)t * width + comp];
+    const double s = block_sum(acc);
+    if (threadIdx.x == 0) out[comp] = s;
+}
+
+// ------------------------------------------------------------------------------------------
+// init
+
+__device__ __forceinline__ double gen_u(uint64_t seed, uint64_t k) {
+    // splitmix64 output k+1 for state `seed`, top 53 bits -> [-1, 1)
+    uint64_t zz = seed + (k + 1) * 0x9E3779B97F4A7C15ull;
+    zz = (zz ^ (zz >> 30)) * 0xBF58476D1CE4E5B9ull;
+    zz = (zz ^ (zz >> 27)) * 0x94D049BB133111EBull;
+    zz = zz ^ (zz >> 31);
+    return (double)(zz >> 11) * (1.0 / 4503599627370496.0) - 1.0;
+}
+
+template <typename T>
+__global__ void k_init_random(T* __restrict__ a, uint64_t n, uint64_t seed, uint64_t goff) {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t g = goff + i;
+        a[2 * i] = (T)gen_u(seed, 2 * g);
+        a[2 * i + 1] = (T)gen_u(seed, 2 * g + 1);
+    }
+}
+
+template <typename T>
+__global__ void k_set_one(T* __restrict__ a, uint64_t idx) {
+    a[2 * idx] = (T)1;
+    a[2 * idx + 1] = (T)0;
+}
+
+template <typename T>
+__global__ void k_scale(T* __restrict__ a, uint64_t n, double f) {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < 2 * n; i += (uint64_t)gridDim.x * blockDim.x)
+        a[i] = (T)((double)a[i] * f);
+}
+
+int g_num_sms = 0;
+int num_sms() {
+    if (g_num_sms == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+        if (g_num_sms <= 0) g_num_sms = 148;
+    }
+    return g_num_sms;
+}
+
+template <typename T, int V>
+cudaError_t launch_stream_t(T* a, int nl, const Pass& p, const DevRot* d_rots, cudaStream_t s) {
+    const DevRot* rec = d_rots + p.rot_begin;
+    int mode, piv = 0;
+    uint64_t units;
+    const uint64_t namps = 1ull << nl;
+    if (p.x0 == 0) {
+        mode = 2;
+        units = namps / V;
+    } else {
+        piv = highest_bit(p.x0);
+        if ((1ull << piv) >= (uint64_t)V) {
+            mode = 0;
+            units = (namps >> 1) / V;
+        } else {
+            mode = 1;
+            units = namps / V;
+        }
+    }
+    constexpr int UNROLL = 2;
+    const uint64_t want = (units + (uint64_t)kStreamThreads * UNROLL - 1) / ((uint64_t)kStreamThreads * UNROLL);
+    const uint64_t cap = (uint64_t)num_sms() * 8;
+    const unsigned grid = (unsigned)(want < cap ? (want ? want : 1) : cap);
+    k_stream<T, V, UNROLL><<<grid, kStreamThreads, 0, s>>>(a, units, mode, piv, p.x0, rec, p.rot_count);
+    return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t launch_tile_t(T* a, int nl, const Pass& p, const DevRot* d_rots, const uint64_t* d_offs,
+                          cudaStream_t s) {
+    const size_t smem = (size_t)(2 * sizeof(T)) << p.kbits;
+    static bool attr_done[2] = {false, false};
+    const int which = sizeof(T) == 8 ? 0 : 1;
+    if (!attr_done[which]) {
+        cudaFuncSetAttribute(k_tile<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        attr_done[which] = true;
+    }
+    const uint64_t ntiles = 1ull << (nl - p.kbits);
+    k_tile<T><<<(unsigned)ntiles, kTileThreads, smem, s>>>(a, p.cbits, p.hbits, p.free_mask, d_offs + p.off_begin,
+                                                           d_rots + p.rot_begin, p.rot_count);
+    return cudaGetLastError();
+}
+
+unsigned red_grid(uint64_t n) {
+    const uint64_t want = (n + kRedThreads - 1) / kRedThreads;
+    const uint64_t cap = (uint64_t)num_sms() * 4;
+    return (unsigned)(want < cap ? (want ? want : 1) : cap);
+}
+
+}  // namespace
+
+// ==========================================================================================
+// launchers (host)
+
+int kernel_max_red_blocks() { return num_sms() * 4; }
+
+cudaError_t launch_stream(int dtype, void* a, int nl, const Pass& p, const DevRot* d_rots, int vec256,
+                          cudaStream_t s) {
+    if (dtype == PS_C128) {
+        if (vec256 && nl >= 2) return launch_stream_t<double, 2>((double*)a, nl, p, d_rots, s);
+        return launch_stream_t<double, 1>((double*)a, nl, p, d_rots, s);
+    }
+    if (vec256 && nl >= 3) return launch_stream_t<float, 4>((float*)a, nl, p, d_rots, s);
+    if (nl >= 2) return launch_stream_t<float, 2>((float*)a, nl, p, d_rots, s);
+    return launch_stream_t<float, 1>((float*)a, nl, p, d_rots, s);
+}
+
+cudaError_t launch_tile(int dtype, void* a, int nl, const Pass& p, const DevRot* d_rots, const uint64_t* d_offs,
+                        cudaStream_t s) {
+    if (dtype == PS_C128) return launch_tile_t<double>((double*)a, nl, p, d_rots, d_offs, s);
+    return launch_tile_t<float>((float*)a, nl, p, d_rots, d_offs, s);
+}
+
+cudaError_t launch_full_update(int dtype, void* a, const void* stage, uint64_t base, uint64_t count, uint64_t pbase,
+                               const DevRot* rec, cudaStream_t s) {
+    const unsigned grid = red_grid(count);
+    if (dtype == PS_C128)
+        k_full_update<double><<<grid, kRedThreads, 0, s>>>((double*)a, (const double*)stage, base, count, pbase, rec);
+    else
+        k_full_update<float><<<grid, kRedThreads, 0, s>>>((float*)a, (const float*)stage, base, count, pbase, rec);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_norm(int dtype, const void* a, uint64_t n, double* d_partial, double* d_out, cudaStream_t s) {
+    const unsigned grid = red_grid(n);
+    if (dtype == PS_C128)
+        k_norm<double><<<grid, kRedThreads, 0, s>>>((const double*)a, n, d_partial);
+    else
+        k_norm<float><<<grid, kRedThreads, 0, s>>>((const float*)a, n, d_partial);
+    k_final_sum<<<1, kRedThreads, 0, s>>>(d_partial, (int)grid, 1, 0, d_out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_inner(int dtype, const void* a, const void* b, uint64_t n, double* d_partial, double* d_out,
+                         cudaStream_t s) {
+    const unsigned grid = red_grid(n);
+    if (dtype == PS_C128)
+        k_inner<double><<<grid, kRedThreads, 0, s>>>((const double*)a, (const double*)b, n, d_partial);
+    else
+        k_inner<float><<<grid, kRedThreads, 0, s>>>((const float*)a, (const float*)b, n, d_partial);
+    k_final_sum<<<1, kRedThreads, 0, s>>>(d_partial, (int)grid, 2, 0, d_out);
+    k_final_sum<<<1, kRedThreads, 0, s>>>(d_partial, (int)grid, 2, 1, d_out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_expect(int dtype, const void* a, uint64_t n, uint64_t x0, const DevTerm* terms, int nt,
+                          double* d_partial, double* d_out_slot, cudaStream_t s) {
+    const unsigned grid = red_grid(x0 ? n / 2 : n);
+    if (dtype == PS_C128)
+        k_expect<double><<<grid, kRedThreads, 0, s>>>((const double*)a, n, x0, terms, nt, d_partial);
+    else
+        k_expect<float><<<grid, kRedThreads, 0, s>>>((const float*)a, n, x0, terms, nt, d_partial);
+    k_final_sum<<<1, kRedThreads, 0, s>>>(d_partial, (int)grid, 1, 0, d_out_slot);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_init_random(int dtype, void* a, uint64_t n, uint64_t seed, uint64_t goff, cudaStream_t s) {
+    const unsigned grid = red_grid(n) * 2;
+    if (dtype == PS_C128)
+        k_init_random<double><<<grid, kRedThreads, 0, s>>>((double*)a, n, seed, goff);
+    else
+        k_init_random<float><<<grid, kRedThreads, 0, s>>>((float*)a, n, seed, goff);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_set_one(int dtype, void* a, uint64_t idx, cudaStream_t s) {
+    if (dtype == PS_C128)
+        k_set_one<double><<<1, 1, 0, s>>>((double*)a, idx);
+    else
+        k_set_one<float><<<1, 1, 0, s>>>((float*)a, idx);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_scale(int dtype, void* a, uint64_t n, double f, cudaStream_t s) {
+    const unsigned grid = red_grid(n) * 2;
+    if (dtype == PS_C128)
+        k_scale<double><<<grid, kRedThreads, 0, s>>>((double*)a, n, f);
+    else
+        k_scale<float><<<grid, kRedThreads, 0, s>>>((float*)a, n, f);
+    return cudaGetLastError();
+}
+
+}  // namespace ps

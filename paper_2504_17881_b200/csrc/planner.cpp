@@ -1,0 +1,607 @@
+// planner.cpp -- host side of the hot path: Pauli-string encoder, gate converter and the
+// order-preserving planner that turns a rotation list into HBM passes and exchanges.
+//
+//   encoder     P:116-121, P:476-484 (two 64-bit masks; worked example XIY -> (5, 4))
+//   converter   P:12, P:37-38 (1- and 2-qubit rotations are universal); R1 sign
+//   planner     P:126-148 Eq. (1) (one exchange per run sharing the upper-qubit X-part),
+//               P:357-430 (partitioned layout, pairwise exchange k <-> k xor q1),
+//               P:403-404 (diagonal upper part: no exchange), P:494-499 (several rotations
+//               per traversal of the array).  The planner never reorders rotations.
+#include <algorithm>
+#include <cctype>
+#include <cmath>
+#include <cstring>
+#include <string>
+
+#include "ps_internal.h"
+
+namespace ps {
+
+int popc64(uint64_t v) { return __builtin_popcountll(v); }
+int highest_bit(uint64_t v) { return v ? 63 - __builtin_clzll(v) : -1; }
+static inline int parity64(uint64_t v) { return __builtin_parityll(v); }
+
+int validate_rotations(int n, const uint64_t* x, const uint64_t* z, const double* angle,
+                       size_t count, std::string* err) {
+    if (count == 0) return PS_OK;
+    if (!x || !z || !angle) {
+        *err = "NULL rotation array with count > 0";
+        return PS_EINVAL;
+    }
+    const uint64_t lim = (n >= 64) ? ~0ull : ((1ull << n) - 1);
+    for (size_t l = 0; l < count; ++l) {
+        if (!std::isfinite(angle[l])) {
+            *err = "non-finite angle at index " + std::to_string(l);
+            return PS_EINVAL;
+        }
+        if ((x[l] & ~lim) || (z[l] & ~lim)) {
+            *err = "mask bit >= n at index " + std::to_string(l);
+            return PS_ERANGE;
+        }
+    }
+    return PS_OK;
+}
+
+// ------------------------------------------------------------------------------------------
+// record construction
+
+// B = sign * sin(phi) * i^(y+1)   (see DevRot)
+static DevRot make_rec(uint64_t x, uint64_t z, uint64_t zt, int y, int sign, double phi) {
+    DevRot r{};
+    r.x = x;
+    r.z = z;
+    r.zt = zt;
+    const double c = std::cos(phi);
+    const double s = std::sin(phi) * (double)sign;
+    switch ((y + 1) & 3) {
+    case 0: r.br = s; r.bi = 0.0; break;
+    case 1: r.br = 0.0; r.bi = s; break;
+    case 2: r.br = -s; r.bi = 0.0; break;
+    default: r.br = 0.0; r.bi = -s; break;
+    }
+    r.c = c;
+    r.pad = 0;
+    return r;
+}
+
+// one rotation in physical local coordinates, before pass formation
+struct PhysRot {
+    uint64_t x, z;
+    int y;       // popc(x & z) mod 4 of the logical string
+    int sign;    // +1 / -1
+    double phi;
+    int input;   // input index
+};
+
+// ------------------------------------------------------------------------------------------
+// GF(2) basis in reduced row-echelon form keyed by the highest set bit (pivot)
+
+struct Basis {
+    std::vector<uint64_t> v;  // each v[t] has a distinct pivot; pivots cleared in all others
+    uint64_t pivots = 0;
+    uint64_t reduce(uint64_t a) const {
+        for (uint64_t b : v) {
+            int p = highest_bit(b);
+            if ((a >> p) & 1) a ^= b;
+        }
+        return a;
+    }
+    // adds a (already reduced, non-zero); keeps RREF
+    void add(uint64_t a) {
+        int p = highest_bit(a);
+        for (auto& b : v)
+            if ((b >> p) & 1) b ^= a;
+        v.push_back(a);
+        pivots |= 1ull << p;
+    }
+    int dim() const { return (int)v.size(); }
+};
+
+// ------------------------------------------------------------------------------------------
+// pass formation over one segment of local physical rotations (no exchange inside)
+
+static void emit_stream(const std::vector<PhysRot>& seg, size_t b, size_t e, Plan* plan) {
+    Pass p;
+    p.kind = PASS_STREAM;
+    p.rot_begin = (int)plan->rots.size();
+    p.first_input = seg[b].input;
+    p.n_input = seg[e - 1].input - seg[b].input + 1;
+    uint64_t x0 = 0;
+    for (size_t t = b; t < e; ++t) {
+        if (seg[t].x) x0 = seg[t].x;
+        plan->rots.push_back(make_rec(seg[t].x, seg[t].z, 0, seg[t].y, seg[t].sign, seg[t].phi));
+    }
+    p.x0 = x0;
+    p.rot_count = (int)(e - b);
+    plan->passes.push_back(p);
+}
+
+static void emit_tile(const std::vector<PhysRot>& seg, size_t b, size_t e, const PlanConfig& cfg,
+                      const Basis& hb, int chunk_min, Plan* plan) {
+    const int nl = cfg.n_local;
+    const int k = std::min(cfg.tile_bits, nl);
+    const uint64_t lmask = (nl >= 64) ? ~0ull : ((1ull << nl) - 1);
+    // all x inside the low k bits -> contiguous tile (K2)
+    uint64_t xor_all = 0;
+    for (size_t t = b; t < e; ++t) xor_all |= seg[t].x;
+    Pass p;
+    p.rot_begin = (int)plan->rots.size();
+    p.first_input = seg[b].input;
+    p.n_input = seg[e - 1].input - seg[b].input + 1;
+    p.rot_count = (int)(e - b);
+    if ((xor_all >> k) == 0) {
+        p.kind = PASS_TILE;
+        p.kbits = k;
+        p.cbits = k;
+        p.hbits = 0;
+        p.free_mask = lmask & ~((1ull << k) - 1);
+        p.off_begin = (int)plan->offsets.size();
+        plan->offsets.push_back(0);
+        const uint64_t kmask = (1ull << k) - 1;
+        for (size_t t = b; t < e; ++t)
+            plan->rots.push_back(make_rec(seg[t].x, seg[t].z & kmask, seg[t].z & p.free_mask,
+                                          seg[t].y, seg[t].sign, seg[t].phi));
+        plan->passes.push_back(p);
+        return;
+    }
+    // coset tile: grow the contiguous chunk while the tile dimension stays <= k
+    int c = chunk_min;
+    auto reduced_dim = [&](int cb) {
+        Basis r;
+        const uint64_t hi = ~((1ull << cb) - 1);
+        for (uint64_t v : hb.v) {
+            uint64_t a = r.reduce(v & hi);
+            if (a) r.add(a);
+        }
+        return r;
+    };
+    Basis vb = reduced_dim(c);
+    while (c + 1 <= k) {
+        Basis nb = reduced_dim(c + 1);
+        if (c + 1 + nb.dim() > k) break;
+        c += 1;
+        vb = nb;
+    }
+    p.kind = PASS_COSET;
+    p.cbits = c;
+    p.hbits = vb.dim();
+    p.kbits = c + vb.dim();
+    const uint64_t cmask = (1ull << c) - 1;
+    p.free_mask = lmask & ~cmask & ~vb.pivots;
+    // order basis vectors by pivot so tile-local bit t <-> t-th smallest pivot
+    std::vector<uint64_t> vs = vb.v;
+    std::sort(vs.begin(), vs.end(), [](uint64_t a, uint64_t bb) { return highest_bit(a) < highest_bit(bb); });
+    p.off_begin = (int)plan->offsets.size();
+    for (uint64_t u = 0; u < (1ull << p.hbits); ++u) {
+        uint64_t o = 0;
+        for (int t = 0; t < p.hbits; ++t)
+            if ((u >> t) & 1) o ^= vs[t];
+        plan->offsets.push_back(o);
+    }
+    for (size_t t = b; t < e; ++t) {
+        const uint64_t x = seg[t].x, z = seg[t].z;
+        const uint64_t xh = x & ~cmask;
+        uint64_t coef = 0, zc = 0, chk = 0;
+        for (int q = 0; q < p.hbits; ++q) {
+            const int piv = highest_bit(vs[q]);
+            if ((xh >> piv) & 1) {
+                coef |= 1ull << q;
+                chk ^= vs[q];
+            }
+            if (parity64(z & vs[q])) zc |= 1ull << q;
+        }
+        (void)chk;  // chk == xh by construction (x lies in the tile space)
+        const uint64_t xl = (coef << c) | (x & cmask);
+        const uint64_t zl = (zc << c) | (z & cmask);
+        plan->rots.push_back(make_rec(xl, zl, z & p.free_mask, seg[t].y, seg[t].sign, seg[t].phi));
+    }
+    plan->passes.push_back(p);
+}
+
+static void form_passes(const std::vector<PhysRot>& seg, const PlanConfig& cfg, Plan* plan) {
+    if (seg.empty()) return;
+    const int nl = cfg.n_local;
+    if (cfg.fusion <= 0) {
+        for (size_t t = 0; t < seg.size(); ++t) emit_stream(seg, t, t + 1, plan);
+        return;
+    }
+    if (cfg.fusion == 1) {
+        size_t b = 0;
+        uint64_t x0 = 0;
+        for (size_t t = 0; t < seg.size(); ++t) {
+            const uint64_t x = seg[t].x;
+            if (x == 0 || x0 == 0 || x == x0) {
+                if (x) x0 = x;
+                continue;
+            }
+            emit_stream(seg, b, t, plan);
+            b = t;
+            x0 = x;
+        }
+        emit_stream(seg, b, seg.size(), plan);
+        return;
+    }
+    // fusion 2: greedy tile spaces (order preserving)
+    const int k = std::min(cfg.tile_bits, nl);
+    const int chunk_min = std::min(cfg.min_chunk_bits, k);
+    const uint64_t low = (1ull << chunk_min) - 1;
+    size_t b = 0;
+    Basis hb;
+    uint64_t x0 = 0;
+    bool same_x = true;
+    int nrot = 0;
+    auto close = [&](size_t e) {
+        if (e <= b) return;
+        if (same_x)
+            emit_stream(seg, b, e, plan);
+        else
+            emit_tile(seg, b, e, cfg, hb, chunk_min, plan);
+    };
+    for (size_t t = 0; t < seg.size(); ++t) {
+        const uint64_t x = seg[t].x;
+        const uint64_t r = hb.reduce(x & ~low);
+        const bool fits = (r == 0 || chunk_min + hb.dim() + 1 <= k) && nrot < cfg.max_pass_rots;
+        if (!fits) {
+            close(t);
+            b = t;
+            hb = Basis();
+            x0 = 0;
+            same_x = true;
+            nrot = 0;
+        }
+        const uint64_t r2 = hb.reduce(x & ~low);
+        if (r2) hb.add(r2);
+        if (x) {
+            if (x0 == 0) x0 = x;
+            else if (x != x0) same_x = false;
+        }
+        ++nrot;
+    }
+    close(seg.size());
+}
+
+// ------------------------------------------------------------------------------------------
+// full plan: layout (exchanges) then passes
+
+void make_plan(const PlanConfig& cfg, const uint64_t* x, const uint64_t* z, const double* angle,
+               size_t count, Plan* plan) {
+    plan->passes.clear();
+    plan->rots.clear();
+    plan->offsets.clear();
+    plan->debug_rots.clear();
+    plan->exchanges = 0;
+    const int nl = cfg.n_local;
+    const uint64_t lmask = (nl >= 64) ? ~0ull : ((1ull << nl) - 1);
+    const uint64_t rank = (uint64_t)cfg.rank;
+    std::vector<PhysRot> seg;
+
+    auto logical_y = [&](size_t l) { return popc64(x[l] & z[l]) & 3; };
+    auto push_debug = [&](const PhysRot& pr) {
+        if (cfg.want_debug) {
+            ps_plan_rot d;
+            d.x = pr.x;
+            d.z = pr.z;
+            d.y = pr.y;
+            d.sign = pr.sign;
+            d.angle = pr.phi;
+            plan->debug_rots.push_back(d);
+        }
+    };
+    auto flush = [&]() {
+        form_passes(seg, cfg, plan);
+        seg.clear();
+    };
+
+    size_t i = 0;
+    while (i < count) {
+        const uint64_t gx = x[i] >> nl;
+        if (cfg.world == 1 || gx == 0) {
+            // local rotation in the canonical layout; z on the rank bits -> per-rank sign
+            PhysRot pr;
+            pr.x = x[i] & lmask;
+            pr.z = z[i] & lmask;
+            pr.y = logical_y(i);
+            pr.sign = parity64((z[i] >> nl) & rank) ? -1 : 1;
+            pr.phi = angle[i];
+            pr.input = (int)i;
+            seg.push_back(pr);
+            push_debug(pr);
+            ++i;
+            continue;
+        }
+        // run sharing the upper X-part gx (Eq. (1)): rotations with upper X-part in
+        // {0, gx} whose local X-parts leave a free pivot bit
+        uint64_t U = 0;
+        size_t j = i, last = count;  // last = last rotation with upper part gx
+        while (j < count) {
+            const uint64_t gj = x[j] >> nl;
+            if (gj != 0 && gj != gx) break;
+            const uint64_t xl = x[j] & lmask;
+            if ((U | xl) == lmask) break;
+            U |= xl;
+            if (gj == gx) last = j;
+            ++j;
+        }
+        flush();
+        if (last == count) {
+            // no free pivot even for rotation i alone: single-rotation full exchange
+            Pass p;
+            p.kind = PASS_EXCHANGE;
+            p.full = 1;
+            p.gx = gx;
+            p.rot_begin = (int)plan->rots.size();
+            p.rot_count = 1;
+            p.first_input = (int)i;
+            p.n_input = 1;
+            PhysRot pr;
+            pr.x = x[i] & lmask;
+            pr.z = z[i] & lmask;
+            pr.y = logical_y(i);
+            pr.sign = parity64((z[i] >> nl) & rank) ? -1 : 1;
+            pr.phi = angle[i];
+            pr.input = (int)i;
+            push_debug(pr);
+            plan->rots.push_back(make_rec(pr.x, pr.z, 0, pr.y, pr.sign, pr.phi));
+            plan->passes.push_back(p);
+            plan->exchanges += 1;
+            ++i;
+            continue;
+        }
+        U = 0;
+        for (size_t t = i; t <= last; ++t) U |= x[t] & lmask;
+        const int ell = highest_bit(lmask & ~U);
+        const int g = __builtin_ctzll(gx);
+        const int keep = (int)((rank >> g) & 1);
+        Pass ex;
+        ex.kind = PASS_EXCHANGE;
+        ex.gx = gx;
+        ex.ell = ell;
+        ex.keep = keep;
+        ex.first_input = (int)i;
+        ex.n_input = (int)(last - i + 1);
+        plan->passes.push_back(ex);
+        plan->exchanges += 1;
+        const uint64_t el = 1ull << ell;
+        for (size_t t = i; t <= last; ++t) {
+            const uint64_t xh = x[t] >> nl, xl = x[t] & lmask;
+            const uint64_t zh = z[t] >> nl, zl = z[t] & lmask;
+            const int kappa = parity64(zh & gx) ^ (int)((zl >> ell) & 1);
+            PhysRot pr;
+            pr.x = xl ^ (xh ? el : 0);
+            pr.z = zl ^ (kappa ? el : 0);
+            pr.y = logical_y(t);
+            pr.sign = (parity64(zh & rank) ^ (keep & kappa)) ? -1 : 1;
+            pr.phi = angle[t];
+            pr.input = (int)t;
+            seg.push_back(pr);
+            push_debug(pr);
+        }
+        flush();
+        plan->passes.push_back(ex);  // swap back to the canonical layout
+        plan->exchanges += 1;
+        i = last + 1;
+    }
+    flush();
+}
+
+}  // namespace ps
+
+// ==========================================================================================
+// C ABI: host-only helpers
+
+using namespace ps;
+
+extern "C" int ps_pauli_encode(const char* word, uint64_t* xmask, uint64_t* zmask) {
+    if (!word || !xmask || !zmask) {
+        set_last_error("ps_pauli_encode: NULL argument");
+        return PS_EINVAL;
+    }
+    const size_t n = std::strlen(word);
+    if (n == 0 || n > 64) {
+        set_last_error("ps_pauli_encode: word length must be 1..64");
+        return PS_EINVAL;
+    }
+    uint64_t x = 0, z = 0;
+    for (size_t q = 0; q < n; ++q) {
+        const char ch = (char)std::toupper((unsigned char)word[q]);
+        const uint64_t bit = 1ull << q;  // factor q+1 -> bit q
+        switch (ch) {
+        case 'I': break;
+        case 'X': x |= bit; break;
+        case 'Y': x |= bit; z |= bit; break;
+        case 'Z': z |= bit; break;
+        default:
+            set_last_error(std::string("ps_pauli_encode: invalid letter '") + word[q] + "'");
+            return PS_EINVAL;
+        }
+    }
+    *xmask = x;
+    *zmask = z;
+    return PS_OK;
+}
+
+extern "C" int ps_pauli_encode_codes(const uint8_t* codes, int n, size_t count, uint64_t* xmask,
+                                     uint64_t* zmask) {
+    if (n < 1 || n > 64) {
+        set_last_error("ps_pauli_encode_codes: n must be 1..64");
+        return PS_EINVAL;
+    }
+    if (count && (!codes || !xmask || !zmask)) {
+        set_last_error("ps_pauli_encode_codes: NULL argument");
+        return PS_EINVAL;
+    }
+    for (size_t l = 0; l < count; ++l) {
+        uint64_t x = 0, z = 0;
+        for (int q = 0; q < n; ++q) {
+            const uint8_t c = codes[l * (size_t)n + q];
+            if (c > 3) {
+                set_last_error("ps_pauli_encode_codes: code > 3");
+                return PS_EINVAL;
+            }
+            if (c == 1 || c == 2) x |= 1ull << q;
+            if (c == 2 || c == 3) z |= 1ull << q;
+        }
+        xmask[l] = x;
+        zmask[l] = z;
+    }
+    return PS_OK;
+}
+
+// gate -> rotations (exp(+i phi P) convention, R1); application order
+extern "C" int ps_gate_to_rotations(const char* gate, const int* qubits, int nq, const double* params,
+                                    int np, uint64_t* xm, uint64_t* zm, double* ang, size_t cap,
+                                    size_t* n_out) {
+    if (!gate || !n_out || (nq > 0 && !qubits)) {
+        set_last_error("ps_gate_to_rotations: NULL argument");
+        return PS_EINVAL;
+    }
+    std::string g(gate);
+    for (auto& ch : g) ch = (char)std::toupper((unsigned char)ch);
+    if (g == "CX") g = "CNOT";
+    const double PI = 3.14159265358979323846;
+    struct R { uint64_t x, z; double a; };
+    std::vector<R> out;
+    auto need = [&](int q, int p) -> bool {
+        if (nq != q || np < p || (p > 0 && !params)) return false;
+        for (int t = 0; t < q; ++t)
+            if (qubits[t] < 0 || qubits[t] > 63) return false;
+        if (q == 2 && qubits[0] == qubits[1]) return false;
+        return true;
+    };
+    auto X1 = [&](int t) { return 1ull << qubits[t]; };
+    bool ok = true;
+    if (g == "RX" || g == "RY" || g == "RZ") {
+        ok = need(1, 1);
+        if (ok) {
+            const uint64_t b = X1(0);
+            const double a = -params[0] / 2;
+            if (g == "RX") out.push_back({b, 0, a});
+            if (g == "RY") out.push_back({b, b, a});
+            if (g == "RZ") out.push_back({0, b, a});
+        }
+    } else if (g == "X" || g == "Y" || g == "Z") {
+        ok = need(1, 0);
+        if (ok) {
+            const uint64_t b = X1(0);
+            out.push_back({g == "Z" ? 0 : b, g == "X" ? 0 : b, PI / 2});
+            out.push_back({0, 0, -PI / 2});
+        }
+    } else if (g == "S" || g == "T") {
+        ok = need(1, 0);
+        if (ok) {
+            const double a = (g == "S") ? PI / 4 : PI / 8;
+            out.push_back({0, X1(0), -a});
+            out.push_back({0, 0, a});
+        }
+    } else if (g == "H") {
+        ok = need(1, 0);
+        if (ok) {
+            const uint64_t b = X1(0);
+            out.push_back({0, b, -PI / 4});
+            out.push_back({b, 0, -PI / 4});
+            out.push_back({0, b, -PI / 4});
+            out.push_back({0, 0, PI / 2});
+        }
+    } else if (g == "CNOT" || g == "CZ" || g == "CPHASE") {
+        ok = need(2, g == "CPHASE" ? 1 : 0);
+        if (ok) {
+            const double lam = (g == "CPHASE") ? params[0] : PI;
+            const uint64_t c = X1(0), t = X1(1);
+            const double a = lam / 4;
+            out.push_back({0, c, -a});
+            if (g == "CNOT") {
+                out.push_back({t, 0, -a});
+                out.push_back({t, c, a});  // Z_c X_t
+            } else {
+                out.push_back({0, t, -a});
+                out.push_back({0, c | t, a});  // Z_c Z_t
+            }
+            out.push_back({0, 0, a});
+        }
+    } else if (g == "SWAP") {
+        ok = need(2, 0);
+        if (ok) {
+            const uint64_t b = X1(0) | X1(1);
+            out.push_back({b, 0, PI / 4});
+            out.push_back({b, b, PI / 4});
+            out.push_back({0, b, PI / 4});
+            out.push_back({0, 0, -PI / 4});
+        }
+    } else if (g == "RZZ") {
+        ok = need(2, 1);
+        if (ok) out.push_back({0, X1(0) | X1(1), -params[0] / 2});
+    } else {
+        set_last_error("ps_gate_to_rotations: unknown gate " + g);
+        return PS_EINVAL;
+    }
+    if (!ok) {
+        set_last_error("ps_gate_to_rotations: bad qubits/params for " + g);
+        return PS_EINVAL;
+    }
+    *n_out = out.size();
+    if (out.size() > cap) {
+        set_last_error("ps_gate_to_rotations: cap too small");
+        return PS_ERANGE;
+    }
+    if (!out.empty() && (!xm || !zm || !ang)) {
+        set_last_error("ps_gate_to_rotations: NULL output");
+        return PS_EINVAL;
+    }
+    for (size_t t = 0; t < out.size(); ++t) {
+        xm[t] = out[t].x;
+        zm[t] = out[t].z;
+        ang[t] = out[t].a;
+    }
+    return PS_OK;
+}
+
+extern "C" int ps_plan_describe(int n_qubits, int world, int rank, int fusion, int tile_bits,
+                                const uint64_t* xmask, const uint64_t* zmask, const double* angle,
+                                size_t count, ps_plan_op* ops, size_t ops_cap, size_t* n_ops,
+                                ps_plan_rot* rots, size_t rots_cap, size_t* n_rots) {
+    if (n_qubits < 1 || n_qubits > 62 || world < 1 || (world & (world - 1)) || rank < 0 ||
+        rank >= world) {
+        set_last_error("ps_plan_describe: bad n/world/rank");
+        return PS_EINVAL;
+    }
+    const int m = __builtin_ctz((unsigned)world);
+    if (n_qubits - m < 1) {
+        set_last_error("ps_plan_describe: world too large for n");
+        return PS_EINVAL;
+    }
+    std::string err;
+    int rc = validate_rotations(n_qubits, xmask, zmask, angle, count, &err);
+    if (rc) {
+        set_last_error(err);
+        return rc;
+    }
+    PlanConfig cfg;
+    cfg.n = n_qubits;
+    cfg.n_local = n_qubits - m;
+    cfg.world = world;
+    cfg.rank = rank;
+    cfg.fusion = fusion;
+    cfg.tile_bits = tile_bits > 0 ? tile_bits : 12;
+    cfg.want_debug = true;
+    Plan plan;
+    make_plan(cfg, xmask, zmask, angle, count, &plan);
+    if (n_ops) *n_ops = plan.passes.size();
+    if (n_rots) *n_rots = plan.debug_rots.size();
+    if (ops) {
+        for (size_t t = 0; t < plan.passes.size() && t < ops_cap; ++t) {
+            const Pass& p = plan.passes[t];
+            ps_plan_op o{};
+            o.kind = p.kind;
+            o.first_rot = p.first_input;
+            o.n_rot = (p.kind == PASS_EXCHANGE && !p.full) ? 0 : p.n_input;
+            o.exch_bit = p.full ? -1 : p.ell;
+            o.exch_gx = p.gx;
+            o.tile_bits = (uint32_t)p.kbits;
+            ops[t] = o;
+        }
+    }
+    if (rots) {
+        for (size_t t = 0; t < plan.debug_rots.size() && t < rots_cap; ++t) rots[t] = plan.debug_rots[t];
+    }
+    return PS_OK;
+}

@@ -1,0 +1,105 @@
+// ps_internal.h -- internal types shared by the planner (host C++), the C-ABI layer and the
+// CUDA kernels of libps.  Not part of the public ABI (see include/ps.h).
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/ps.h"
+
+namespace ps {
+
+// ------------------------------------------------------------------------------------------
+// Device rotation record (one per rotation per pass), 56 bytes.
+//
+// A pass applies rotations to pairs {i, i xor x} in PHYSICAL local coordinates (for K1 the
+// physical local index; for tile passes the tile-local index).  With B = sign * sin(phi) *
+// i^(y+1) (y = popc(x & z) of the ORIGINAL logical string) and
+// sigma = (-1)^(popc(z & i) [xor tile sign]) the update is (R3)
+//     a'_i = c a_i + sigma * A a_j,   A = (-br, bi)   (= i sin(phi) conj(i^y))
+//     a'_j = c a_j + sigma * B a_i,   B = ( br, bi)   (= i sin(phi) i^y)
+// where i is the member whose pivot bit (highest bit of x) is 0.  For x = 0 (diagonal) the
+// element update is a' = c a + sigma * A a.
+struct DevRot {
+    uint64_t x;   // xor mask (physical local, or tile-local for tile passes)
+    uint64_t z;   // phase mask in the same coordinates
+    uint64_t zt;  // tile passes: z restricted to the tile-enumeration bits (tile sign); else 0
+    double c;     // cos(phi)
+    double br;    // Re B
+    double bi;    // Im B
+    uint64_t pad; // keeps 8-byte fields aligned to 64 B records
+};
+static_assert(sizeof(DevRot) == 56 || sizeof(DevRot) == 64, "DevRot layout");
+
+// expectation term record: contribution sigma(i) * (kr * tr + ki * ti) per pair (x != 0) with
+// t = conj(a_j) a_i, or sigma(i) * kr * |a_i|^2 per element (x = 0)
+struct DevTerm {
+    uint64_t z;
+    double kr;
+    double ki;
+};
+
+enum PassKind : int {
+    PASS_STREAM = PS_K_STREAM,
+    PASS_TILE = PS_K_TILE,
+    PASS_COSET = PS_K_COSET,
+    PASS_EXCHANGE = PS_K_EXCHANGE,
+};
+
+constexpr int kMaxTileHigh = 10;  // at most 2^10 gathered chunks per coset tile
+
+struct Pass {
+    int kind = PASS_STREAM;
+    int rot_begin = 0;    // first record in the call's DevRot array
+    int rot_count = 0;    // records in this pass
+    int first_input = 0;  // first input rotation covered
+    int n_input = 0;      // input rotations covered
+    // STREAM
+    uint64_t x0 = 0;      // shared non-zero xor mask of the run (0: diagonal-only run)
+    // TILE / COSET: tile = i0 xor off[u] | w, w < 2^cbits, u < 2^hbits, i0 = pdep(tau, free_mask)
+    int kbits = 0;        // log2 tile amplitudes = cbits + hbits
+    int cbits = 0;        // log2 contiguous chunk amplitudes
+    int hbits = 0;        // number of gathered high basis vectors
+    uint64_t free_mask = 0;
+    int off_begin = 0;    // first entry of this pass's 2^hbits chunk offsets in the call's table
+    // EXCHANGE
+    uint64_t gx = 0;      // partner = rank xor gx
+    int ell = 0;          // local pivot bit
+    int keep = 0;         // this rank keeps slots with bit ell == keep
+    int full = 0;         // 1: single-rotation full exchange (no free pivot); rot_begin/rot_count valid
+};
+
+struct Plan {
+    std::vector<Pass> passes;
+    std::vector<DevRot> rots;
+    std::vector<uint64_t> offsets;
+    std::vector<ps_plan_rot> debug_rots;  // filled when requested (plan dump)
+    uint64_t exchanges = 0;
+};
+
+struct PlanConfig {
+    int n = 0;          // total qubits
+    int n_local = 0;    // local qubits n - m
+    int world = 1;
+    int rank = 0;
+    int fusion = 2;
+    int tile_bits = 12;
+    int min_chunk_bits = 4;     // coset tiles gather chunks of >= 2^min_chunk_bits amplitudes
+    int max_pass_rots = 1 << 30;
+    bool want_debug = false;
+};
+
+// planner.cpp
+int validate_rotations(int n, const uint64_t* x, const uint64_t* z, const double* angle,
+                       size_t count, std::string* err);
+void make_plan(const PlanConfig& cfg, const uint64_t* x, const uint64_t* z, const double* angle,
+               size_t count, Plan* plan);
+int popc64(uint64_t v);
+int highest_bit(uint64_t v);
+
+// thread-local last error
+void set_last_error(const std::string& msg);
+
+}  // namespace ps

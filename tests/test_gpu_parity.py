@@ -1,0 +1,273 @@
+"""GPU parity tests (``-m gpu``): the CUDA path, called through the C ABI, against the CPU oracle.
+
+Tolerances (BASELINE.json north_star): max |a_gpu - a_oracle| <= 1e-10 for fp64 and <= 1e-4 for
+fp32 after up to 1000 rotations, on unnormalised O(1) amplitudes (reading R10); index
+and mask handling bit-exact (basis permutations under X-only rotations at phi = pi/2, R8).
+"""
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+import workloads
+import paper_2504_17881_b200 as P
+from paper_2504_17881_b200 import ps
+
+pytestmark = pytest.mark.gpu
+
+SEED = 250417881
+TOL = {"c128": 1e-10, "c64": 1e-4}
+
+_oracle_cache: dict = {}
+
+
+def _want(n, kind, count, seed):
+    key = (n, kind, count, seed)
+    if key not in _oracle_cache:
+        codes, ang = workloads.random_layer(n, count, seed=seed, kind=kind)
+        _oracle_cache[key] = (codes, ang, oracle.apply(n, oracle.random_state(SEED, n), codes, ang))
+    return _oracle_cache[key]
+
+
+def _run(n, dtype, codes, ang, fusion=2, tile_bits=None, init="random"):
+    x, z = P.pauli_encode_codes(codes)
+    with P.State(n, dtype) as st:
+        st.set_option(ps.OPT_FUSION, fusion)
+        if tile_bits:
+            st.set_option(ps.OPT_TILE_BITS, tile_bits)
+        if init == "random":
+            st.init_random(SEED)
+        else:
+            st.init_basis(init)
+        st.apply_rotations(x, z, ang)
+        out = st.get_amplitudes()
+        stats = st.stats()
+    return out, stats
+
+
+@pytest.mark.parametrize("dtype", ["c128", "c64"])
+@pytest.mark.parametrize("fusion", [0, 1, 2])
+def test_config1(dtype, fusion):
+    """BASELINE config 1: 10 qubits, 200 random rotations of weight 1-10."""
+    codes, ang, want = _want(10, "R10", 200, 1)
+    got, _ = _run(10, dtype, codes, ang, fusion=fusion, tile_bits=6)
+    assert np.max(np.abs(got - want)) <= TOL[dtype]
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 5, 8, 11, 14, 17])
+@pytest.mark.parametrize("kind", ["R4", "R10", "D", "S8", "LOW"])
+@pytest.mark.parametrize("dtype", ["c128", "c64"])
+@pytest.mark.parametrize("tile_bits", [None, 6])
+def test_sizes_and_kinds(n, kind, dtype, tile_bits):
+    count = 1000 if n <= 14 else 300
+    codes, ang, want = _want(n, kind, count, 2)
+    got, stats = _run(n, dtype, codes, ang, fusion=2, tile_bits=tile_bits)
+    err = np.max(np.abs(got - want))
+    assert err <= TOL[dtype], (err, stats["launches"])
+
+
+@pytest.mark.parametrize("dtype", ["c128", "c64"])
+@pytest.mark.parametrize("kind", ["R10", "LOW", "S8", "R4"])
+def test_fused_equals_unfused_bitwise(dtype, kind):
+    """Fusion changes traffic, not arithmetic: K1 one-rotation passes, same-x runs and tile passes
+    give bitwise identical states (R9)."""
+    n = 16
+    codes, ang = workloads.random_layer(n, 400, seed=3, kind=kind)
+    outs = []
+    for fusion, tb in ((0, None), (1, None), (2, None), (2, 7)):
+        got, stats = _run(n, dtype, codes, ang, fusion=fusion, tile_bits=tb)
+        outs.append(got)
+    for o in outs[1:]:
+        assert np.array_equal(o.view(np.uint8), outs[0].view(np.uint8))
+
+
+@pytest.mark.parametrize("dtype", ["c128", "c64"])
+@pytest.mark.parametrize("fusion", [0, 2])
+def test_bit_exact_basis_permutation(dtype, fusion):
+    """X-only rotations at phi = pi/2 from |b>: the index is b xor x_1 ... xor x_k bit-exactly,
+    the surviving amplitude is i^k with a component exactly +-1 (R8)."""
+    rng = np.random.default_rng(5)
+    n = 14
+    for trial in range(6):
+        k = int(rng.integers(1, 41))
+        b = int(rng.integers(0, 1 << n))
+        codes = rng.integers(0, 2, size=(k, n)).astype(np.uint8)
+        codes[codes.sum(axis=1) == 0, 0] = 1
+        got, _ = _run(n, dtype, codes, [math.pi / 2] * k, fusion=fusion, init=b)
+        target = b
+        for row in codes:
+            for q in range(n):
+                if row[q]:
+                    target ^= 1 << q
+        big = np.flatnonzero(np.abs(got) > 0.5)
+        assert big.tolist() == [target]
+        ph = 1j ** k
+        v = got[target]
+        if ph.real != 0:
+            assert v.real == ph.real
+        else:
+            assert v.imag == ph.imag
+        rest_tol = k * (1e-16 if dtype == "c128" else 1e-7)
+        assert np.max(np.abs(np.delete(got, target))) <= rest_tol
+
+
+@pytest.mark.parametrize("dtype", ["c128", "c64"])
+def test_closed_forms(dtype):
+    n = 12
+    rng = np.random.default_rng(6)
+    codes = rng.integers(0, 4, size=(20, n)).astype(np.uint8)
+    with P.State(n, dtype) as st:
+        st.init_random(SEED)
+        a0 = st.get_amplitudes()
+        x, z = P.pauli_encode_codes(codes)
+        st.apply_rotations(x, z, np.zeros(20))
+        assert np.array_equal(st.get_amplitudes(), a0)  # phi = 0 -> identity, bitwise
+        st.apply_rotations([0], [0], [0.37])  # identity string -> e^{i phi}
+        assert np.max(np.abs(st.get_amplitudes() - np.exp(0.37j) * a0)) <= TOL[dtype]
+
+
+@pytest.mark.parametrize("dtype", ["c128", "c64"])
+def test_init_random_matches_generator(dtype):
+    n = 15
+    with P.State(n, dtype) as st:
+        st.init_random(SEED)
+        got = st.get_amplitudes()
+    want = oracle.random_state(SEED, n)
+    if dtype == "c128":
+        assert np.array_equal(got, want)
+    else:
+        assert np.array_equal(got, want.astype(np.complex64))
+
+
+@pytest.mark.parametrize("dtype", ["c128", "c64"])
+def test_norm_expectation_inner(dtype):
+    n = 13
+    codes, ang, psi = _want(n, "R10", 300, 4)
+    hcodes = np.random.default_rng(7).integers(0, 4, size=(40, n)).astype(np.uint8)
+    hcodes[:10, :] = np.where(hcodes[:10, :] % 2 == 1, 3, 0)  # some diagonal terms
+    hcodes[10:14] = hcodes[14]  # shared x groups
+    coeffs = np.random.default_rng(8).standard_normal(40)
+    x, z = P.pauli_encode_codes(codes)
+    hx, hz = P.pauli_encode_codes(hcodes)
+    tol = 1e-10 if dtype == "c128" else 2e-3
+    with P.State(n, dtype) as st, P.State(n, dtype) as st2:
+        st.init_random(SEED)
+        st.apply_rotations(x, z, ang)
+        nrm = oracle.norm(n, psi)
+        assert abs(st.norm() - nrm) <= tol * nrm
+        e_want = oracle.expectation(n, psi, hcodes, coeffs)
+        assert abs(st.expectation(hx, hz, coeffs) - e_want) <= tol * max(1.0, nrm)
+        st2.init_random(SEED + 1)
+        ip_want = oracle.inner(n, psi, oracle.random_state(SEED + 1, n))
+        assert abs(st.inner(st2) - ip_want) <= tol * nrm
+        st.normalize()
+        assert abs(st.norm() - 1.0) <= (1e-12 if dtype == "c128" else 1e-5)
+
+
+def test_set_get_and_errors():
+    n = 9
+    rng = np.random.default_rng(9)
+    psi = rng.standard_normal(1 << n) + 1j * rng.standard_normal(1 << n)
+    with P.State(n, "c128") as st:
+        st.set_state(psi)
+        assert np.array_equal(st.get_amplitudes(), psi)
+        assert np.array_equal(st.get_amplitudes(100, 50), psi[100:150])
+        st.set_state(psi[:7] * 2, first=500)
+        psi2 = psi.copy()
+        psi2[500:507] = psi[:7] * 2
+        assert np.array_equal(st.get_amplitudes(), psi2)
+        # validation failures leave the state unchanged
+        with pytest.raises(P.PsError) as ei:
+            st.apply_rotations([1, 1 << n], [0, 0], [0.1, 0.2])
+        assert ei.value.code == -2
+        with pytest.raises(P.PsError) as ei:
+            st.apply_rotations([1], [0], [float("nan")])
+        assert ei.value.code == -1
+        with pytest.raises(P.PsError):
+            st.get_amplitudes(510, 10)
+        with pytest.raises(P.PsError):
+            st.init_basis(1 << n)
+        assert np.array_equal(st.get_amplitudes(), psi2)
+
+
+def test_torch_memory_and_stream():
+    import torch
+    n = 12
+    codes, ang, want = _want(n, "R10", 200, 10)
+    x, z = P.pauli_encode_codes(codes)
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        with P.State(n, "c128", torch_memory=True) as st:
+            st.init_random(SEED)
+            st.apply_rotations(x, z, ang)
+            t = st._tensor.view(torch.complex128).cpu().numpy()
+    assert np.max(np.abs(t - want)) <= 1e-10
+
+
+def test_stats_and_profile():
+    n = 14
+    codes, ang = workloads.random_layer(n, 100, seed=11, kind="R10")
+    x, z = P.pauli_encode_codes(codes)
+    with P.State(n, "c128") as st:
+        st.set_option(ps.OPT_PROFILE, 1)
+        st.init_random(SEED)
+        st.reset_stats()
+        st.apply_rotations(x, z, ang)
+        st.synchronize()
+        s = st.stats()
+    assert s["rotations"] == 100
+    assert sum(s["rotations_by"].values()) == 100
+    assert s["passes"] == sum(s["launches"][k] for k in ("stream", "tile", "coset"))
+    assert sum(s["kernel_ms"][k] for k in ("stream", "tile", "coset")) > 0
+
+
+# ------------------------------------------------------------------ full size (BASELINE config 2)
+
+def test_30q_inverse_layer_and_norm():
+    """30 qubits fp64 (16 GiB), the bench workload and launch configuration: a 1000-rotation R10
+    layer followed by its inverse returns the seeded initial amplitudes, which the oracle
+    regenerates one by one at sampled indices; the norm is preserved."""
+    n = 30
+    codes, ang = workloads.random_layer(n, 1000, seed=0, kind="R10")
+    x, z = P.pauli_encode_codes(codes)
+    rng = np.random.default_rng(12)
+    sample = np.unique(np.concatenate([rng.integers(0, 1 << n, 2000), [0, (1 << n) - 1]]))
+    with P.State(n, "c128", torch_memory=True) as st:
+        st.init_random(SEED)
+        n0 = st.norm()
+        st.apply_rotations(x, z, ang)
+        n1 = st.norm()
+        st.apply_rotations(x[::-1], z[::-1], -ang[::-1])
+        got = np.array([st.get_amplitudes(int(i), 1)[0] for i in sample[:300]])
+    want = np.array([oracle.random_amplitudes(SEED, int(i), 1)[0] for i in sample[:300]])
+    assert abs(n1 - n0) <= 1e-12 * n0
+    assert np.max(np.abs(got - want)) <= 1e-10
+
+
+def test_30q_coset_oracle():
+    """30 qubits with X-support restricted to 16 qubits (Z anywhere): every coset of the X-span is
+    invariant, so the coset oracle computes those amplitudes exactly (R13)."""
+    n = 30
+    rng = np.random.default_rng(13)
+    xq = np.sort(rng.choice(n, 16, replace=False))
+    L = 200
+    codes = rng.integers(0, 2, size=(L, n)).astype(np.uint8) * 3
+    for l in range(L):
+        w = rng.integers(1, 6)
+        pos = rng.choice(xq, w, replace=False)
+        codes[l, pos] = rng.integers(1, 3, size=w)
+    ang = rng.uniform(-np.pi, np.pi, L)
+    x, z = P.pauli_encode_codes(codes)
+    with P.State(n, "c128", torch_memory=True) as st:
+        st.init_random(SEED)
+        st.apply_rotations(x, z, ang)
+        for i0 in (0, int(rng.integers(0, 1 << n))):
+            mem = oracle.coset_members(n, i0, x)
+            init = np.array([oracle.random_amplitudes(SEED, int(m), 1)[0] for m in mem])
+            want = oracle.apply_coset(n, mem, init, codes, ang)
+            sel = rng.choice(len(mem), 200, replace=False)
+            got = np.array([st.get_amplitudes(int(mem[s]), 1)[0] for s in sel])
+            assert np.max(np.abs(got - want[sel])) <= 1e-10

@@ -1,0 +1,288 @@
+"""Host-side tests of libps (``-m "not gpu"``): the C-ABI library loads and exports every symbol
+include/ps.h declares; the encoder, gate converter and planner are checked against the oracle
+and the paper.  No compute entry point is called (no GPU here)."""
+from __future__ import annotations
+
+import math
+import os
+import re
+
+import numpy as np
+import pytest
+
+import oracle
+from oracle import dense
+import workloads
+import paper_2504_17881_b200 as P
+from paper_2504_17881_b200 import ps
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+GOLDEN = os.path.join(ROOT, "tests", "golden")
+
+
+def header_symbols():
+    txt = open(os.path.join(ROOT, "include", "ps.h")).read()
+    txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
+    return sorted(set(re.findall(r"\b(ps_[a-z_0-9]+)\s*\(", txt)))
+
+
+def test_library_exports_every_header_symbol():
+    L = P.lib()
+    syms = header_symbols()
+    assert len(syms) >= 20
+    for s in syms:
+        assert hasattr(L, s), s
+    assert sorted(ps.EXPORTS) == syms
+
+
+def test_status_strings():
+    L = P.lib()
+    for code in range(-7, 1):
+        assert L.ps_status_string(code)
+
+
+# ---------------------------------------------------------------- encoder (a1)
+
+def _golden(name):
+    for raw in open(os.path.join(GOLDEN, name)):
+        line = raw.split("#", 1)[0].strip()
+        if line:
+            yield line
+
+
+@pytest.mark.parametrize("line", list(_golden("encode_examples.txt")))
+def test_encode_golden(line):
+    word, p1, p2 = line.split()
+    assert P.pauli_encode(word) == (int(p1), int(p2))
+
+
+def test_encode_roundtrip_against_oracle_decode():
+    """Product encoder -> masks -> the oracle's independent decode -> same letters."""
+    rng = np.random.default_rng(0)
+    for n in (1, 2, 7, 36, 64):
+        codes = rng.integers(0, 4, size=(50, n)).astype(np.uint8)
+        x, z = P.pauli_encode_codes(codes)
+        assert np.array_equal(oracle.decode_masks(n, x, z), codes)
+        for row, xx, zz in zip(codes[:5], x, z):
+            word = "".join("IXYZ"[c] for c in row)
+            assert P.pauli_encode(word) == (int(xx), int(zz))
+
+
+@pytest.mark.parametrize("bad", ["", "XA", "X" * 65])
+def test_encode_errors(bad):
+    with pytest.raises(P.PsError):
+        P.pauli_encode(bad)
+
+
+# ---------------------------------------------------------------- gate converter (a1)
+
+_H = np.array([[1, 1], [1, -1]]) / math.sqrt(2)
+_S = np.diag([1, 1j])
+_T = np.diag([1, np.exp(1j * math.pi / 4)])
+_X = np.array([[0, 1], [1, 0]])
+_Y = np.array([[0, -1j], [1j, 0]])
+_Z = np.diag([1, -1])
+
+
+def _rx(t):
+    return np.array([[math.cos(t / 2), -1j * math.sin(t / 2)], [-1j * math.sin(t / 2), math.cos(t / 2)]])
+
+
+def _ry(t):
+    return np.array([[math.cos(t / 2), -math.sin(t / 2)], [math.sin(t / 2), math.cos(t / 2)]])
+
+
+def _rz(t):
+    return np.diag([np.exp(-1j * t / 2), np.exp(1j * t / 2)])
+
+
+def _textbook(name, qubits, params, n):
+    """Gate matrix on n qubits, qubit q = bit q of the index, built from textbook definitions."""
+    dim = 1 << n
+    if len(qubits) == 1:
+        m1 = {"H": _H, "S": _S, "T": _T, "X": _X, "Y": _Y, "Z": _Z}.get(name)
+        if m1 is None:
+            m1 = {"RX": _rx, "RY": _ry, "RZ": _rz}[name](params[0])
+        q = qubits[0]
+        u = np.zeros((dim, dim), complex)
+        for i in range(dim):
+            b = (i >> q) & 1
+            for b2 in (0, 1):
+                j = (i & ~(1 << q)) | (b2 << q)
+                u[j, i] += m1[b2, b]
+        return u
+    c, t = qubits
+    u = np.zeros((dim, dim), complex)
+    for i in range(dim):
+        bc, bt = (i >> c) & 1, (i >> t) & 1
+        if name == "CNOT":
+            j = i ^ (1 << t) if bc else i
+            u[j, i] = 1
+        elif name == "CZ":
+            u[i, i] = -1 if (bc and bt) else 1
+        elif name == "CPHASE":
+            u[i, i] = np.exp(1j * params[0]) if (bc and bt) else 1
+        elif name == "SWAP":
+            j = i & ~((1 << c) | (1 << t)) | (bt << c) | (bc << t)
+            u[j, i] = 1
+        elif name == "RZZ":
+            u[i, i] = np.exp(-1j * params[0] / 2 * (1 if bc == bt else -1))
+    return u
+
+
+@pytest.mark.parametrize("name,qubits,params", [
+    ("H", (1,), ()), ("S", (0,), ()), ("T", (2,), ()), ("X", (1,), ()), ("Y", (0,), ()), ("Z", (2,), ()),
+    ("RX", (0,), (0.37,)), ("RY", (2,), (-1.1,)), ("RZ", (1,), (2.5,)),
+    ("CNOT", (0, 2), ()), ("CNOT", (2, 0), ()), ("CZ", (1, 2), ()), ("SWAP", (0, 1), ()),
+    ("CPHASE", (2, 1), (0.77,)), ("RZZ", (0, 2), (-0.4,)),
+])
+def test_gate_converter_matches_textbook(name, qubits, params):
+    n = 3
+    x, z, a = P.gate_to_rotations(name, qubits, params)
+    f = oracle.decode_masks(n, x, z)
+    u = dense.dense_layer(f, a)  # product of expm(i phi P) in application order
+    assert np.max(np.abs(u - _textbook(name, qubits, params, n))) <= 1e-13
+
+
+def test_gate_converter_errors():
+    with pytest.raises(P.PsError):
+        P.gate_to_rotations("FOO", (0,))
+    with pytest.raises(P.PsError):
+        P.gate_to_rotations("CNOT", (1, 1))
+    with pytest.raises(P.PsError):
+        P.gate_to_rotations("RX", (0,))  # missing angle
+
+
+# ---------------------------------------------------------------- planner host model (a2, a5)
+
+def _apply_phys(a: np.ndarray, r: dict):
+    """Test-side model of one physical-coordinate rotation:
+    a'_i = c a_i + i s w(i^x) a_(i^x),  w(i) = i^y * sign * (-1)^popc(z & i)."""
+    n = len(a)
+    idx = np.arange(n, dtype=np.uint64)
+    x, z = np.uint64(r["x"]), np.uint64(r["z"])
+    par = np.array([bin(int(v)).count("1") & 1 for v in (idx ^ x) & z])
+    w = (1j ** r["y"]) * r["sign"] * np.where(par == 1, -1.0, 1.0)
+    c, s = math.cos(r["angle"]), math.sin(r["angle"])
+    j = (idx ^ x).astype(np.int64)
+    return c * a + 1j * s * w * a[j]
+
+
+def _run_model(n, world, x, z, ang, fusion=2, tile_bits=3):
+    m = world.bit_length() - 1
+    nl = n - m
+    plans = [P.plan_describe(n, x, z, ang, world=world, rank=r, fusion=fusion, tile_bits=tile_bits)
+             for r in range(world)]
+    kinds = [[(o["kind"], o["exch_bit"], o["exch_gx"], o["n_rot"]) for o in ops] for ops, _ in plans]
+    assert all(k == kinds[0] for k in kinds), "plans must be SPMD-identical in structure"
+    return plans, nl
+
+
+def _execute(n, world, psi, plans, nl):
+    local = [psi[r << nl:(r + 1) << nl].copy() for r in range(world)]
+    cursors = [0] * world
+    ops0 = plans[0][0]
+    for t, op in enumerate(ops0):
+        if op["kind"] == ps.K_EXCHANGE and op["exch_bit"] >= 0:
+            ell, gx = op["exch_bit"], op["exch_gx"]
+            g = (gx & -gx).bit_length() - 1
+            new = [v.copy() for v in local]
+            for r in range(world):
+                keep = (r >> g) & 1
+                p = r ^ gx
+                for slot in range(1 << nl):
+                    if ((slot >> ell) & 1) != keep:
+                        new[r][slot] = local[p][slot ^ (1 << ell)]
+            local = new
+        elif op["kind"] == ps.K_EXCHANGE:
+            # full exchange of a single rotation: own elements against the partner's old values
+            gx = op["exch_gx"]
+            new = []
+            for r in range(world):
+                rr = plans[r][1][cursors[r]]
+                cursors[r] += 1
+                p = r ^ gx
+                idx = np.arange(1 << nl, dtype=np.uint64)
+                par = np.array([bin(int(v)).count("1") & 1 for v in idx & np.uint64(rr["z"])])
+                w = (1j ** rr["y"]) * rr["sign"] * np.where(par == 1, -1.0, 1.0)  # w(own i)
+                c, s = math.cos(rr["angle"]), math.sin(rr["angle"])
+                j = (idx ^ np.uint64(rr["x"])).astype(np.int64)
+                new.append(c * local[r] + 1j * s * np.conj(w) * local[p][j])
+            local = new
+        else:
+            for r in range(world):
+                for _ in range(op["n_rot"]):
+                    local[r] = _apply_phys(local[r], plans[r][1][cursors[r]])
+                    cursors[r] += 1
+    return np.concatenate(local)
+
+
+@pytest.mark.parametrize("world", [1, 2, 4, 8])
+@pytest.mark.parametrize("kind", ["R4", "R10", "S8"])
+def test_planner_model_matches_oracle(world, kind):
+    n = 6
+    codes, ang = workloads.random_layer(n, 40, seed=world, kind=kind)
+    x, z = P.pauli_encode_codes(codes)
+    psi = oracle.random_state(3, n)
+    want = oracle.apply(n, psi, codes, ang)
+    plans, nl = _run_model(n, world, x, z, ang)
+    got = _execute(n, world, psi, plans, nl)
+    assert np.max(np.abs(got - want)) <= 1e-12
+
+
+def test_planner_full_exchange_fallback():
+    """A global-X string whose local X-part covers every local bit has no free pivot: the plan
+    uses the single-rotation full exchange and still matches the oracle."""
+    n, world = 4, 2
+    words = ["XXXX", "YXZY", "ZZZZ", "XYXY", "IXIX"]
+    codes = oracle.words_to_factors(words)
+    x, z = P.pauli_encode_codes(codes)
+    ang = np.array([0.3, -1.2, 0.7, 2.0, -0.5])
+    psi = oracle.random_state(5, n)
+    plans, nl = _run_model(n, world, x, z, ang)
+    assert any(o["kind"] == ps.K_EXCHANGE and o["exch_bit"] < 0 for o in plans[0][0])
+    got = _execute(n, world, psi, plans, nl)
+    assert np.max(np.abs(got - oracle.apply(n, psi, codes, ang))) <= 1e-12
+
+
+def test_exchange_economy():
+    """Eq. (1): a run sharing the upper X-part needs one exchange (plus the
+    swap back); z-only upper support needs none."""
+    n, world = 8, 4  # top 2 qubits are global
+    rng = np.random.default_rng(1)
+    L = 30
+    codes = np.zeros((L, n), np.uint8)
+    codes[:, :4] = rng.integers(0, 4, size=(L, 4))
+    codes[:, 6] = 1  # X on global qubit 6 for every rotation
+    codes[:, 7] = rng.integers(0, 2, size=L) * 3  # I/Z on global qubit 7
+    x, z = P.pauli_encode_codes(codes)
+    ops, _ = P.plan_describe(n, x, z, rng.uniform(-1, 1, L), world=world, rank=1)
+    assert sum(o["kind"] == ps.K_EXCHANGE for o in ops) == 2
+    codes[:, 6] = 3  # now Z only on the global qubits
+    x, z = P.pauli_encode_codes(codes)
+    ops, _ = P.plan_describe(n, x, z, rng.uniform(-1, 1, L), world=world, rank=1)
+    assert sum(o["kind"] == ps.K_EXCHANGE for o in ops) == 0
+
+
+def test_fusion_levels_cover_every_rotation_in_order():
+    n = 16
+    codes, ang = workloads.random_layer(n, 300, seed=2, kind="R10")
+    x, z = P.pauli_encode_codes(codes)
+    for fusion in (0, 1, 2):
+        ops, rots = P.plan_describe(n, x, z, ang, fusion=fusion, tile_bits=12)
+        covered = []
+        for o in ops:
+            covered.extend(range(o["first_rot"], o["first_rot"] + o["n_rot"]))
+        assert covered == list(range(300))
+        if fusion == 0:
+            assert len(ops) == 300
+    ops2, _ = P.plan_describe(n, x, z, ang, fusion=2, tile_bits=12)
+    assert len(ops2) < 300 / 3  # coset tiles fuse random layers
+
+
+def test_jw_hamiltonian_shape():
+    codes, coeffs = workloads.jw_hamiltonian(16, 3000, 27.0, n_local=14)
+    assert codes.shape == (3000, 16)
+    assert abs(np.abs(coeffs).sum() - 27.0) < 1e-9
+    x, z = P.pauli_encode_codes(codes)
+    assert len(np.unique(np.stack([x, z], 1), axis=0)) == 3000
