@@ -230,7 +230,7 @@ def run_ours(args):
     enc = [P.pauli_encode_codes(c) + (a,) for c, a in lay]
     st.init_random(workloads.BASE_SEED)
 
-    stream = torch.cuda.current_stream()
+    stream = st.torch_stream  # the stream libps enqueues on
     for w in range(args.warmup):
         x, z, a = enc[w]
         st.apply_rotations(x, z, a)

@@ -20,8 +20,8 @@ namespace ps {
 int kernel_max_red_blocks();
 cudaError_t launch_stream(int dtype, void* a, int nl, const Pass& p, const DevRot* d_rots, int vec256,
                           cudaStream_t s);
-cudaError_t launch_tile(int dtype, void* a, int nl, const Pass& p, const DevRot* d_rots, const uint64_t* d_offs,
-                        cudaStream_t s);
+cudaError_t launch_tile(int dtype, void* a, int nl, const Pass& p, const DevSub* d_subs, const DevTRot* d_trots,
+                        const uint64_t* d_offs, cudaStream_t s);
 cudaError_t launch_full_update(int dtype, void* a, const void* stage, uint64_t base, uint64_t count, uint64_t pbase,
                                const DevRot* rec, cudaStream_t s);
 cudaError_t launch_norm(int dtype, const void* a, uint64_t n, double* d_partial, double* d_out, cudaStream_t s);
@@ -59,6 +59,10 @@ struct ps_state {
     size_t d_rots_cap = 0;
     uint64_t* d_offs = nullptr;
     size_t d_offs_cap = 0;
+    DevSub* d_subs = nullptr;
+    size_t d_subs_cap = 0;
+    DevTRot* d_trots = nullptr;
+    size_t d_trots_cap = 0;
     void* h_stage[2] = {nullptr, nullptr};
     size_t h_stage_cap[2] = {0, 0};
     cudaEvent_t h_stage_ev[2] = {nullptr, nullptr};
@@ -196,6 +200,8 @@ static void free_state(ps_state* h) {
     }
     if (h->d_rots) cudaFree(h->d_rots);
     if (h->d_offs) cudaFree(h->d_offs);
+    if (h->d_subs) cudaFree(h->d_subs);
+    if (h->d_trots) cudaFree(h->d_trots);
     if (h->d_terms) cudaFree(h->d_terms);
     if (h->d_partial) cudaFree(h->d_partial);
     if (h->d_result) cudaFree(h->d_result);
@@ -312,8 +318,8 @@ extern "C" int ps_set_option(ps_handle h, int option, int64_t value) {
         h->fusion = (int)value;
         break;
     case PS_OPT_TILE_BITS: {
-        const int maxb = h->dtype == PS_C128 ? 13 : 14;  // <= 128 KiB of shared memory per tile
-        if (value < 1 || value > maxb) return fail(PS_EINVAL, "tile bits out of range");
+        const int maxb = h->dtype == PS_C128 ? 12 : 13;  // 3 stages of <= 64 KiB of shared memory
+        if (value < 4 || value > maxb) return fail(PS_EINVAL, "tile bits out of range [4, 12|13]");
         h->tile_bits = (int)value;
         break;
     }
@@ -529,11 +535,14 @@ static int exchange_full(ps_state* h, const Pass& p, const DevRot* d_rec, const 
 static int upload_plan(ps_state* h, const Plan& plan) {
     const size_t rb = plan.rots.size() * sizeof(DevRot);
     const size_t ob = plan.offsets.size() * sizeof(uint64_t);
-    const size_t total = rb + ob;
+    const size_t sb = plan.subs.size() * sizeof(DevSub);
+    const size_t tb = plan.trots.size() * sizeof(DevTRot);
+    const size_t total = rb + ob + sb + tb;
     if (total == 0) return PS_OK;
     int rc = ensure_dev(h, &h->d_rots, &h->d_rots_cap, std::max<size_t>(plan.rots.size(), 1));
-    if (rc) return rc;
-    rc = ensure_dev(h, &h->d_offs, &h->d_offs_cap, std::max<size_t>(plan.offsets.size(), 1));
+    if (!rc) rc = ensure_dev(h, &h->d_offs, &h->d_offs_cap, std::max<size_t>(plan.offsets.size(), 1));
+    if (!rc) rc = ensure_dev(h, &h->d_subs, &h->d_subs_cap, std::max<size_t>(plan.subs.size(), 1));
+    if (!rc) rc = ensure_dev(h, &h->d_trots, &h->d_trots_cap, std::max<size_t>(plan.trots.size(), 1));
     if (rc) return rc;
     const int b = h->stage_flip;
     h->stage_flip ^= 1;
@@ -546,10 +555,19 @@ static int upload_plan(ps_state* h, const Plan& plan) {
         h->h_stage_cap[b] = cap;
     }
     char* hs = (char*)h->h_stage[b];
-    if (rb) std::memcpy(hs, plan.rots.data(), rb);
-    if (ob) std::memcpy(hs + rb, plan.offsets.data(), ob);
-    if (rb) CUDA_TRY(h, cudaMemcpyAsync(h->d_rots, hs, rb, cudaMemcpyHostToDevice, h->stream));
-    if (ob) CUDA_TRY(h, cudaMemcpyAsync(h->d_offs, hs + rb, ob, cudaMemcpyHostToDevice, h->stream));
+    size_t off = 0;
+    auto put = [&](void* dst, const void* src, size_t bytes) -> int {
+        if (!bytes) return PS_OK;
+        std::memcpy(hs + off, src, bytes);
+        CUDA_TRY(h, cudaMemcpyAsync(dst, hs + off, bytes, cudaMemcpyHostToDevice, h->stream));
+        off += bytes;
+        return PS_OK;
+    };
+    rc = put(h->d_rots, plan.rots.data(), rb);
+    if (!rc) rc = put(h->d_offs, plan.offsets.data(), ob);
+    if (!rc) rc = put(h->d_subs, plan.subs.data(), sb);
+    if (!rc) rc = put(h->d_trots, plan.trots.data(), tb);
+    if (rc) return rc;
     CUDA_TRY(h, cudaEventRecord(h->h_stage_ev[b], h->stream));
     return PS_OK;
 }
@@ -589,7 +607,7 @@ extern "C" int ps_apply_rotations(ps_handle h, const uint64_t* xmask, const uint
         case PASS_TILE:
         case PASS_COSET: {
             Timed t(h, p.kind);
-            CUDA_TRY(h, launch_tile(h->dtype, h->d_state, h->nl, p, h->d_rots, h->d_offs, h->stream));
+            CUDA_TRY(h, launch_tile(h->dtype, h->d_state, h->nl, p, h->d_subs, h->d_trots, h->d_offs, h->stream));
             break;
         }
         case PASS_EXCHANGE: {

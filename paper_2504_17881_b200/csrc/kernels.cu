@@ -167,6 +167,26 @@ __device__ __forceinline__ void st_vec<float, 4>(float* p, const Vec<float, 4>& 
 
 constexpr int kStreamThreads = 256;
 
+// permutes v[e] <- v[e ^ m] for m < V with selects only (no dynamically indexed registers)
+template <typename T, int V>
+__device__ __forceinline__ void xor_permute(Vec<T, V>& v, int m) {
+#pragma unroll
+    for (int b = 1; b < V; b <<= 1) {
+        if (m & b) {
+#pragma unroll
+            for (int e = 0; e < V; ++e) {
+                if (e & b) continue;
+                const T r = v.r[e], i = v.i[e];
+                v.r[e] = v.r[e | b];
+                v.i[e] = v.i[e | b];
+                v.r[e | b] = r;
+                v.i[e | b] = i;
+            }
+        }
+    }
+}
+
+// vj has been permuted so that vj[e] is the partner of vi[e]
 template <typename T, int V>
 __device__ __forceinline__ void apply_run_pair(Vec<T, V>& vi, Vec<T, V>& vj, uint64_t ibase, int xin,
                                                uint64_t jbase, const DevRot* __restrict__ rec, int nrec) {
@@ -179,17 +199,28 @@ __device__ __forceinline__ void apply_run_pair(Vec<T, V>& vi, Vec<T, V>& vj, uin
             for (int e = 0; e < V; ++e) {
                 const int si = par64(z & (ibase + e));
                 rot_diag(vi.r[e], vi.i[e], k.c, flip(k.br, si), flip(k.bi, si));
-                const int sj = par64(z & (jbase + e));
+                const int sj = par64(z & (jbase + (e ^ xin)));
                 rot_diag(vj.r[e], vj.i[e], k.c, flip(k.br, sj), flip(k.bi, sj));
             }
         } else {
 #pragma unroll
             for (int e = 0; e < V; ++e) {
                 const int s = par64(z & (ibase + e));
-                const int f = e ^ xin;
-                rot_pair(vi.r[e], vi.i[e], vj.r[f], vj.i[f], k.c, flip(k.br, s), flip(k.bi, s));
+                rot_pair(vi.r[e], vi.i[e], vj.r[e], vj.i[e], k.c, flip(k.br, s), flip(k.bi, s));
             }
         }
+    }
+}
+
+template <typename T, int V, int X0>
+__device__ __forceinline__ void intra_pairs(Vec<T, V>& v, uint64_t base, uint64_t z, const Coef<T>& k) {
+    constexpr int piv = (X0 >= 2) ? 1 : 0;
+#pragma unroll
+    for (int e = 0; e < V; ++e) {
+        if ((e >> piv) & 1) continue;
+        const int f = e ^ X0;
+        const int s = par64(z & (base + e));
+        rot_pair(v.r[e], v.i[e], v.r[f], v.i[f], k.c, flip(k.br, s), flip(k.bi, s));
     }
 }
 
@@ -206,14 +237,12 @@ __device__ __forceinline__ void apply_run_intra(Vec<T, V>& v, uint64_t base, int
                 const int s = par64(z & (base + e));
                 rot_diag(v.r[e], v.i[e], k.c, flip(k.br, s), flip(k.bi, s));
             }
-        } else {
-#pragma unroll
-            for (int e = 0; e < V; ++e) {
-                if ((e >> piv) & 1) continue;
-                const int f = e ^ x0;
-                const int s = par64(z & (base + e));
-                rot_pair(v.r[e], v.i[e], v.r[f], v.i[f], k.c, flip(k.br, s), flip(k.bi, s));
-            }
+        } else if (x == 1) {
+            intra_pairs<T, V, 1>(v, base, z, k);
+        } else if (V >= 4 && x == 2) {
+            intra_pairs<T, V, (V >= 4 ? 2 : 1)>(v, base, z, k);
+        } else if (V >= 4) {
+            intra_pairs<T, V, (V >= 4 ? 3 : 1)>(v, base, z, k);
         }
     }
 }
@@ -242,7 +271,11 @@ __global__ void __launch_bounds__(kStreamThreads) k_stream(T* __restrict__ a, ui
 #pragma unroll
             for (int q = 0; q < UNROLL; ++q) {
                 const uint64_t uq = u + (uint64_t)q * stride;
-                if (uq < units) apply_run_pair<T, V>(vi[q], vj[q], ib[q], xin, ib[q] ^ xv, rec, nrec);
+                if (uq < units) {
+                    xor_permute<T, V>(vj[q], xin);
+                    apply_run_pair<T, V>(vi[q], vj[q], ib[q], xin, ib[q] ^ xv, rec, nrec);
+                    xor_permute<T, V>(vj[q], xin);
+                }
             }
 #pragma unroll
             for (int q = 0; q < UNROLL; ++q) {
@@ -276,13 +309,18 @@ __global__ void __launch_bounds__(kStreamThreads) k_stream(T* __restrict__ a, ui
 }
 
 // ------------------------------------------------------------------------------------------
-// K2 / K7: tile pass through shared memory with TMA bulk copies.
+// K2 / K7: tile pass.  Persistent CTAs walk tiles tau = blockIdx.x + m*gridDim.x through a
+// 3-stage shared-memory ring filled and drained by TMA bulk copies (cp.async.bulk, mbarrier
+// complete_tx; bulk stores with bulk_group read-completion before a stage is refilled).
 //
 // tile tau: i0 = pdep(tau, free_mask); chunk u (u < 2^h) = amplitudes [i0 ^ off[u], +2^c);
-// tile-local index l = (u << c) | w.  Rotation records are in tile-local coordinates; the
-// per-tile sign is parity(zt & i0).
+// tile-local index l = (u << c) | w.  Within a tile the pass's rotations are applied sub-group
+// by sub-group (ps_internal.h DevSub): each thread loads its 16-amplitude coset
+// r ^ span{u_0..u_3} from shared memory into registers, applies every rotation of the
+// sub-group there (pairs (d, d ^ dx), compile-time unrolled per dx), and writes it back.
 
-constexpr int kTileThreads = 512;
+constexpr int kStages = 3;
+constexpr int kTileMaxThreads = 512;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return (uint32_t)__cvta_generic_to_shared(p);
@@ -298,105 +336,197 @@ __device__ __forceinline__ uint64_t pdep64(uint64_t v, uint64_t mask) {
     return out;
 }
 
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    uint32_t done = 0;
+    while (!done) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done)
+            : "r"(smem_u32(bar)), "r"(parity)
+            : "memory");
+    }
+}
+
 template <typename T>
-__global__ void __launch_bounds__(kTileThreads) k_tile(T* __restrict__ a, int cbits, int hbits,
-                                                       uint64_t free_mask,
-                                                       const uint64_t* __restrict__ offs,
-                                                       const DevRot* __restrict__ rec, int nrec) {
+struct SmemAmp;
+template <>
+struct SmemAmp<double> {
+    using V = double2;
+};
+template <>
+struct SmemAmp<float> {
+    using V = float2;
+};
+
+__host__ __device__ constexpr int hibit(int v) { return v >= 8 ? 3 : v >= 4 ? 2 : v >= 2 ? 1 : 0; }
+
+template <typename T, int DX>
+__device__ __forceinline__ void sub_pairs(T (&vr)[kSubAmps], T (&vi)[kSubAmps], uint32_t M, int s0, T c, T br,
+                                          T bi) {
+    constexpr int piv = hibit(DX);
+#pragma unroll
+    for (int d = 0; d < kSubAmps; ++d) {
+        if ((d >> piv) & 1) continue;
+        const int e = d ^ DX;
+        const int s = s0 ^ (int)((M >> d) & 1u);
+        rot_pair(vr[d], vi[d], vr[e], vi[e], c, flip(br, s), flip(bi, s));
+    }
+}
+
+template <typename T>
+__device__ __forceinline__ void sub_rotation(T (&vr)[kSubAmps], T (&vi)[kSubAmps], uint32_t dx, uint32_t M, int s0,
+                                             T c, T br, T bi) {
+    switch (dx) {
+    case 0:
+#pragma unroll
+        for (int d = 0; d < kSubAmps; ++d) {
+            const int s = s0 ^ (int)((M >> d) & 1u);
+            rot_diag(vr[d], vi[d], c, flip(br, s), flip(bi, s));
+        }
+        break;
+    case 1: sub_pairs<T, 1>(vr, vi, M, s0, c, br, bi); break;
+    case 2: sub_pairs<T, 2>(vr, vi, M, s0, c, br, bi); break;
+    case 3: sub_pairs<T, 3>(vr, vi, M, s0, c, br, bi); break;
+    case 4: sub_pairs<T, 4>(vr, vi, M, s0, c, br, bi); break;
+    case 5: sub_pairs<T, 5>(vr, vi, M, s0, c, br, bi); break;
+    case 6: sub_pairs<T, 6>(vr, vi, M, s0, c, br, bi); break;
+    case 7: sub_pairs<T, 7>(vr, vi, M, s0, c, br, bi); break;
+    case 8: sub_pairs<T, 8>(vr, vi, M, s0, c, br, bi); break;
+    case 9: sub_pairs<T, 9>(vr, vi, M, s0, c, br, bi); break;
+    case 10: sub_pairs<T, 10>(vr, vi, M, s0, c, br, bi); break;
+    case 11: sub_pairs<T, 11>(vr, vi, M, s0, c, br, bi); break;
+    case 12: sub_pairs<T, 12>(vr, vi, M, s0, c, br, bi); break;
+    case 13: sub_pairs<T, 13>(vr, vi, M, s0, c, br, bi); break;
+    case 14: sub_pairs<T, 14>(vr, vi, M, s0, c, br, bi); break;
+    default: sub_pairs<T, 15>(vr, vi, M, s0, c, br, bi); break;
+    }
+}
+
+template <typename T>
+__device__ __forceinline__ void apply_subgroup(T* __restrict__ tile, const DevSub* __restrict__ sp,
+                                               const DevTRot* __restrict__ trots, uint32_t tid, uint64_t i0) {
+    using V2 = typename SmemAmp<T>::V;
+    V2* t2 = reinterpret_cast<V2*>(tile);
+    uint32_t u[kSubDim];
+#pragma unroll
+    for (int b = 0; b < kSubDim; ++b) u[b] = __ldg(&sp->u[b]);
+    const uint32_t piv = __ldg(&sp->piv);
+    const int rb = __ldg(&sp->rot_begin), nr = __ldg(&sp->nrot);
+    // representative: thread index with zero bits inserted at the (ascending) pivots
+    uint32_t r = tid;
+#pragma unroll
+    for (int b = 0; b < kSubDim; ++b) {
+        const uint32_t p = (piv >> (8 * b)) & 0xffu;
+        r = ((r >> p) << (p + 1)) | (r & ((1u << p) - 1u));
+    }
+    T vr[kSubAmps], vi[kSubAmps];
+#pragma unroll
+    for (int d = 0; d < kSubAmps; ++d) {
+        uint32_t l = r;
+#pragma unroll
+        for (int b = 0; b < kSubDim; ++b)
+            if ((d >> b) & 1) l ^= u[b];
+        const V2 v = t2[l];
+        vr[d] = v.x;
+        vi[d] = v.y;
+    }
+    for (int q = 0; q < nr; ++q) {
+        const DevTRot* tr = trots + rb + q;
+        const uint32_t dx = __ldg(&tr->dx);
+        const uint32_t M = __ldg(&tr->M);
+        const int s0 = (__popc(__ldg(&tr->zr) & r) & 1) ^ (__popcll(__ldg(&tr->zt) & i0) & 1);
+        sub_rotation<T>(vr, vi, dx, M, s0, (T)__ldg(&tr->c), (T)__ldg(&tr->br), (T)__ldg(&tr->bi));
+    }
+#pragma unroll
+    for (int d = 0; d < kSubAmps; ++d) {
+        uint32_t l = r;
+#pragma unroll
+        for (int b = 0; b < kSubDim; ++b)
+            if ((d >> b) & 1) l ^= u[b];
+        V2 v;
+        v.x = vr[d];
+        v.y = vi[d];
+        t2[l] = v;
+    }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kTileMaxThreads, 1)
+    k_tile(T* __restrict__ a, int kbits, int cbits, uint64_t free_mask, const uint64_t* __restrict__ offs,
+           uint64_t ntiles, const DevSub* __restrict__ subs, int nsub, const DevTRot* __restrict__ trots) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    __shared__ __align__(8) uint64_t mbar;
-    T* tile = reinterpret_cast<T*>(smem_raw);
-    const int kbits = cbits + hbits;
+    __shared__ __align__(8) uint64_t mbar[kStages];
     const uint32_t tile_amps = 1u << kbits;
-    const uint32_t chunk_bytes = (2u * sizeof(T)) << cbits;
-    const uint32_t nchunks = 1u << hbits;
-    const uint64_t i0 = pdep64((uint64_t)blockIdx.x, free_mask);
-    const int tid = threadIdx.x;
+    const uint32_t tile_bytes = tile_amps * (uint32_t)(2 * sizeof(T));
+    const uint32_t nchunks = 1u << (kbits - cbits);
+    const uint32_t chunk_bytes = (uint32_t)(2 * sizeof(T)) << cbits;
+    const uint32_t tid = threadIdx.x;
+    const uint32_t lane = tid & 31u;
+    const bool issuer = tid < 32;
+    const uint32_t wmask = blockDim.x >= 32 ? 0xffffffffu : ((1u << blockDim.x) - 1u);
+    const uint64_t my_tiles = ntiles > blockIdx.x ? (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+    auto stage_ptr = [&](int st) { return reinterpret_cast<T*>(smem_raw + (size_t)st * tile_bytes); };
 
     if (tid == 0) {
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&mbar)));
+        for (int st = 0; st < kStages; ++st)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&mbar[st])));
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    // ---- TMA bulk loads of the 2^h chunks into smem (warp 0 issues)
-    if (tid < 32) {
-        if (tid == 0) {
-            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&mbar)),
-                         "r"(tile_amps * (uint32_t)(2 * sizeof(T)))
+
+    auto issue_load = [&](uint64_t m) {
+        const uint64_t i0 = pdep64((uint64_t)blockIdx.x + m * gridDim.x, free_mask);
+        const int st = (int)(m % kStages);
+        T* buf = stage_ptr(st);
+        if (lane == 0)
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&mbar[st])),
+                         "r"(tile_bytes)
                          : "memory");
-        }
-        __syncwarp();
-        for (uint32_t u = tid; u < nchunks; u += 32) {
-            const uint64_t g = i0 ^ __ldg(&offs[u]);
-            const T* src = a + 2 * g;
-            T* dst = tile + 2 * ((uint64_t)u << cbits);
+        __syncwarp(wmask);
+        for (uint32_t u = lane; u < nchunks; u += 32) {
+            const T* src = a + 2 * (i0 ^ __ldg(&offs[u]));
             asm volatile(
                 "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                    smem_u32(dst)),
-                "l"(src), "r"(chunk_bytes), "r"(smem_u32(&mbar))
+                    smem_u32(buf + 2 * ((size_t)u << cbits))),
+                "l"(src), "r"(chunk_bytes), "r"(smem_u32(&mbar[st]))
                 : "memory");
         }
-    }
-    // ---- wait for the tile
-    {
-        uint32_t done = 0;
-        while (!done) {
-            asm volatile(
-                "{\n\t.reg .pred p;\n\t"
-                "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\n\t"
-                "selp.u32 %0, 1, 0, p;\n\t}"
-                : "=r"(done)
-                : "r"(smem_u32(&mbar))
-                : "memory");
-        }
-    }
-    // ---- every rotation of the pass, in order
-    for (int r = 0; r < nrec; ++r) {
-        const uint32_t X = (uint32_t)__ldg(&rec[r].x);
-        const uint32_t Z = (uint32_t)__ldg(&rec[r].z);
-        const int ts = par64(__ldg(&rec[r].zt) & i0);
-        const Coef<T> k = load_coef<T>(&rec[r]);
-        if (X == 0) {
-            for (uint32_t l = tid; l < tile_amps; l += kTileThreads) {
-                const int s = (__popc(Z & l) & 1) ^ ts;
-                T re = tile[2 * l], im = tile[2 * l + 1];
-                rot_diag(re, im, k.c, flip(k.br, s), flip(k.bi, s));
-                tile[2 * l] = re;
-                tile[2 * l + 1] = im;
-            }
-        } else {
-            const int piv = 31 - __clz(X);
-            const uint32_t lo = (1u << piv) - 1;
-            for (uint32_t p = tid; p < (tile_amps >> 1); p += kTileThreads) {
-                const uint32_t l = ((p >> piv) << (piv + 1)) | (p & lo);
-                const uint32_t m = l ^ X;
-                const int s = (__popc(Z & l) & 1) ^ ts;
-                T ir = tile[2 * l], ii = tile[2 * l + 1];
-                T jr = tile[2 * m], ji = tile[2 * m + 1];
-                rot_pair(ir, ii, jr, ji, k.c, flip(k.br, s), flip(k.bi, s));
-                tile[2 * l] = ir;
-                tile[2 * l + 1] = ii;
-                tile[2 * m] = jr;
-                tile[2 * m + 1] = ji;
-            }
-        }
-        __syncthreads();
-    }
-    // ---- TMA bulk stores back to HBM
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    __syncthreads();
-    if (tid < 32) {
-        for (uint32_t u = tid; u < nchunks; u += 32) {
-            const uint64_t g = i0 ^ __ldg(&offs[u]);
-            T* dst = a + 2 * g;
-            const T* src = tile + 2 * ((uint64_t)u << cbits);
+    };
+    auto issue_store = [&](uint64_t m) {
+        const uint64_t i0 = pdep64((uint64_t)blockIdx.x + m * gridDim.x, free_mask);
+        T* buf = stage_ptr((int)(m % kStages));
+        for (uint32_t u = lane; u < nchunks; u += 32) {
+            T* dst = a + 2 * (i0 ^ __ldg(&offs[u]));
             asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
-                         "r"(smem_u32(src)), "r"(chunk_bytes)
+                         "r"(smem_u32(buf + 2 * ((size_t)u << cbits))), "r"(chunk_bytes)
                          : "memory");
         }
         asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+    };
+
+    if (issuer && my_tiles > 0) issue_load(0);
+    for (uint64_t m = 0; m < my_tiles; ++m) {
+        const int st = (int)(m % kStages);
+        if (issuer && m + 1 < my_tiles) {
+            // stage (m+1)%3 last held tile m-2, whose store group is the older of the two pending
+            asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+            __syncwarp(wmask);
+            issue_load(m + 1);
+        }
+        mbar_wait(&mbar[st], (uint32_t)((m / kStages) & 1));
+        const uint64_t i0 = pdep64((uint64_t)blockIdx.x + m * gridDim.x, free_mask);
+        T* buf = stage_ptr(st);
+        for (int g = 0; g < nsub; ++g) {
+            apply_subgroup<T>(buf, subs + g, trots, tid, i0);
+            __syncthreads();
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncthreads();
+        if (issuer) issue_store(m);
     }
+    if (issuer) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
 // ------------------------------------------------------------------------------------------
@@ -591,18 +721,25 @@ cudaError_t launch_stream_t(T* a, int nl, const Pass& p, const DevRot* d_rots, c
 }
 
 template <typename T>
-cudaError_t launch_tile_t(T* a, int nl, const Pass& p, const DevRot* d_rots, const uint64_t* d_offs,
-                          cudaStream_t s) {
-    const size_t smem = (size_t)(2 * sizeof(T)) << p.kbits;
+cudaError_t launch_tile_t(T* a, int nl, const Pass& p, const DevSub* d_subs, const DevTRot* d_trots,
+                          const uint64_t* d_offs, cudaStream_t s) {
+    const size_t stage_bytes = (size_t)(2 * sizeof(T)) << p.kbits;
+    const size_t smem = stage_bytes * kStages;
     static bool attr_done[2] = {false, false};
     const int which = sizeof(T) == 8 ? 0 : 1;
     if (!attr_done[which]) {
         cudaFuncSetAttribute(k_tile<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         attr_done[which] = true;
     }
+    const int threads = 1 << (p.kbits - kSubDim);
+    int occ = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_tile<T>, threads, smem);
+    if (occ < 1) occ = 1;
     const uint64_t ntiles = 1ull << (nl - p.kbits);
-    k_tile<T><<<(unsigned)ntiles, kTileThreads, smem, s>>>(a, p.cbits, p.hbits, p.free_mask, d_offs + p.off_begin,
-                                                           d_rots + p.rot_begin, p.rot_count);
+    const uint64_t cap = (uint64_t)num_sms() * (uint64_t)occ;
+    const unsigned grid = (unsigned)(ntiles < cap ? ntiles : cap);
+    k_tile<T><<<grid, threads, smem, s>>>(a, p.kbits, p.cbits, p.free_mask, d_offs + p.off_begin, ntiles,
+                                          d_subs + p.sub_begin, p.sub_count, d_trots);
     return cudaGetLastError();
 }
 
@@ -630,10 +767,10 @@ cudaError_t launch_stream(int dtype, void* a, int nl, const Pass& p, const DevRo
     return launch_stream_t<float, 1>((float*)a, nl, p, d_rots, s);
 }
 
-cudaError_t launch_tile(int dtype, void* a, int nl, const Pass& p, const DevRot* d_rots, const uint64_t* d_offs,
-                        cudaStream_t s) {
-    if (dtype == PS_C128) return launch_tile_t<double>((double*)a, nl, p, d_rots, d_offs, s);
-    return launch_tile_t<float>((float*)a, nl, p, d_rots, d_offs, s);
+cudaError_t launch_tile(int dtype, void* a, int nl, const Pass& p, const DevSub* d_subs, const DevTRot* d_trots,
+                        const uint64_t* d_offs, cudaStream_t s) {
+    if (dtype == PS_C128) return launch_tile_t<double>((double*)a, nl, p, d_subs, d_trots, d_offs, s);
+    return launch_tile_t<float>((float*)a, nl, p, d_subs, d_trots, d_offs, s);
 }
 
 cudaError_t launch_full_update(int dtype, void* a, const void* stage, uint64_t base, uint64_t count, uint64_t pbase,

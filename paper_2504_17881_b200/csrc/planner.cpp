@@ -116,6 +116,77 @@ static void emit_stream(const std::vector<PhysRot>& seg, size_t b, size_t e, Pla
     plan->passes.push_back(p);
 }
 
+// tile-local rotation before sub-grouping
+struct LocalRot {
+    uint64_t x, z, zt;
+    int y, sign;
+    double phi;
+};
+
+// Splits a tile pass's rotations into sub-groups of <= kSubDim-dimensional xor span (order
+// preserving) and emits DevSub / DevTRot records (see ps_internal.h).
+static void make_subgroups(const std::vector<LocalRot>& lr, int k, Plan* plan, Pass* p) {
+    p->sub_begin = (int)plan->subs.size();
+    size_t b = 0;
+    while (b < lr.size()) {
+        Basis S;
+        size_t e = b;
+        for (; e < lr.size(); ++e) {
+            const uint64_t r = S.reduce(lr[e].x);
+            if (r) {
+                if (S.dim() == kSubDim) break;
+                S.add(r);
+            }
+        }
+        // pad to kSubDim dimensions with the highest free unit vectors (keeps low bits free so
+        // consecutive threads own consecutive tile-local indices: conflict-free 16-B smem access)
+        for (int q = k - 1; q >= 0 && S.dim() < kSubDim; --q) {
+            if ((S.pivots >> q) & 1) continue;
+            const uint64_t r = S.reduce(1ull << q);
+            if (r) S.add(r);
+        }
+        std::vector<uint64_t> u = S.v;
+        std::sort(u.begin(), u.end(), [](uint64_t a, uint64_t c) { return highest_bit(a) < highest_bit(c); });
+        DevSub sub{};
+        sub.piv = 0;
+        for (int t = 0; t < kSubDim; ++t) {
+            sub.u[t] = (uint32_t)u[t];
+            sub.piv |= (uint32_t)highest_bit(u[t]) << (8 * t);
+        }
+        sub.rot_begin = (int)plan->trots.size();
+        sub.nrot = (int)(e - b);
+        for (size_t t = b; t < e; ++t) {
+            const LocalRot& L = lr[t];
+            uint32_t dx = 0, dz = 0;
+            uint64_t chk = 0;
+            for (int q = 0; q < kSubDim; ++q) {
+                if ((L.x >> highest_bit(u[q])) & 1) {
+                    dx |= 1u << q;
+                    chk ^= u[q];
+                }
+                if (parity64(L.z & u[q])) dz |= 1u << q;
+            }
+            (void)chk;  // == L.x: the sub-group span contains every member's xor mask
+            uint32_t M = 0;
+            for (int d = 0; d < kSubAmps; ++d)
+                if (parity64((uint64_t)(dz & (uint32_t)d))) M |= 1u << d;
+            const DevRot r = make_rec(L.x, L.z, L.zt, L.y, L.sign, L.phi);
+            DevTRot tr{};
+            tr.dx = dx;
+            tr.M = M;
+            tr.zr = (uint32_t)L.z;
+            tr.zt = L.zt;
+            tr.c = r.c;
+            tr.br = r.br;
+            tr.bi = r.bi;
+            plan->trots.push_back(tr);
+        }
+        plan->subs.push_back(sub);
+        b = e;
+    }
+    p->sub_count = (int)plan->subs.size() - p->sub_begin;
+}
+
 static void emit_tile(const std::vector<PhysRot>& seg, size_t b, size_t e, const PlanConfig& cfg,
                       const Basis& hb, int chunk_min, Plan* plan) {
     const int nl = cfg.n_local;
@@ -138,9 +209,10 @@ static void emit_tile(const std::vector<PhysRot>& seg, size_t b, size_t e, const
         p.off_begin = (int)plan->offsets.size();
         plan->offsets.push_back(0);
         const uint64_t kmask = (1ull << k) - 1;
+        std::vector<LocalRot> lr;
         for (size_t t = b; t < e; ++t)
-            plan->rots.push_back(make_rec(seg[t].x, seg[t].z & kmask, seg[t].z & p.free_mask,
-                                          seg[t].y, seg[t].sign, seg[t].phi));
+            lr.push_back({seg[t].x, seg[t].z & kmask, seg[t].z & p.free_mask, seg[t].y, seg[t].sign, seg[t].phi});
+        make_subgroups(lr, k, plan, &p);
         plan->passes.push_back(p);
         return;
     }
@@ -178,6 +250,7 @@ static void emit_tile(const std::vector<PhysRot>& seg, size_t b, size_t e, const
             if ((u >> t) & 1) o ^= vs[t];
         plan->offsets.push_back(o);
     }
+    std::vector<LocalRot> lr;
     for (size_t t = b; t < e; ++t) {
         const uint64_t x = seg[t].x, z = seg[t].z;
         const uint64_t xh = x & ~cmask;
@@ -193,8 +266,9 @@ static void emit_tile(const std::vector<PhysRot>& seg, size_t b, size_t e, const
         (void)chk;  // chk == xh by construction (x lies in the tile space)
         const uint64_t xl = (coef << c) | (x & cmask);
         const uint64_t zl = (zc << c) | (z & cmask);
-        plan->rots.push_back(make_rec(xl, zl, z & p.free_mask, seg[t].y, seg[t].sign, seg[t].phi));
+        lr.push_back({xl, zl, z & p.free_mask, seg[t].y, seg[t].sign, seg[t].phi});
     }
+    make_subgroups(lr, p.kbits, plan, &p);
     plan->passes.push_back(p);
 }
 
@@ -221,8 +295,14 @@ static void form_passes(const std::vector<PhysRot>& seg, const PlanConfig& cfg, 
         emit_stream(seg, b, seg.size(), plan);
         return;
     }
-    // fusion 2: greedy tile spaces (order preserving)
+    // fusion 2: greedy tile spaces (order preserving); a tile needs >= 2^kSubDim amplitudes
     const int k = std::min(cfg.tile_bits, nl);
+    if (k < kSubDim) {
+        PlanConfig c1 = cfg;
+        c1.fusion = 1;
+        form_passes(seg, c1, plan);
+        return;
+    }
     const int chunk_min = std::min(cfg.min_chunk_bits, k);
     const uint64_t low = (1ull << chunk_min) - 1;
     size_t b = 0;
@@ -268,6 +348,8 @@ void make_plan(const PlanConfig& cfg, const uint64_t* x, const uint64_t* z, cons
     plan->passes.clear();
     plan->rots.clear();
     plan->offsets.clear();
+    plan->subs.clear();
+    plan->trots.clear();
     plan->debug_rots.clear();
     plan->exchanges = 0;
     const int nl = cfg.n_local;

@@ -33,6 +33,37 @@ struct DevRot {
 };
 static_assert(sizeof(DevRot) == 56 || sizeof(DevRot) == 64, "DevRot layout");
 
+// Tile passes (K2/K7) apply their rotations in SUB-GROUPS: consecutive rotations whose
+// tile-local xor masks span <= kSubDim dimensions.  For a sub-group with basis u_0..u_3
+// (tile-local, pivots p_0 < .. < p_3 = highest set bits, reduced row-echelon form) every thread
+// owns one coset r xor span{u}: r = its thread index with zero bits inserted at the pivots, and
+// holds the 16 amplitudes l_d = r xor U(d), U(d) = xor of u_b over the set bits b of d, in
+// registers while the sub-group's rotations are applied.
+constexpr int kSubDim = 4;
+constexpr int kSubAmps = 1 << kSubDim;
+
+struct DevSub {
+    uint32_t u[kSubDim];  // basis in tile-local coordinates
+    uint32_t piv;         // pivot positions p_b in byte b, ascending
+    int32_t rot_begin;    // first DevTRot of this sub-group (index into the call's table)
+    int32_t nrot;
+    uint32_t pad;
+};
+static_assert(sizeof(DevSub) == 32, "DevSub layout");
+
+// one rotation of a sub-group: pair (d, d xor dx) of the thread's 16 registers ("i" member: bit
+// highest(dx) of d is 0), sigma = parity(zr & r) xor parity(zt & i0) xor bit d of M, with
+// M bit d = parity(Dz & d), Dz_b = parity(Z_loc & u_b); c, br, bi as in DevRot.
+struct DevTRot {
+    uint32_t dx;  // 0: diagonal
+    uint32_t M;
+    uint32_t zr;  // tile-local phase mask (parity with the coset representative r)
+    uint32_t pad;
+    uint64_t zt;  // phase mask on the tile-enumeration bits (parity with the tile base i0)
+    double c, br, bi;
+};
+static_assert(sizeof(DevTRot) == 48, "DevTRot layout");
+
 // expectation term record: contribution sigma(i) * (kr * tr + ki * ti) per pair (x != 0) with
 // t = conj(a_j) a_i, or sigma(i) * kr * |a_i|^2 per element (x = 0)
 struct DevTerm {
@@ -64,6 +95,8 @@ struct Pass {
     int hbits = 0;        // number of gathered high basis vectors
     uint64_t free_mask = 0;
     int off_begin = 0;    // first entry of this pass's 2^hbits chunk offsets in the call's table
+    int sub_begin = 0;    // first DevSub of this pass
+    int sub_count = 0;
     // EXCHANGE
     uint64_t gx = 0;      // partner = rank xor gx
     int ell = 0;          // local pivot bit
@@ -75,6 +108,8 @@ struct Plan {
     std::vector<Pass> passes;
     std::vector<DevRot> rots;
     std::vector<uint64_t> offsets;
+    std::vector<DevSub> subs;
+    std::vector<DevTRot> trots;
     std::vector<ps_plan_rot> debug_rots;  // filled when requested (plan dump)
     uint64_t exchanges = 0;
 };

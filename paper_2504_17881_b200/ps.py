@@ -216,6 +216,7 @@ class State:
         self.world, self.rank = int(world), int(rank)
         self._h = ctypes.c_void_p()
         self._tensor = None
+        self.torch_stream = None
         L = lib()
         nid = None
         if self.world > 1:
@@ -236,7 +237,11 @@ class State:
             self._tensor = torch.empty(2 << nl, dtype=tdt, device="cuda")
             dev_ptr = self._tensor.data_ptr()
             nbytes = self._tensor.numel() * self._tensor.element_size()
-            stream = torch.cuda.current_stream().cuda_stream
+            cur = torch.cuda.current_stream()
+            # the legacy default stream has handle 0, which libps reads as "make your own":
+            # give libps a real torch stream so torch events on it see the work
+            self.torch_stream = cur if cur.cuda_stream != 0 else torch.cuda.Stream()
+            stream = self.torch_stream.cuda_stream
         _check("ps_create_ex", L.ps_create_ex(self.n, self.dtype, dev_ptr, nbytes, stream, self.rank, self.world,
                                               nid, ctypes.byref(self._h)))
         nq, nl = ctypes.c_int(), ctypes.c_int()
