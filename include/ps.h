@@ -83,10 +83,11 @@ typedef struct ps_stats {
 enum {
     PS_OPT_PROFILE = 0,       /* 1: time every launch with CUDA events on the handle's stream (default 0) */
     PS_OPT_FUSION = 1,        /* 0: one rotation per pass (K1 only); 1: same-x runs; 2: + tiles (default 2) */
-    PS_OPT_TILE_BITS = 2,     /* log2 amplitudes per fused tile (default: 12 for C128, 13 for C64) */
+    PS_OPT_TILE_BITS = 2,     /* log2 amplitudes per fused tile, 4..12 (default 12) */
     PS_OPT_CHUNK_BYTES = 3,   /* exchange chunk size in bytes (default 256 MiB) */
     PS_OPT_MAX_PASS_ROTS = 4, /* cap on rotations fused into one tile pass (default 64) */
-    PS_OPT_VEC256 = 5         /* 1: 256-bit LDG/STG in K1 (default 1); 0: 128-bit */
+    PS_OPT_VEC256 = 5,        /* 1: 256-bit LDG/STG in K1 (default 1); 0: 128-bit */
+    PS_OPT_TILE_TMA = 6       /* 1: tile passes stage whole tiles through a TMA ring (A/B); default 0 */
 };
 
 /* ------------------------------------------------------------------------------------------ */

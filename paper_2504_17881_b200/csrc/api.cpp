@@ -21,7 +21,7 @@ int kernel_max_red_blocks();
 cudaError_t launch_stream(int dtype, void* a, int nl, const Pass& p, const DevRot* d_rots, int vec256,
                           cudaStream_t s);
 cudaError_t launch_tile(int dtype, void* a, int nl, const Pass& p, const DevSub* d_subs, const DevTRot* d_trots,
-                        const uint64_t* d_offs, cudaStream_t s);
+                        const uint64_t* d_offs, int use_tma, cudaStream_t s);
 cudaError_t launch_full_update(int dtype, void* a, const void* stage, uint64_t base, uint64_t count, uint64_t pbase,
                                const DevRot* rec, cudaStream_t s);
 cudaError_t launch_norm(int dtype, const void* a, uint64_t n, double* d_partial, double* d_out, cudaStream_t s);
@@ -79,7 +79,7 @@ struct ps_state {
     size_t xstage_bytes = 0;
     size_t chunk_bytes = 256ull << 20;
     // options
-    int profile = 0, fusion = 2, tile_bits = 12, vec256 = 1, max_pass_rots = 1 << 30;
+    int profile = 0, fusion = 2, tile_bits = 12, vec256 = 1, max_pass_rots = 1 << 30, tile_tma = 0;
     ps_stats stats{};
     std::vector<PendingTiming> pending;
     std::vector<cudaEvent_t> event_pool;
@@ -231,7 +231,7 @@ extern "C" int ps_create_ex(int n_qubits, int dtype, void* dev_buf, size_t bytes
     h->world = world;
     h->dtype = dtype;
     h->amp_bytes = dtype == PS_C128 ? 16 : 8;
-    h->tile_bits = dtype == PS_C128 ? 12 : 13;
+    h->tile_bits = 12;
     cudaError_t e = cudaGetDevice(&h->device);
     if (e != cudaSuccess) {
         delete h;
@@ -318,8 +318,8 @@ extern "C" int ps_set_option(ps_handle h, int option, int64_t value) {
         h->fusion = (int)value;
         break;
     case PS_OPT_TILE_BITS: {
-        const int maxb = h->dtype == PS_C128 ? 12 : 13;  // 3 stages of <= 64 KiB of shared memory
-        if (value < 4 || value > maxb) return fail(PS_EINVAL, "tile bits out of range [4, 12|13]");
+        // <= 256 threads x 16 amplitudes per tile (and 3 TMA stages of <= 64 KiB)
+        if (value < 4 || value > 12) return fail(PS_EINVAL, "tile bits out of range [4, 12]");
         h->tile_bits = (int)value;
         break;
     }
@@ -332,6 +332,7 @@ extern "C" int ps_set_option(ps_handle h, int option, int64_t value) {
         h->max_pass_rots = (int)std::min<int64_t>(value, 1 << 30);
         break;
     case PS_OPT_VEC256: h->vec256 = value ? 1 : 0; break;
+    case PS_OPT_TILE_TMA: h->tile_tma = value ? 1 : 0; break;
     default: return fail(PS_EINVAL, "unknown option");
     }
     return PS_OK;
@@ -607,7 +608,7 @@ extern "C" int ps_apply_rotations(ps_handle h, const uint64_t* xmask, const uint
         case PASS_TILE:
         case PASS_COSET: {
             Timed t(h, p.kind);
-            CUDA_TRY(h, launch_tile(h->dtype, h->d_state, h->nl, p, h->d_subs, h->d_trots, h->d_offs, h->stream));
+            CUDA_TRY(h, launch_tile(h->dtype, h->d_state, h->nl, p, h->d_subs, h->d_trots, h->d_offs, h->tile_tma, h->stream));
             break;
         }
         case PASS_EXCHANGE: {

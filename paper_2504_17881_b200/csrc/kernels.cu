@@ -3,94 +3,42 @@
 //   K1 k_stream     streaming pair-rotation pass: one rotation or a same-x run applied to each
 //                   pair {i, i xor x} in registers, 256-bit LDG/STG, pair indices by bit
 //                   insertion (P:96-101 direct sum of 2x2 blocks; P:119-121 AND/XOR/parity)
-//   K2/K7 k_tile    fused tile pass: a 2^k-amplitude tile (contiguous for K2, a gathered coset
-//                   i0 xor span{v_t} of contiguous chunks for K7) is staged in shared memory by
-//                   TMA bulk copies (cp.async.bulk + mbarrier), every rotation of the pass is
-//                   applied there, and the tile is written back by TMA bulk stores
-//                   (several rotations per traversal of the array)
+//   K2/K7 k_coset   fused tile pass (default): a 2^k-amplitude tile -- contiguous (K2) or a
+//                   gathered coset i0 xor span{v_t} of contiguous chunks (K7) -- whose rotations
+//                   are applied in sub-groups of <= 4-dimensional xor span, each thread holding a
+//                   16-amplitude coset in registers; the first sub-group loads straight from HBM,
+//                   the last stores straight back, shared memory carries the tile only between
+//                   sub-groups (several rotations per traversal of the array)
+//   K2/K7 k_tile    the same pass with the whole tile staged in shared memory by TMA bulk copies
+//                   (cp.async.bulk + mbarrier ring; PS_OPT_TILE_TMA=1, kept for A/B evidence)
 //   K5 k_norm/k_expect/k_inner   fp64-accumulating reductions
 //   K6 k_init_*     seeded counter-based init, basis states
 //   K3 k_full_update  single-rotation full-exchange update against a partner chunk
 //
-// Every kernel applies the SAME per-pair arithmetic (rot_pair / rot_diag below, explicit
-// round-to-nearest intrinsics, no contraction freedom) so fused and unfused passes, and 1-GPU
-// and G-GPU runs, are bitwise identical.
+// Every kernel applies the SAME per-pair arithmetic (arith.cuh).
 #include <cuda_runtime.h>
 #include <cstdint>
 
+#include "arith.cuh"
 #include "ps_internal.h"
 
 namespace ps {
 namespace {
 
-// ------------------------------------------------------------------------------------------
-// per-pair arithmetic (DevRot in ps_internal.h):
-//   a'_i = c a_i + s*A a_j, A = (-br, bi);   a'_j = c a_j + s*B a_i, B = (br, bi);  s = +-1
-
-__device__ __forceinline__ void rot_pair(double& ir, double& ii, double& jr, double& ji, double c,
-                                         double br, double bi) {
-    const double ur = __fma_rn(-br, jr, __dmul_rn(-bi, ji));
-    const double ui = __fma_rn(-br, ji, __dmul_rn(bi, jr));
-    const double vr = __fma_rn(br, ir, __dmul_rn(-bi, ii));
-    const double vi = __fma_rn(br, ii, __dmul_rn(bi, ir));
-    const double nir = __fma_rn(c, ir, ur);
-    const double nii = __fma_rn(c, ii, ui);
-    const double njr = __fma_rn(c, jr, vr);
-    const double nji = __fma_rn(c, ji, vi);
-    ir = nir; ii = nii; jr = njr; ji = nji;
-}
-
-__device__ __forceinline__ void rot_pair(float& ir, float& ii, float& jr, float& ji, float c,
-                                         float br, float bi) {
-    const float ur = __fmaf_rn(-br, jr, __fmul_rn(-bi, ji));
-    const float ui = __fmaf_rn(-br, ji, __fmul_rn(bi, jr));
-    const float vr = __fmaf_rn(br, ir, __fmul_rn(-bi, ii));
-    const float vi = __fmaf_rn(br, ii, __fmul_rn(bi, ir));
-    const float nir = __fmaf_rn(c, ir, ur);
-    const float nii = __fmaf_rn(c, ii, ui);
-    const float njr = __fmaf_rn(c, jr, vr);
-    const float nji = __fmaf_rn(c, ji, vi);
-    ir = nir; ii = nii; jr = njr; ji = nji;
-}
-
-__device__ __forceinline__ void rot_diag(double& r, double& i, double c, double br, double bi) {
-    const double ur = __fma_rn(-br, r, __dmul_rn(-bi, i));
-    const double ui = __fma_rn(-br, i, __dmul_rn(bi, r));
-    r = __fma_rn(c, r, ur);
-    i = __fma_rn(c, i, ui);
-}
-
-__device__ __forceinline__ void rot_diag(float& r, float& i, float c, float br, float bi) {
-    const float ur = __fmaf_rn(-br, r, __fmul_rn(-bi, i));
-    const float ui = __fmaf_rn(-br, i, __fmul_rn(bi, r));
-    r = __fmaf_rn(c, r, ur);
-    i = __fmaf_rn(c, i, ui);
-}
-
 template <typename T>
-struct Coef {
-    T c, br, bi;
+struct RotK {
+    T c, b;
+    int real;
 };
 
+
 template <typename T>
-__device__ __forceinline__ Coef<T> load_coef(const DevRot* __restrict__ r) {
-    Coef<T> k;
+__device__ __forceinline__ RotK<T> load_rot(const DevRot* __restrict__ r) {
+    RotK<T> k;
     k.c = (T)__ldg(&r->c);
-    k.br = (T)__ldg(&r->br);
-    k.bi = (T)__ldg(&r->bi);
+    k.b = (T)__ldg(&r->b);
+    k.real = (int)__ldg(&r->real);
     return k;
-}
-
-template <typename T>
-__device__ __forceinline__ T flip(T v, int neg) {
-    return neg ? -v : v;
-}
-
-__device__ __forceinline__ int par64(uint64_t v) { return __popcll(v) & 1; }
-
-__device__ __forceinline__ uint64_t insert0(uint64_t t, int p) {
-    const uint64_t lo = t & ((1ull << p) - 1);
-    return ((t >> p) << (p + 1)) | lo;
 }
 
 // ------------------------------------------------------------------------------------------
@@ -186,64 +134,84 @@ __device__ __forceinline__ void xor_permute(Vec<T, V>& v, int m) {
     }
 }
 
-// vj has been permuted so that vj[e] is the partner of vi[e]
+template <int REAL, typename T, int V>
+__device__ __forceinline__ void pair_vecs(Vec<T, V>& vi, Vec<T, V>& vj, uint64_t ibase, uint64_t z, T c, T b) {
+#pragma unroll
+    for (int e = 0; e < V; ++e) {
+        const int s = par64(z & (ibase + e));
+        rot_pair<REAL>(vi.r[e], vi.i[e], vj.r[e], vj.i[e], c, flip(b, s));
+    }
+}
+
+template <int REAL, typename T, int V>
+__device__ __forceinline__ void diag_vec(Vec<T, V>& v, uint64_t base, int xin, uint64_t z, T c, T b) {
+#pragma unroll
+    for (int e = 0; e < V; ++e) {
+        const int s = par64(z & (base + (e ^ xin)));
+        rot_diag<REAL>(v.r[e], v.i[e], c, flip(b, s));
+    }
+}
+
+// vj has been permuted so that vj[e] is the partner of vi[e] (original index jbase + (e ^ xin))
 template <typename T, int V>
 __device__ __forceinline__ void apply_run_pair(Vec<T, V>& vi, Vec<T, V>& vj, uint64_t ibase, int xin,
                                                uint64_t jbase, const DevRot* __restrict__ rec, int nrec) {
     for (int r = 0; r < nrec; ++r) {
         const uint64_t x = __ldg(&rec[r].x);
         const uint64_t z = __ldg(&rec[r].z);
-        const Coef<T> k = load_coef<T>(&rec[r]);
+        const RotK<T> k = load_rot<T>(&rec[r]);
         if (x == 0) {
-#pragma unroll
-            for (int e = 0; e < V; ++e) {
-                const int si = par64(z & (ibase + e));
-                rot_diag(vi.r[e], vi.i[e], k.c, flip(k.br, si), flip(k.bi, si));
-                const int sj = par64(z & (jbase + (e ^ xin)));
-                rot_diag(vj.r[e], vj.i[e], k.c, flip(k.br, sj), flip(k.bi, sj));
+            if (k.real) {
+                diag_vec<1>(vi, ibase, 0, z, k.c, k.b);
+                diag_vec<1>(vj, jbase, xin, z, k.c, k.b);
+            } else {
+                diag_vec<0>(vi, ibase, 0, z, k.c, k.b);
+                diag_vec<0>(vj, jbase, xin, z, k.c, k.b);
             }
+        } else if (k.real) {
+            pair_vecs<1>(vi, vj, ibase, z, k.c, k.b);
         } else {
-#pragma unroll
-            for (int e = 0; e < V; ++e) {
-                const int s = par64(z & (ibase + e));
-                rot_pair(vi.r[e], vi.i[e], vj.r[e], vj.i[e], k.c, flip(k.br, s), flip(k.bi, s));
-            }
+            pair_vecs<0>(vi, vj, ibase, z, k.c, k.b);
         }
     }
 }
 
-template <typename T, int V, int X0>
-__device__ __forceinline__ void intra_pairs(Vec<T, V>& v, uint64_t base, uint64_t z, const Coef<T>& k) {
+template <int REAL, typename T, int V, int X0>
+__device__ __forceinline__ void intra_pairs(Vec<T, V>& v, uint64_t base, uint64_t z, T c, T b) {
     constexpr int piv = (X0 >= 2) ? 1 : 0;
 #pragma unroll
     for (int e = 0; e < V; ++e) {
         if ((e >> piv) & 1) continue;
         const int f = e ^ X0;
         const int s = par64(z & (base + e));
-        rot_pair(v.r[e], v.i[e], v.r[f], v.i[f], k.c, flip(k.br, s), flip(k.bi, s));
+        rot_pair<REAL>(v.r[e], v.i[e], v.r[f], v.i[f], c, flip(b, s));
+    }
+}
+
+template <int REAL, typename T, int V>
+__device__ __forceinline__ void intra_rot(Vec<T, V>& v, uint64_t base, uint64_t x, uint64_t z, T c, T b) {
+    if (x == 0) {
+        diag_vec<REAL>(v, base, 0, z, c, b);
+    } else if (x == 1) {
+        intra_pairs<REAL, T, V, 1>(v, base, z, c, b);
+    } else if (V >= 4 && x == 2) {
+        intra_pairs<REAL, T, V, (V >= 4 ? 2 : 1)>(v, base, z, c, b);
+    } else if (V >= 4) {
+        intra_pairs<REAL, T, V, (V >= 4 ? 3 : 1)>(v, base, z, c, b);
     }
 }
 
 template <typename T, int V>
-__device__ __forceinline__ void apply_run_intra(Vec<T, V>& v, uint64_t base, int x0, int piv,
-                                                const DevRot* __restrict__ rec, int nrec) {
+__device__ __forceinline__ void apply_run_intra(Vec<T, V>& v, uint64_t base, const DevRot* __restrict__ rec,
+                                                int nrec) {
     for (int r = 0; r < nrec; ++r) {
         const uint64_t x = __ldg(&rec[r].x);
         const uint64_t z = __ldg(&rec[r].z);
-        const Coef<T> k = load_coef<T>(&rec[r]);
-        if (x == 0) {
-#pragma unroll
-            for (int e = 0; e < V; ++e) {
-                const int s = par64(z & (base + e));
-                rot_diag(v.r[e], v.i[e], k.c, flip(k.br, s), flip(k.bi, s));
-            }
-        } else if (x == 1) {
-            intra_pairs<T, V, 1>(v, base, z, k);
-        } else if (V >= 4 && x == 2) {
-            intra_pairs<T, V, (V >= 4 ? 2 : 1)>(v, base, z, k);
-        } else if (V >= 4) {
-            intra_pairs<T, V, (V >= 4 ? 3 : 1)>(v, base, z, k);
-        }
+        const RotK<T> k = load_rot<T>(&rec[r]);
+        if (k.real)
+            intra_rot<1>(v, base, x, z, k.c, k.b);
+        else
+            intra_rot<0>(v, base, x, z, k.c, k.b);
     }
 }
 
@@ -297,7 +265,7 @@ __global__ void __launch_bounds__(kStreamThreads) k_stream(T* __restrict__ a, ui
 #pragma unroll
             for (int q = 0; q < UNROLL; ++q) {
                 const uint64_t uq = u + (uint64_t)q * stride;
-                if (uq < units) apply_run_intra<T, V>(v[q], uq * V, (int)x0, piv, rec, nrec);
+                if (uq < units) apply_run_intra<T, V>(v[q], uq * V, rec, nrec);
             }
 #pragma unroll
             for (int q = 0; q < UNROLL; ++q) {
@@ -309,22 +277,106 @@ __global__ void __launch_bounds__(kStreamThreads) k_stream(T* __restrict__ a, ui
 }
 
 // ------------------------------------------------------------------------------------------
-// K2 / K7: tile pass.  Persistent CTAs walk tiles tau = blockIdx.x + m*gridDim.x through a
-// 3-stage shared-memory ring filled and drained by TMA bulk copies (cp.async.bulk, mbarrier
-// complete_tx; bulk stores with bulk_group read-completion before a stage is refilled).
-//
-// tile tau: i0 = pdep(tau, free_mask); chunk u (u < 2^h) = amplitudes [i0 ^ off[u], +2^c);
-// tile-local index l = (u << c) | w.  Within a tile the pass's rotations are applied sub-group
-// by sub-group (ps_internal.h DevSub): each thread loads its 16-amplitude coset
-// r ^ span{u_0..u_3} from shared memory into registers, applies every rotation of the
-// sub-group there (pairs (d, d ^ dx), compile-time unrolled per dx), and writes it back.
+// sub-group arithmetic shared by both tile kernels
 
-constexpr int kStages = 3;
-constexpr int kTileMaxThreads = 512;
+__host__ __device__ constexpr int hibit(int v) { return v >= 8 ? 3 : v >= 4 ? 2 : v >= 2 ? 1 : 0; }
 
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-    return (uint32_t)__cvta_generic_to_shared(p);
+template <int REAL, typename T, int DX>
+__device__ __forceinline__ void sub_pairs(T (&vr)[kSubAmps], T (&vi)[kSubAmps], uint32_t M, T c, T b) {
+    constexpr int piv = hibit(DX);
+#pragma unroll
+    for (int d = 0; d < kSubAmps; ++d) {
+        if ((d >> piv) & 1) continue;
+        const int e = d ^ DX;
+        rot_pair<REAL>(vr[d], vi[d], vr[e], vi[e], c, flip(b, (int)((M >> d) & 1u)));
+    }
 }
+
+template <int REAL, typename T>
+__device__ __forceinline__ void sub_rotation(T (&vr)[kSubAmps], T (&vi)[kSubAmps], uint32_t dx, uint32_t M, T c,
+                                             T b) {
+    switch (dx) {
+    case 0:
+#pragma unroll
+        for (int d = 0; d < kSubAmps; ++d) rot_diag<REAL>(vr[d], vi[d], c, flip(b, (int)((M >> d) & 1u)));
+        break;
+    case 1: sub_pairs<REAL, T, 1>(vr, vi, M, c, b); break;
+    case 2: sub_pairs<REAL, T, 2>(vr, vi, M, c, b); break;
+    case 3: sub_pairs<REAL, T, 3>(vr, vi, M, c, b); break;
+    case 4: sub_pairs<REAL, T, 4>(vr, vi, M, c, b); break;
+    case 5: sub_pairs<REAL, T, 5>(vr, vi, M, c, b); break;
+    case 6: sub_pairs<REAL, T, 6>(vr, vi, M, c, b); break;
+    case 7: sub_pairs<REAL, T, 7>(vr, vi, M, c, b); break;
+    case 8: sub_pairs<REAL, T, 8>(vr, vi, M, c, b); break;
+    case 9: sub_pairs<REAL, T, 9>(vr, vi, M, c, b); break;
+    case 10: sub_pairs<REAL, T, 10>(vr, vi, M, c, b); break;
+    case 11: sub_pairs<REAL, T, 11>(vr, vi, M, c, b); break;
+    case 12: sub_pairs<REAL, T, 12>(vr, vi, M, c, b); break;
+    case 13: sub_pairs<REAL, T, 13>(vr, vi, M, c, b); break;
+    case 14: sub_pairs<REAL, T, 14>(vr, vi, M, c, b); break;
+    default: sub_pairs<REAL, T, 15>(vr, vi, M, c, b); break;
+    }
+}
+
+// applies the rotations [rb, rb + nr) of a sub-group to the thread's 16 registers
+template <typename T>
+__device__ __forceinline__ void sub_apply(T (&vr)[kSubAmps], T (&vi)[kSubAmps], const DevTRot* __restrict__ trots,
+                                          int rb, int nr, uint32_t r, uint64_t i0) {
+    for (int q = 0; q < nr; ++q) {
+        const DevTRot* tr = trots + rb + q;
+        const uint32_t dx = __ldg(&tr->dx);
+        const int s0 = par32(__ldg(&tr->zr) & r) ^ par64(__ldg(&tr->zt) & i0);
+        // fold the thread's sign into M: bit d of Ms = sigma of element d
+        const uint32_t Ms = __ldg(&tr->M) ^ (s0 ? 0xffffu : 0u);
+        const T c = (T)__ldg(&tr->c), b = (T)__ldg(&tr->b);
+        if (__ldg(&tr->real))
+            sub_rotation<1, T>(vr, vi, dx, Ms, c, b);
+        else
+            sub_rotation<0, T>(vr, vi, dx, Ms, c, b);
+    }
+}
+
+struct SubHdr {
+    uint32_t u[kSubDim];
+    uint32_t r;  // this thread's coset representative
+    int rb, nr;
+};
+
+__device__ __forceinline__ SubHdr load_sub(const DevSub* __restrict__ sp, uint32_t tid) {
+    SubHdr h;
+#pragma unroll
+    for (int b = 0; b < kSubDim; ++b) h.u[b] = __ldg(&sp->u[b]);
+    const uint32_t piv = __ldg(&sp->piv);
+    h.rb = __ldg(&sp->rot_begin);
+    h.nr = __ldg(&sp->nrot);
+    uint32_t r = tid;  // thread index with zero bits inserted at the ascending pivots
+#pragma unroll
+    for (int b = 0; b < kSubDim; ++b) {
+        const uint32_t p = (piv >> (8 * b)) & 0xffu;
+        r = ((r >> p) << (p + 1)) | (r & ((1u << p) - 1u));
+    }
+    h.r = r;
+    return h;
+}
+
+__device__ __forceinline__ uint32_t sub_local(const SubHdr& h, int d) {
+    uint32_t l = h.r;
+#pragma unroll
+    for (int b = 0; b < kSubDim; ++b)
+        if ((d >> b) & 1) l ^= h.u[b];
+    return l;
+}
+
+template <typename T>
+struct SmemAmp;
+template <>
+struct SmemAmp<double> {
+    using V = double2;
+};
+template <>
+struct SmemAmp<float> {
+    using V = float2;
+};
 
 __device__ __forceinline__ uint64_t pdep64(uint64_t v, uint64_t mask) {
     uint64_t out = 0;
@@ -334,6 +386,97 @@ __device__ __forceinline__ uint64_t pdep64(uint64_t v, uint64_t mask) {
         v >>= 1;
     }
     return out;
+}
+
+// ------------------------------------------------------------------------------------------
+// K2 / K7 (default): register-direct coset tile pass.
+//
+// tile tau: i0 = pdep(tau, free_mask); tile-local index l = (u << c) | w <-> global index
+// i0 ^ off[u] | w (chunk u of 2^c contiguous amplitudes).  Sub-group 0 gathers its 16
+// amplitudes per thread straight from HBM (consecutive threads own consecutive tile-local
+// indices, so each warp load covers contiguous 256-B chunks), the last sub-group scatters
+// straight back; shared memory holds the tile only between sub-groups.
+
+constexpr int kCosetThreads = 256;
+
+template <typename T>
+__global__ void __launch_bounds__(kCosetThreads, 2)
+    k_coset(T* __restrict__ a, int kbits, int cbits, uint64_t free_mask, const uint64_t* __restrict__ offs,
+            uint64_t ntiles, const DevSub* __restrict__ subs, int nsub, const DevTRot* __restrict__ trots) {
+    using V2 = typename SmemAmp<T>::V;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    const int hbits = kbits - cbits;
+    uint64_t* soff = reinterpret_cast<uint64_t*>(smem_raw);
+    V2* tile = reinterpret_cast<V2*>(smem_raw + (sizeof(uint64_t) << hbits));
+    const uint32_t tid = threadIdx.x;
+    const uint32_t cmask = (1u << cbits) - 1u;
+    for (uint32_t u = tid; u < (1u << hbits); u += blockDim.x) soff[u] = __ldg(&offs[u]);
+    __syncthreads();
+    V2* g = reinterpret_cast<V2*>(a);
+    for (uint64_t tau = blockIdx.x; tau < ntiles; tau += gridDim.x) {
+        const uint64_t i0 = pdep64(tau, free_mask);
+        T vr[kSubAmps], vi[kSubAmps];
+        for (int s = 0; s < nsub; ++s) {
+            const SubHdr h = load_sub(subs + s, tid);
+            if (s == 0) {
+                uint64_t gi[kSubAmps];
+#pragma unroll
+                for (int d = 0; d < kSubAmps; ++d) {
+                    const uint32_t l = sub_local(h, d);
+                    gi[d] = (i0 ^ soff[l >> cbits]) | (l & cmask);
+                }
+                V2 v[kSubAmps];
+#pragma unroll
+                for (int d = 0; d < kSubAmps; ++d) v[d] = __ldcs(&g[gi[d]]);
+#pragma unroll
+                for (int d = 0; d < kSubAmps; ++d) {
+                    vr[d] = v[d].x;
+                    vi[d] = v[d].y;
+                }
+            } else {
+#pragma unroll
+                for (int d = 0; d < kSubAmps; ++d) {
+                    const V2 v = tile[sub_local(h, d)];
+                    vr[d] = v.x;
+                    vi[d] = v.y;
+                }
+            }
+            sub_apply<T>(vr, vi, trots, h.rb, h.nr, h.r, i0);
+            if (s == nsub - 1) {
+#pragma unroll
+                for (int d = 0; d < kSubAmps; ++d) {
+                    const uint32_t l = sub_local(h, d);
+                    V2 v;
+                    v.x = vr[d];
+                    v.y = vi[d];
+                    __stcs(&g[(i0 ^ soff[l >> cbits]) | (l & cmask)], v);
+                }
+            } else {
+#pragma unroll
+                for (int d = 0; d < kSubAmps; ++d) {
+                    V2 v;
+                    v.x = vr[d];
+                    v.y = vi[d];
+                    tile[sub_local(h, d)] = v;
+                }
+                __syncthreads();
+            }
+        }
+        if (nsub > 1) __syncthreads();  // last sub-group's shared reads before the next tile's writes
+    }
+}
+
+// ------------------------------------------------------------------------------------------
+// K2 / K7 (TMA variant): persistent CTAs walk tiles through a 3-stage shared-memory ring filled
+// and drained by TMA bulk copies (cp.async.bulk, mbarrier complete_tx; bulk stores with
+// bulk_group read-completion before a stage is refilled); every sub-group goes through shared
+// memory.
+
+constexpr int kStages = 3;
+constexpr int kTileMaxThreads = 512;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
 }
 
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
@@ -350,112 +493,10 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 }
 
 template <typename T>
-struct SmemAmp;
-template <>
-struct SmemAmp<double> {
-    using V = double2;
-};
-template <>
-struct SmemAmp<float> {
-    using V = float2;
-};
-
-__host__ __device__ constexpr int hibit(int v) { return v >= 8 ? 3 : v >= 4 ? 2 : v >= 2 ? 1 : 0; }
-
-template <typename T, int DX>
-__device__ __forceinline__ void sub_pairs(T (&vr)[kSubAmps], T (&vi)[kSubAmps], uint32_t M, int s0, T c, T br,
-                                          T bi) {
-    constexpr int piv = hibit(DX);
-#pragma unroll
-    for (int d = 0; d < kSubAmps; ++d) {
-        if ((d >> piv) & 1) continue;
-        const int e = d ^ DX;
-        const int s = s0 ^ (int)((M >> d) & 1u);
-        rot_pair(vr[d], vi[d], vr[e], vi[e], c, flip(br, s), flip(bi, s));
-    }
-}
-
-template <typename T>
-__device__ __forceinline__ void sub_rotation(T (&vr)[kSubAmps], T (&vi)[kSubAmps], uint32_t dx, uint32_t M, int s0,
-                                             T c, T br, T bi) {
-    switch (dx) {
-    case 0:
-#pragma unroll
-        for (int d = 0; d < kSubAmps; ++d) {
-            const int s = s0 ^ (int)((M >> d) & 1u);
-            rot_diag(vr[d], vi[d], c, flip(br, s), flip(bi, s));
-        }
-        break;
-    case 1: sub_pairs<T, 1>(vr, vi, M, s0, c, br, bi); break;
-    case 2: sub_pairs<T, 2>(vr, vi, M, s0, c, br, bi); break;
-    case 3: sub_pairs<T, 3>(vr, vi, M, s0, c, br, bi); break;
-    case 4: sub_pairs<T, 4>(vr, vi, M, s0, c, br, bi); break;
-    case 5: sub_pairs<T, 5>(vr, vi, M, s0, c, br, bi); break;
-    case 6: sub_pairs<T, 6>(vr, vi, M, s0, c, br, bi); break;
-    case 7: sub_pairs<T, 7>(vr, vi, M, s0, c, br, bi); break;
-    case 8: sub_pairs<T, 8>(vr, vi, M, s0, c, br, bi); break;
-    case 9: sub_pairs<T, 9>(vr, vi, M, s0, c, br, bi); break;
-    case 10: sub_pairs<T, 10>(vr, vi, M, s0, c, br, bi); break;
-    case 11: sub_pairs<T, 11>(vr, vi, M, s0, c, br, bi); break;
-    case 12: sub_pairs<T, 12>(vr, vi, M, s0, c, br, bi); break;
-    case 13: sub_pairs<T, 13>(vr, vi, M, s0, c, br, bi); break;
-    case 14: sub_pairs<T, 14>(vr, vi, M, s0, c, br, bi); break;
-    default: sub_pairs<T, 15>(vr, vi, M, s0, c, br, bi); break;
-    }
-}
-
-template <typename T>
-__device__ __forceinline__ void apply_subgroup(T* __restrict__ tile, const DevSub* __restrict__ sp,
-                                               const DevTRot* __restrict__ trots, uint32_t tid, uint64_t i0) {
-    using V2 = typename SmemAmp<T>::V;
-    V2* t2 = reinterpret_cast<V2*>(tile);
-    uint32_t u[kSubDim];
-#pragma unroll
-    for (int b = 0; b < kSubDim; ++b) u[b] = __ldg(&sp->u[b]);
-    const uint32_t piv = __ldg(&sp->piv);
-    const int rb = __ldg(&sp->rot_begin), nr = __ldg(&sp->nrot);
-    // representative: thread index with zero bits inserted at the (ascending) pivots
-    uint32_t r = tid;
-#pragma unroll
-    for (int b = 0; b < kSubDim; ++b) {
-        const uint32_t p = (piv >> (8 * b)) & 0xffu;
-        r = ((r >> p) << (p + 1)) | (r & ((1u << p) - 1u));
-    }
-    T vr[kSubAmps], vi[kSubAmps];
-#pragma unroll
-    for (int d = 0; d < kSubAmps; ++d) {
-        uint32_t l = r;
-#pragma unroll
-        for (int b = 0; b < kSubDim; ++b)
-            if ((d >> b) & 1) l ^= u[b];
-        const V2 v = t2[l];
-        vr[d] = v.x;
-        vi[d] = v.y;
-    }
-    for (int q = 0; q < nr; ++q) {
-        const DevTRot* tr = trots + rb + q;
-        const uint32_t dx = __ldg(&tr->dx);
-        const uint32_t M = __ldg(&tr->M);
-        const int s0 = (__popc(__ldg(&tr->zr) & r) & 1) ^ (__popcll(__ldg(&tr->zt) & i0) & 1);
-        sub_rotation<T>(vr, vi, dx, M, s0, (T)__ldg(&tr->c), (T)__ldg(&tr->br), (T)__ldg(&tr->bi));
-    }
-#pragma unroll
-    for (int d = 0; d < kSubAmps; ++d) {
-        uint32_t l = r;
-#pragma unroll
-        for (int b = 0; b < kSubDim; ++b)
-            if ((d >> b) & 1) l ^= u[b];
-        V2 v;
-        v.x = vr[d];
-        v.y = vi[d];
-        t2[l] = v;
-    }
-}
-
-template <typename T>
 __global__ void __launch_bounds__(kTileMaxThreads, 1)
     k_tile(T* __restrict__ a, int kbits, int cbits, uint64_t free_mask, const uint64_t* __restrict__ offs,
            uint64_t ntiles, const DevSub* __restrict__ subs, int nsub, const DevTRot* __restrict__ trots) {
+    using V2 = typename SmemAmp<T>::V;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     __shared__ __align__(8) uint64_t mbar[kStages];
     const uint32_t tile_amps = 1u << kbits;
@@ -517,9 +558,24 @@ __global__ void __launch_bounds__(kTileMaxThreads, 1)
         }
         mbar_wait(&mbar[st], (uint32_t)((m / kStages) & 1));
         const uint64_t i0 = pdep64((uint64_t)blockIdx.x + m * gridDim.x, free_mask);
-        T* buf = stage_ptr(st);
-        for (int g = 0; g < nsub; ++g) {
-            apply_subgroup<T>(buf, subs + g, trots, tid, i0);
+        V2* buf = reinterpret_cast<V2*>(stage_ptr(st));
+        for (int s = 0; s < nsub; ++s) {
+            const SubHdr h = load_sub(subs + s, tid);
+            T vr[kSubAmps], vi[kSubAmps];
+#pragma unroll
+            for (int d = 0; d < kSubAmps; ++d) {
+                const V2 v = buf[sub_local(h, d)];
+                vr[d] = v.x;
+                vi[d] = v.y;
+            }
+            sub_apply<T>(vr, vi, trots, h.rb, h.nr, h.r, i0);
+#pragma unroll
+            for (int d = 0; d < kSubAmps; ++d) {
+                V2 v;
+                v.x = vr[d];
+                v.y = vi[d];
+                buf[sub_local(h, d)] = v;
+            }
             __syncthreads();
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -531,23 +587,26 @@ __global__ void __launch_bounds__(kTileMaxThreads, 1)
 
 // ------------------------------------------------------------------------------------------
 // K3 fallback: own element i (local index base+t) updated against the partner's OLD value at
-// local index i ^ x, held in `stage` (partner chunk starting at local index pbase).
-//   a'_i = c a_i + s A b_(i^x)
+// local index i ^ x, held in `stage` (partner chunk starting at local index pbase):
+//   a'_i = c a_i + sigma A b_(i^x)   (the first half of the pair update)
 
 template <typename T>
 __global__ void k_full_update(T* __restrict__ a, const T* __restrict__ stage, uint64_t base,
                               uint64_t count, uint64_t pbase, const DevRot* __restrict__ rec) {
     const uint64_t x = __ldg(&rec->x);
     const uint64_t z = __ldg(&rec->z);
-    const Coef<T> k = load_coef<T>(rec);
+    const RotK<T> k = load_rot<T>(rec);
     for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < count;
          t += (uint64_t)gridDim.x * blockDim.x) {
         const uint64_t i = base + t;
         const uint64_t j = (i ^ x) - pbase;
-        const int s = par64(z & i);
+        const T b = flip(k.b, par64(z & i));
         T ir = a[2 * i], ii = a[2 * i + 1];
         T jr = stage[2 * j], ji = stage[2 * j + 1];
-        rot_pair(ir, ii, jr, ji, k.c, flip(k.br, s), flip(k.bi, s));
+        if (k.real)
+            rot_pair<1>(ir, ii, jr, ji, k.c, b);
+        else
+            rot_pair<0>(ir, ii, jr, ji, k.c, b);
         a[2 * i] = ir;
         a[2 * i + 1] = ii;
     }
@@ -721,6 +780,29 @@ cudaError_t launch_stream_t(T* a, int nl, const Pass& p, const DevRot* d_rots, c
 }
 
 template <typename T>
+cudaError_t launch_coset_t(T* a, int nl, const Pass& p, const DevSub* d_subs, const DevTRot* d_trots,
+                           const uint64_t* d_offs, cudaStream_t s) {
+    const size_t smem = (sizeof(uint64_t) << (p.kbits - p.cbits)) + ((size_t)(2 * sizeof(T)) << p.kbits);
+    static bool attr_done[2] = {false, false};
+    const int which = sizeof(T) == 8 ? 0 : 1;
+    if (!attr_done[which]) {
+        cudaFuncSetAttribute(k_coset<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        attr_done[which] = true;
+    }
+    const int threads = 1 << (p.kbits - kSubDim);
+    if (threads > kCosetThreads) return cudaErrorInvalidValue;
+    int occ = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_coset<T>, threads, smem);
+    if (occ < 1) occ = 1;
+    const uint64_t ntiles = 1ull << (nl - p.kbits);
+    const uint64_t cap = (uint64_t)num_sms() * (uint64_t)occ * 4;
+    const unsigned grid = (unsigned)(ntiles < cap ? ntiles : cap);
+    k_coset<T><<<grid, threads, smem, s>>>(a, p.kbits, p.cbits, p.free_mask, d_offs + p.off_begin, ntiles,
+                                           d_subs + p.sub_begin, p.sub_count, d_trots);
+    return cudaGetLastError();
+}
+
+template <typename T>
 cudaError_t launch_tile_t(T* a, int nl, const Pass& p, const DevSub* d_subs, const DevTRot* d_trots,
                           const uint64_t* d_offs, cudaStream_t s) {
     const size_t stage_bytes = (size_t)(2 * sizeof(T)) << p.kbits;
@@ -768,9 +850,13 @@ cudaError_t launch_stream(int dtype, void* a, int nl, const Pass& p, const DevRo
 }
 
 cudaError_t launch_tile(int dtype, void* a, int nl, const Pass& p, const DevSub* d_subs, const DevTRot* d_trots,
-                        const uint64_t* d_offs, cudaStream_t s) {
-    if (dtype == PS_C128) return launch_tile_t<double>((double*)a, nl, p, d_subs, d_trots, d_offs, s);
-    return launch_tile_t<float>((float*)a, nl, p, d_subs, d_trots, d_offs, s);
+                        const uint64_t* d_offs, int use_tma, cudaStream_t s) {
+    if (use_tma) {
+        if (dtype == PS_C128) return launch_tile_t<double>((double*)a, nl, p, d_subs, d_trots, d_offs, s);
+        return launch_tile_t<float>((float*)a, nl, p, d_subs, d_trots, d_offs, s);
+    }
+    if (dtype == PS_C128) return launch_coset_t<double>((double*)a, nl, p, d_subs, d_trots, d_offs, s);
+    return launch_coset_t<float>((float*)a, nl, p, d_subs, d_trots, d_offs, s);
 }
 
 cudaError_t launch_full_update(int dtype, void* a, const void* stage, uint64_t base, uint64_t count, uint64_t pbase,

@@ -45,21 +45,20 @@ int validate_rotations(int n, const uint64_t* x, const uint64_t* z, const double
 // ------------------------------------------------------------------------------------------
 // record construction
 
-// B = sign * sin(phi) * i^(y+1)   (see DevRot)
+// B = sign * sin(phi) * i^(y+1)   (see DevRot): i^1 = i, i^2 = -1, i^3 = -i, i^4 = 1
 static DevRot make_rec(uint64_t x, uint64_t z, uint64_t zt, int y, int sign, double phi) {
     DevRot r{};
     r.x = x;
     r.z = z;
     r.zt = zt;
-    const double c = std::cos(phi);
     const double s = std::sin(phi) * (double)sign;
     switch ((y + 1) & 3) {
-    case 0: r.br = s; r.bi = 0.0; break;
-    case 1: r.br = 0.0; r.bi = s; break;
-    case 2: r.br = -s; r.bi = 0.0; break;
-    default: r.br = 0.0; r.bi = -s; break;
+    case 0: r.real = 1; r.b = s; break;
+    case 1: r.real = 0; r.b = s; break;
+    case 2: r.real = 1; r.b = -s; break;
+    default: r.real = 0; r.b = -s; break;
     }
-    r.c = c;
+    r.c = std::cos(phi);
     r.pad = 0;
     return r;
 }
@@ -177,8 +176,8 @@ static void make_subgroups(const std::vector<LocalRot>& lr, int k, Plan* plan, P
             tr.zr = (uint32_t)L.z;
             tr.zt = L.zt;
             tr.c = r.c;
-            tr.br = r.br;
-            tr.bi = r.bi;
+            tr.b = r.b;
+            tr.real = r.real;
             plan->trots.push_back(tr);
         }
         plan->subs.push_back(sub);

@@ -12,26 +12,27 @@
 namespace ps {
 
 // ------------------------------------------------------------------------------------------
-// Device rotation record (one per rotation per pass), 56 bytes.
+// Device rotation record (one per rotation per pass), 48 bytes.
 //
-// A pass applies rotations to pairs {i, i xor x} in PHYSICAL local coordinates (for K1 the
-// physical local index; for tile passes the tile-local index).  With B = sign * sin(phi) *
-// i^(y+1) (y = popc(x & z) of the ORIGINAL logical string) and
-// sigma = (-1)^(popc(z & i) [xor tile sign]) the update is (R3)
-//     a'_i = c a_i + sigma * A a_j,   A = (-br, bi)   (= i sin(phi) conj(i^y))
-//     a'_j = c a_j + sigma * B a_i,   B = ( br, bi)   (= i sin(phi) i^y)
-// where i is the member whose pivot bit (highest bit of x) is 0.  For x = 0 (diagonal) the
-// element update is a' = c a + sigma * A a.
+// A pass applies rotations to pairs {i, i xor x} in PHYSICAL local coordinates.  With
+// B = sign * sin(phi) * i^(y+1) (y = popc(x & z) of the ORIGINAL logical string),
+// A = -conj(B) and sigma = (-1)^(popc(z & i) [xor tile sign]) the update is
+// (R3)
+//     a'_i = c a_i + sigma * A a_j      (= c a_i + i sin(phi) w(j) a_j,  w(j) = conj w(i))
+//     a'_j = c a_j + sigma * B a_i      (= c a_j + i sin(phi) w(i) a_i)
+// where i is the member whose pivot bit (highest bit of x) is 0.  B is purely real
+// (y odd: B = b) or purely imaginary (y even: B = i b), so each pair costs 4 multiplies and
+// 4 fused multiply-adds.  For x = 0 (diagonal, y = 0) the element update is a' = c a + sigma A a.
 struct DevRot {
-    uint64_t x;   // xor mask (physical local, or tile-local for tile passes)
-    uint64_t z;   // phase mask in the same coordinates
-    uint64_t zt;  // tile passes: z restricted to the tile-enumeration bits (tile sign); else 0
-    double c;     // cos(phi)
-    double br;    // Re B
-    double bi;    // Im B
-    uint64_t pad; // keeps 8-byte fields aligned to 64 B records
+    uint64_t x;    // xor mask (physical local)
+    uint64_t z;    // phase mask in the same coordinates
+    uint64_t zt;   // unused by K1 (0)
+    double c;      // cos(phi)
+    double b;      // B = b (real) or i b (imaginary)
+    uint32_t real; // 1: B real, 0: B imaginary
+    uint32_t pad;
 };
-static_assert(sizeof(DevRot) == 56 || sizeof(DevRot) == 64, "DevRot layout");
+static_assert(sizeof(DevRot) == 48, "DevRot layout");
 
 // Tile passes (K2/K7) apply their rotations in SUB-GROUPS: consecutive rotations whose
 // tile-local xor masks span <= kSubDim dimensions.  For a sub-group with basis u_0..u_3
@@ -53,16 +54,16 @@ static_assert(sizeof(DevSub) == 32, "DevSub layout");
 
 // one rotation of a sub-group: pair (d, d xor dx) of the thread's 16 registers ("i" member: bit
 // highest(dx) of d is 0), sigma = parity(zr & r) xor parity(zt & i0) xor bit d of M, with
-// M bit d = parity(Dz & d), Dz_b = parity(Z_loc & u_b); c, br, bi as in DevRot.
+// M bit d = parity(Dz & d), Dz_b = parity(Z_loc & u_b); c, b, real as in DevRot.
 struct DevTRot {
-    uint32_t dx;  // 0: diagonal
+    uint32_t dx;   // 0: diagonal
     uint32_t M;
-    uint32_t zr;  // tile-local phase mask (parity with the coset representative r)
-    uint32_t pad;
-    uint64_t zt;  // phase mask on the tile-enumeration bits (parity with the tile base i0)
-    double c, br, bi;
+    uint32_t zr;   // tile-local phase mask (parity with the coset representative r)
+    uint32_t real; // as DevRot
+    uint64_t zt;   // phase mask on the tile-enumeration bits (parity with the tile base i0)
+    double c, b;
 };
-static_assert(sizeof(DevTRot) == 48, "DevTRot layout");
+static_assert(sizeof(DevTRot) == 40, "DevTRot layout");
 
 // expectation term record: contribution sigma(i) * (kr * tr + ki * ti) per pair (x != 0) with
 // t = conj(a_j) a_i, or sigma(i) * kr * |a_i|^2 per element (x = 0)
