@@ -47,6 +47,7 @@ def parse():
     ap.add_argument("--dtype", default="c128", choices=["c128", "c64"])
     ap.add_argument("--fusion", type=int, default=2)
     ap.add_argument("--tile-bits", type=int, default=0)
+    ap.add_argument("--tile-mode", type=int, default=2, help="0 TMA prefetch, 1 TMA ring, 2 register-direct")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     return ap.parse_args()
@@ -225,6 +226,7 @@ def run_ours(args):
     st.set_option(ps.OPT_FUSION, args.fusion)
     if args.tile_bits:
         st.set_option(ps.OPT_TILE_BITS, args.tile_bits)
+    st.set_option(ps.OPT_TILE_TMA, args.tile_mode)
     st.set_option(ps.OPT_PROFILE, 1)
     lay = layers(args, args.warmup + args.steps)
     enc = [P.pauli_encode_codes(c) + (a,) for c, a in lay]
@@ -313,7 +315,8 @@ def run_ours(args):
             "scaling": "strong", "vs_baseline": None, "dtype": "f64" if args.dtype == "c128" else "f32",
             "data": "synthetic",
             "config": {"workload": workload_name(args), "n_qubits": args.n, "rotations_per_step": args.layer,
-                       "fusion": args.fusion, "parallelism": f"state sharded over {world} GPU(s) by top qubits",
+                       "fusion": args.fusion, "tile_mode": args.tile_mode, "tile_bits": args.tile_bits or 11,
+                       "parallelism": f"state sharded over {world} GPU(s) by top qubits",
                        "l2": "inputs larger than L2 (state %.1f GiB per GPU)" % (local_state / 2 ** 30)},
             "hbm_gbs": hbm_alg,
             "bytes_per_rotation": stats["algo_bytes"]["stream"] / max(1, stats["rotations_by"]["stream"])

@@ -83,11 +83,14 @@ typedef struct ps_stats {
 enum {
     PS_OPT_PROFILE = 0,       /* 1: time every launch with CUDA events on the handle's stream (default 0) */
     PS_OPT_FUSION = 1,        /* 0: one rotation per pass (K1 only); 1: same-x runs; 2: + tiles (default 2) */
-    PS_OPT_TILE_BITS = 2,     /* log2 amplitudes per fused tile, 4..12 (default 12) */
+    PS_OPT_TILE_BITS = 2,     /* log2 amplitudes per fused tile, 4..12 (default 11) */
     PS_OPT_CHUNK_BYTES = 3,   /* exchange chunk size in bytes (default 256 MiB) */
     PS_OPT_MAX_PASS_ROTS = 4, /* cap on rotations fused into one tile pass (default 64) */
     PS_OPT_VEC256 = 5,        /* 1: 256-bit LDG/STG in K1 (default 1); 0: 128-bit */
-    PS_OPT_TILE_TMA = 6       /* 1: tile passes stage whole tiles through a TMA ring (A/B); default 0 */
+    PS_OPT_TILE_TMA = 6       /* tile-pass kernel: 2 = register-direct (default): first sub-group
+                                 loads from HBM, last stores to HBM, smem between sub-groups;
+                                 0 = TMA-prefetched double buffer; 1 = 3-stage TMA ring
+                                 (0 and 1 kept for A/B) */
 };
 
 /* ------------------------------------------------------------------------------------------ */

@@ -79,7 +79,7 @@ struct ps_state {
     size_t xstage_bytes = 0;
     size_t chunk_bytes = 256ull << 20;
     // options
-    int profile = 0, fusion = 2, tile_bits = 12, vec256 = 1, max_pass_rots = 1 << 30, tile_tma = 0;
+    int profile = 0, fusion = 2, tile_bits = 11, vec256 = 1, max_pass_rots = 1 << 30, tile_tma = 2;
     ps_stats stats{};
     std::vector<PendingTiming> pending;
     std::vector<cudaEvent_t> event_pool;
@@ -231,7 +231,7 @@ extern "C" int ps_create_ex(int n_qubits, int dtype, void* dev_buf, size_t bytes
     h->world = world;
     h->dtype = dtype;
     h->amp_bytes = dtype == PS_C128 ? 16 : 8;
-    h->tile_bits = 12;
+    h->tile_bits = 11;
     cudaError_t e = cudaGetDevice(&h->device);
     if (e != cudaSuccess) {
         delete h;
@@ -332,7 +332,10 @@ extern "C" int ps_set_option(ps_handle h, int option, int64_t value) {
         h->max_pass_rots = (int)std::min<int64_t>(value, 1 << 30);
         break;
     case PS_OPT_VEC256: h->vec256 = value ? 1 : 0; break;
-    case PS_OPT_TILE_TMA: h->tile_tma = value ? 1 : 0; break;
+    case PS_OPT_TILE_TMA:
+        if (value < 0 || value > 2) return fail(PS_EINVAL, "tile mode must be 0, 1 or 2");
+        h->tile_tma = (int)value;
+        break;
     default: return fail(PS_EINVAL, "unknown option");
     }
     return PS_OK;

@@ -399,6 +399,11 @@ __device__ __forceinline__ uint64_t pdep64(uint64_t v, uint64_t mask) {
 
 constexpr int kCosetThreads = 256;
 
+// chunk-offset table size in shared memory, rounded up so the tile that follows is 128-B aligned
+__host__ __device__ inline size_t coset_off_bytes(int hbits) {
+    return ((sizeof(uint64_t) << hbits) + 127) & ~(size_t)127;
+}
+
 template <typename T>
 __global__ void __launch_bounds__(kCosetThreads, 2)
     k_coset(T* __restrict__ a, int kbits, int cbits, uint64_t free_mask, const uint64_t* __restrict__ offs,
@@ -407,7 +412,7 @@ __global__ void __launch_bounds__(kCosetThreads, 2)
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int hbits = kbits - cbits;
     uint64_t* soff = reinterpret_cast<uint64_t*>(smem_raw);
-    V2* tile = reinterpret_cast<V2*>(smem_raw + (sizeof(uint64_t) << hbits));
+    V2* tile = reinterpret_cast<V2*>(smem_raw + coset_off_bytes(hbits));
     const uint32_t tid = threadIdx.x;
     const uint32_t cmask = (1u << cbits) - 1u;
     for (uint32_t u = tid; u < (1u << hbits); u += blockDim.x) soff[u] = __ldg(&offs[u]);
@@ -463,6 +468,111 @@ __global__ void __launch_bounds__(kCosetThreads, 2)
             }
         }
         if (nsub > 1) __syncthreads();  // last sub-group's shared reads before the next tile's writes
+    }
+}
+
+// ------------------------------------------------------------------------------------------
+// K2 / K7 (default): TMA-prefetched coset tile pass.  Each persistent CTA double-buffers tiles in
+// shared memory: while the sub-groups of tile m run on buffer m&1 (in place, the last one storing
+// straight to HBM), the TMA engine fills buffer (m+1)&1 with tile m+1 -- one cp.async.bulk per
+// 2^c-amplitude chunk, issued by all threads, completion on an mbarrier (complete_tx).
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void mbar_wait_parity(uint64_t* bar, uint32_t parity) {
+    uint32_t done = 0;
+    while (!done) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done)
+            : "r"(smem_addr(bar)), "r"(parity)
+            : "memory");
+    }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kCosetThreads, 1)
+    k_coset_pf(T* __restrict__ a, int kbits, int cbits, uint64_t free_mask, const uint64_t* __restrict__ offs,
+               uint64_t ntiles, const DevSub* __restrict__ subs, int nsub, const DevTRot* __restrict__ trots) {
+    using V2 = typename SmemAmp<T>::V;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    __shared__ __align__(8) uint64_t mbar[2];
+    const int hbits = kbits - cbits;
+    const uint32_t tile_bytes = (uint32_t)(2 * sizeof(T)) << kbits;
+    const uint32_t chunk_bytes = (uint32_t)(2 * sizeof(T)) << cbits;
+    const uint32_t nchunks = 1u << hbits;
+    uint64_t* soff = reinterpret_cast<uint64_t*>(smem_raw);
+    unsigned char* bufs = smem_raw + coset_off_bytes(hbits);
+    const uint32_t tid = threadIdx.x;
+    const uint32_t cmask = (1u << cbits) - 1u;
+    const uint64_t my_tiles = ntiles > blockIdx.x ? (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+    for (uint32_t u = tid; u < nchunks; u += blockDim.x) soff[u] = __ldg(&offs[u]);
+    if (tid == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&mbar[0])));
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&mbar[1])));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    auto prefetch = [&](uint64_t m) {
+        const uint64_t i0 = pdep64((uint64_t)blockIdx.x + m * gridDim.x, free_mask);
+        const int b = (int)(m & 1);
+        unsigned char* dst = bufs + (size_t)b * tile_bytes;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        if (tid == 0)
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(&mbar[b])),
+                         "r"(tile_bytes)
+                         : "memory");
+        for (uint32_t u = tid; u < nchunks; u += blockDim.x) {
+            const T* src = a + 2 * (i0 ^ soff[u]);
+            asm volatile(
+                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                    smem_addr(dst + (size_t)u * chunk_bytes)),
+                "l"(src), "r"(chunk_bytes), "r"(smem_addr(&mbar[b]))
+                : "memory");
+        }
+    };
+    V2* g = reinterpret_cast<V2*>(a);
+    if (my_tiles > 0) prefetch(0);
+    for (uint64_t m = 0; m < my_tiles; ++m) {
+        if (m + 1 < my_tiles) prefetch(m + 1);  // buffer (m+1)&1 was released by the barrier ending tile m-1
+        const int b = (int)(m & 1);
+        mbar_wait_parity(&mbar[b], (uint32_t)((m >> 1) & 1));
+        V2* tile = reinterpret_cast<V2*>(bufs + (size_t)b * tile_bytes);
+        const uint64_t i0 = pdep64((uint64_t)blockIdx.x + m * gridDim.x, free_mask);
+        for (int s = 0; s < nsub; ++s) {
+            const SubHdr h = load_sub(subs + s, tid);
+            T vr[kSubAmps], vi[kSubAmps];
+#pragma unroll
+            for (int d = 0; d < kSubAmps; ++d) {
+                const V2 v = tile[sub_local(h, d)];
+                vr[d] = v.x;
+                vi[d] = v.y;
+            }
+            sub_apply<T>(vr, vi, trots, h.rb, h.nr, h.r, i0);
+            if (s == nsub - 1) {
+#pragma unroll
+                for (int d = 0; d < kSubAmps; ++d) {
+                    const uint32_t l = sub_local(h, d);
+                    V2 v;
+                    v.x = vr[d];
+                    v.y = vi[d];
+                    __stcs(&g[(i0 ^ soff[l >> cbits]) | (l & cmask)], v);
+                }
+            } else {
+#pragma unroll
+                for (int d = 0; d < kSubAmps; ++d) {
+                    V2 v;
+                    v.x = vr[d];
+                    v.y = vi[d];
+                    tile[sub_local(h, d)] = v;
+                }
+            }
+            __syncthreads();
+        }
     }
 }
 
@@ -782,7 +892,7 @@ cudaError_t launch_stream_t(T* a, int nl, const Pass& p, const DevRot* d_rots, c
 template <typename T>
 cudaError_t launch_coset_t(T* a, int nl, const Pass& p, const DevSub* d_subs, const DevTRot* d_trots,
                            const uint64_t* d_offs, cudaStream_t s) {
-    const size_t smem = (sizeof(uint64_t) << (p.kbits - p.cbits)) + ((size_t)(2 * sizeof(T)) << p.kbits);
+    const size_t smem = coset_off_bytes(p.kbits - p.cbits) + ((size_t)(2 * sizeof(T)) << p.kbits);
     static bool attr_done[2] = {false, false};
     const int which = sizeof(T) == 8 ? 0 : 1;
     if (!attr_done[which]) {
@@ -799,6 +909,28 @@ cudaError_t launch_coset_t(T* a, int nl, const Pass& p, const DevSub* d_subs, co
     const unsigned grid = (unsigned)(ntiles < cap ? ntiles : cap);
     k_coset<T><<<grid, threads, smem, s>>>(a, p.kbits, p.cbits, p.free_mask, d_offs + p.off_begin, ntiles,
                                            d_subs + p.sub_begin, p.sub_count, d_trots);
+    return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t launch_coset_pf_t(T* a, int nl, const Pass& p, const DevSub* d_subs, const DevTRot* d_trots,
+                              const uint64_t* d_offs, cudaStream_t s) {
+    const size_t smem = coset_off_bytes(p.kbits - p.cbits) + 2 * ((size_t)(2 * sizeof(T)) << p.kbits);
+    static bool attr_done[2] = {false, false};
+    const int which = sizeof(T) == 8 ? 0 : 1;
+    if (!attr_done[which]) {
+        cudaFuncSetAttribute(k_coset_pf<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        attr_done[which] = true;
+    }
+    const int threads = 1 << (p.kbits - kSubDim);
+    int occ = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_coset_pf<T>, threads, smem);
+    if (occ < 1) occ = 1;
+    const uint64_t ntiles = 1ull << (nl - p.kbits);
+    const uint64_t cap = (uint64_t)num_sms() * (uint64_t)occ;
+    const unsigned grid = (unsigned)(ntiles < cap ? ntiles : cap);
+    k_coset_pf<T><<<grid, threads, smem, s>>>(a, p.kbits, p.cbits, p.free_mask, d_offs + p.off_begin, ntiles,
+                                              d_subs + p.sub_begin, p.sub_count, d_trots);
     return cudaGetLastError();
 }
 
@@ -851,12 +983,16 @@ cudaError_t launch_stream(int dtype, void* a, int nl, const Pass& p, const DevRo
 
 cudaError_t launch_tile(int dtype, void* a, int nl, const Pass& p, const DevSub* d_subs, const DevTRot* d_trots,
                         const uint64_t* d_offs, int use_tma, cudaStream_t s) {
-    if (use_tma) {
+    if (use_tma == 1) {
         if (dtype == PS_C128) return launch_tile_t<double>((double*)a, nl, p, d_subs, d_trots, d_offs, s);
         return launch_tile_t<float>((float*)a, nl, p, d_subs, d_trots, d_offs, s);
     }
-    if (dtype == PS_C128) return launch_coset_t<double>((double*)a, nl, p, d_subs, d_trots, d_offs, s);
-    return launch_coset_t<float>((float*)a, nl, p, d_subs, d_trots, d_offs, s);
+    if (use_tma == 2) {
+        if (dtype == PS_C128) return launch_coset_t<double>((double*)a, nl, p, d_subs, d_trots, d_offs, s);
+        return launch_coset_t<float>((float*)a, nl, p, d_subs, d_trots, d_offs, s);
+    }
+    if (dtype == PS_C128) return launch_coset_pf_t<double>((double*)a, nl, p, d_subs, d_trots, d_offs, s);
+    return launch_coset_pf_t<float>((float*)a, nl, p, d_subs, d_trots, d_offs, s);
 }
 
 cudaError_t launch_full_update(int dtype, void* a, const void* stage, uint64_t base, uint64_t count, uint64_t pbase,
