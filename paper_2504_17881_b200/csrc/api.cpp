@@ -585,6 +585,7 @@ static PlanConfig plan_config(const ps_state* h) {
     cfg.fusion = h->fusion;
     cfg.tile_bits = h->tile_bits;
     cfg.min_chunk_bits = h->dtype == PS_C128 ? 4 : 5;  // >= 256-byte gathered chunks
+    cfg.phase_bits = h->dtype == PS_C128 ? 3 : 4;      // 16-B vs 8-B shared-memory accesses
     cfg.max_pass_rots = h->max_pass_rots;
     return cfg;
 }

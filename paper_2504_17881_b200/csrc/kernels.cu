@@ -277,62 +277,138 @@ __global__ void __launch_bounds__(kStreamThreads) k_stream(T* __restrict__ a, ui
 }
 
 // ------------------------------------------------------------------------------------------
-// sub-group arithmetic shared by both tile kernels
+// sub-group arithmetic shared by the tile kernels (deferred-scale form, ps_internal.h DevTRot):
+// each component update is one fused multiply-add; F = product of the factors is applied when
+// the amplitudes leave the registers.
 
 __host__ __device__ constexpr int hibit(int v) { return v >= 8 ? 3 : v >= 4 ? 2 : v >= 2 ? 1 : 0; }
 
-template <int REAL, typename T, int DX>
-__device__ __forceinline__ void sub_pairs(T (&vr)[kSubAmps], T (&vi)[kSubAmps], uint32_t M, T c, T b) {
+// SFORM = 0: a'_i = a_i + s*Ac a_j, a'_j = a_j + s*Bc a_i with Bc = t (REAL) or i t, Ac = -conj(Bc)
+// SFORM = 1: a'_i = t a_i + s*Ac a_j, a'_j = t a_j + s*Bc a_i with Bc = g (REAL) or i g, g = +-1
+template <int REAL, int SFORM, typename T>
+__device__ __forceinline__ void dpair(T& ir, T& ii, T& jr, T& ji, T t, int neg) {
+    if (!SFORM) {
+        const T b = flip(t, neg);
+        if (REAL) {
+            const T nir = pfma(-b, jr, ir), nii = pfma(-b, ji, ii);
+            const T njr = pfma(b, ir, jr), nji = pfma(b, ii, ji);
+            ir = nir; ii = nii; jr = njr; ji = nji;
+        } else {
+            const T nir = pfma(-b, ji, ir), nii = pfma(b, jr, ii);
+            const T njr = pfma(-b, ii, jr), nji = pfma(b, ir, ji);
+            ir = nir; ii = nii; jr = njr; ji = nji;
+        }
+    } else {
+        if (REAL) {
+            const T nir = pfma(t, ir, flip(jr, !neg)), nii = pfma(t, ii, flip(ji, !neg));
+            const T njr = pfma(t, jr, flip(ir, neg)), nji = pfma(t, ji, flip(ii, neg));
+            ir = nir; ii = nii; jr = njr; ji = nji;
+        } else {
+            const T nir = pfma(t, ir, flip(ji, !neg)), nii = pfma(t, ii, flip(jr, neg));
+            const T njr = pfma(t, jr, flip(ii, !neg)), nji = pfma(t, ji, flip(ir, neg));
+            ir = nir; ii = nii; jr = njr; ji = nji;
+        }
+    }
+}
+
+// diagonal element: a' = a + s*Ac a (SFORM 0) or t a + s*Ac a (SFORM 1)
+template <int REAL, int SFORM, typename T>
+__device__ __forceinline__ void ddiag(T& r, T& i, T t, int neg) {
+    if (!SFORM) {
+        const T b = flip(t, neg);
+        if (REAL) {
+            const T nr = pfma(-b, r, r), ni = pfma(-b, i, i);
+            r = nr; i = ni;
+        } else {
+            const T nr = pfma(-b, i, r), ni = pfma(b, r, i);
+            r = nr; i = ni;
+        }
+    } else {
+        if (REAL) {
+            const T nr = pfma(t, r, flip(r, !neg)), ni = pfma(t, i, flip(i, !neg));
+            r = nr; i = ni;
+        } else {
+            const T nr = pfma(t, r, flip(i, !neg)), ni = pfma(t, i, flip(r, neg));
+            r = nr; i = ni;
+        }
+    }
+}
+
+// Ms bit d = sigma of element d (1: -1) xor the NEG bit of SFORM rotations
+template <int REAL, int SFORM, typename T, int DX>
+__device__ __forceinline__ void sub_pairs(T (&vr)[kSubAmps], T (&vi)[kSubAmps], uint32_t Ms, T t) {
     constexpr int piv = hibit(DX);
 #pragma unroll
     for (int d = 0; d < kSubAmps; ++d) {
         if ((d >> piv) & 1) continue;
         const int e = d ^ DX;
-        rot_pair<REAL>(vr[d], vi[d], vr[e], vi[e], c, flip(b, (int)((M >> d) & 1u)));
+        dpair<REAL, SFORM>(vr[d], vi[d], vr[e], vi[e], t, (int)((Ms >> d) & 1u));
     }
 }
 
-template <int REAL, typename T>
-__device__ __forceinline__ void sub_rotation(T (&vr)[kSubAmps], T (&vi)[kSubAmps], uint32_t dx, uint32_t M, T c,
-                                             T b) {
+template <int REAL, int SFORM, typename T>
+__device__ __forceinline__ void sub_rotation(T (&vr)[kSubAmps], T (&vi)[kSubAmps], uint32_t dx, uint32_t Ms, T t) {
     switch (dx) {
     case 0:
 #pragma unroll
-        for (int d = 0; d < kSubAmps; ++d) rot_diag<REAL>(vr[d], vi[d], c, flip(b, (int)((M >> d) & 1u)));
+        for (int d = 0; d < kSubAmps; ++d) ddiag<REAL, SFORM>(vr[d], vi[d], t, (int)((Ms >> d) & 1u));
         break;
-    case 1: sub_pairs<REAL, T, 1>(vr, vi, M, c, b); break;
-    case 2: sub_pairs<REAL, T, 2>(vr, vi, M, c, b); break;
-    case 3: sub_pairs<REAL, T, 3>(vr, vi, M, c, b); break;
-    case 4: sub_pairs<REAL, T, 4>(vr, vi, M, c, b); break;
-    case 5: sub_pairs<REAL, T, 5>(vr, vi, M, c, b); break;
-    case 6: sub_pairs<REAL, T, 6>(vr, vi, M, c, b); break;
-    case 7: sub_pairs<REAL, T, 7>(vr, vi, M, c, b); break;
-    case 8: sub_pairs<REAL, T, 8>(vr, vi, M, c, b); break;
-    case 9: sub_pairs<REAL, T, 9>(vr, vi, M, c, b); break;
-    case 10: sub_pairs<REAL, T, 10>(vr, vi, M, c, b); break;
-    case 11: sub_pairs<REAL, T, 11>(vr, vi, M, c, b); break;
-    case 12: sub_pairs<REAL, T, 12>(vr, vi, M, c, b); break;
-    case 13: sub_pairs<REAL, T, 13>(vr, vi, M, c, b); break;
-    case 14: sub_pairs<REAL, T, 14>(vr, vi, M, c, b); break;
-    default: sub_pairs<REAL, T, 15>(vr, vi, M, c, b); break;
+    case 1: sub_pairs<REAL, SFORM, T, 1>(vr, vi, Ms, t); break;
+    case 2: sub_pairs<REAL, SFORM, T, 2>(vr, vi, Ms, t); break;
+    case 3: sub_pairs<REAL, SFORM, T, 3>(vr, vi, Ms, t); break;
+    case 4: sub_pairs<REAL, SFORM, T, 4>(vr, vi, Ms, t); break;
+    case 5: sub_pairs<REAL, SFORM, T, 5>(vr, vi, Ms, t); break;
+    case 6: sub_pairs<REAL, SFORM, T, 6>(vr, vi, Ms, t); break;
+    case 7: sub_pairs<REAL, SFORM, T, 7>(vr, vi, Ms, t); break;
+    case 8: sub_pairs<REAL, SFORM, T, 8>(vr, vi, Ms, t); break;
+    case 9: sub_pairs<REAL, SFORM, T, 9>(vr, vi, Ms, t); break;
+    case 10: sub_pairs<REAL, SFORM, T, 10>(vr, vi, Ms, t); break;
+    case 11: sub_pairs<REAL, SFORM, T, 11>(vr, vi, Ms, t); break;
+    case 12: sub_pairs<REAL, SFORM, T, 12>(vr, vi, Ms, t); break;
+    case 13: sub_pairs<REAL, SFORM, T, 13>(vr, vi, Ms, t); break;
+    case 14: sub_pairs<REAL, SFORM, T, 14>(vr, vi, Ms, t); break;
+    default: sub_pairs<REAL, SFORM, T, 15>(vr, vi, Ms, t); break;
     }
 }
 
-// applies the rotations [rb, rb + nr) of a sub-group to the thread's 16 registers
+// applies the rotations [rb, rb + nr) of a sub-group to the thread's 16 registers; the next
+// record is fetched while the current one is applied
 template <typename T>
 __device__ __forceinline__ void sub_apply(T (&vr)[kSubAmps], T (&vi)[kSubAmps], const DevTRot* __restrict__ trots,
                                           int rb, int nr, uint32_t r, uint64_t i0) {
+    if (nr <= 0) return;
+    const DevTRot* tr = trots + rb;
+    uint4 h = __ldg(reinterpret_cast<const uint4*>(tr));
+    uint64_t zt = __ldg(&tr->zt);
+    double t = __ldg(&tr->t);
     for (int q = 0; q < nr; ++q) {
-        const DevTRot* tr = trots + rb + q;
-        const uint32_t dx = __ldg(&tr->dx);
-        const int s0 = par32(__ldg(&tr->zr) & r) ^ par64(__ldg(&tr->zt) & i0);
-        // fold the thread's sign into M: bit d of Ms = sigma of element d
-        const uint32_t Ms = __ldg(&tr->M) ^ (s0 ? 0xffffu : 0u);
-        const T c = (T)__ldg(&tr->c), b = (T)__ldg(&tr->b);
-        if (__ldg(&tr->real))
-            sub_rotation<1, T>(vr, vi, dx, Ms, c, b);
-        else
-            sub_rotation<0, T>(vr, vi, dx, Ms, c, b);
+        const uint32_t dx = h.x, M = h.y, zr = h.z, mode = h.w;
+        const uint64_t zt_c = zt;
+        const T tq = (T)t;
+        if (q + 1 < nr) {
+            const DevTRot* tn = trots + rb + q + 1;
+            h = __ldg(reinterpret_cast<const uint4*>(tn));
+            zt = __ldg(&tn->zt);
+            t = __ldg(&tn->t);
+        }
+        const int s0 = par32(zr & r) ^ par64(zt_c & i0);
+        uint32_t Ms = M ^ (s0 ? 0xffffu : 0u);
+        if (mode & 4u) Ms ^= 0xffffu;
+        switch (mode & 3u) {
+        case 0: sub_rotation<0, 0, T>(vr, vi, dx, Ms, tq); break;
+        case 1: sub_rotation<1, 0, T>(vr, vi, dx, Ms, tq); break;
+        case 2: sub_rotation<0, 1, T>(vr, vi, dx, Ms, tq); break;
+        default: sub_rotation<1, 1, T>(vr, vi, dx, Ms, tq); break;
+        }
+    }
+}
+
+template <typename T>
+__device__ __forceinline__ void sub_scale(T (&vr)[kSubAmps], T (&vi)[kSubAmps], T F) {
+#pragma unroll
+    for (int d = 0; d < kSubAmps; ++d) {
+        vr[d] = pmul(vr[d], F);
+        vi[d] = pmul(vi[d], F);
     }
 }
 
@@ -340,21 +416,20 @@ struct SubHdr {
     uint32_t u[kSubDim];
     uint32_t r;  // this thread's coset representative
     int rb, nr;
+    double F;
 };
 
-__device__ __forceinline__ SubHdr load_sub(const DevSub* __restrict__ sp, uint32_t tid) {
+__device__ __forceinline__ SubHdr load_sub(const DevSub* __restrict__ sp, uint32_t tid, int ncols) {
     SubHdr h;
 #pragma unroll
     for (int b = 0; b < kSubDim; ++b) h.u[b] = __ldg(&sp->u[b]);
-    const uint32_t piv = __ldg(&sp->piv);
     h.rb = __ldg(&sp->rot_begin);
     h.nr = __ldg(&sp->nrot);
-    uint32_t r = tid;  // thread index with zero bits inserted at the ascending pivots
+    h.F = __ldg(&sp->F);
+    uint32_t r = 0;
 #pragma unroll
-    for (int b = 0; b < kSubDim; ++b) {
-        const uint32_t p = (piv >> (8 * b)) & 0xffu;
-        r = ((r >> p) << (p + 1)) | (r & ((1u << p) - 1u));
-    }
+    for (int b = 0; b < kMaxCols; ++b)
+        if (b < ncols && ((tid >> b) & 1u)) r ^= (uint32_t)__ldg(&sp->col[b]);
     h.r = r;
     return h;
 }
@@ -422,7 +497,7 @@ __global__ void __launch_bounds__(kCosetThreads, 2)
         const uint64_t i0 = pdep64(tau, free_mask);
         T vr[kSubAmps], vi[kSubAmps];
         for (int s = 0; s < nsub; ++s) {
-            const SubHdr h = load_sub(subs + s, tid);
+            const SubHdr h = load_sub(subs + s, tid, kbits - kSubDim);
             if (s == 0) {
                 uint64_t gi[kSubAmps];
 #pragma unroll
@@ -447,6 +522,7 @@ __global__ void __launch_bounds__(kCosetThreads, 2)
                 }
             }
             sub_apply<T>(vr, vi, trots, h.rb, h.nr, h.r, i0);
+            sub_scale<T>(vr, vi, (T)h.F);
             if (s == nsub - 1) {
 #pragma unroll
                 for (int d = 0; d < kSubAmps; ++d) {
@@ -544,7 +620,7 @@ __global__ void __launch_bounds__(kCosetThreads, 1)
         V2* tile = reinterpret_cast<V2*>(bufs + (size_t)b * tile_bytes);
         const uint64_t i0 = pdep64((uint64_t)blockIdx.x + m * gridDim.x, free_mask);
         for (int s = 0; s < nsub; ++s) {
-            const SubHdr h = load_sub(subs + s, tid);
+            const SubHdr h = load_sub(subs + s, tid, kbits - kSubDim);
             T vr[kSubAmps], vi[kSubAmps];
 #pragma unroll
             for (int d = 0; d < kSubAmps; ++d) {
@@ -553,6 +629,7 @@ __global__ void __launch_bounds__(kCosetThreads, 1)
                 vi[d] = v.y;
             }
             sub_apply<T>(vr, vi, trots, h.rb, h.nr, h.r, i0);
+            sub_scale<T>(vr, vi, (T)h.F);
             if (s == nsub - 1) {
 #pragma unroll
                 for (int d = 0; d < kSubAmps; ++d) {
@@ -670,7 +747,7 @@ __global__ void __launch_bounds__(kTileMaxThreads, 1)
         const uint64_t i0 = pdep64((uint64_t)blockIdx.x + m * gridDim.x, free_mask);
         V2* buf = reinterpret_cast<V2*>(stage_ptr(st));
         for (int s = 0; s < nsub; ++s) {
-            const SubHdr h = load_sub(subs + s, tid);
+            const SubHdr h = load_sub(subs + s, tid, kbits - kSubDim);
             T vr[kSubAmps], vi[kSubAmps];
 #pragma unroll
             for (int d = 0; d < kSubAmps; ++d) {
@@ -679,6 +756,7 @@ __global__ void __launch_bounds__(kTileMaxThreads, 1)
                 vi[d] = v.y;
             }
             sub_apply<T>(vr, vi, trots, h.rb, h.nr, h.r, i0);
+            sub_scale<T>(vr, vi, (T)h.F);
 #pragma unroll
             for (int d = 0; d < kSubAmps; ++d) {
                 V2 v;

@@ -122,23 +122,63 @@ struct LocalRot {
     double phi;
 };
 
+// Representative columns of a sub-group (see DevSub): k - kSubDim vectors spanning a complement
+// of span{u}; the first `phase_bits` have linearly independent projections on the low
+// phase_bits tile-local bits, so the lanes of one shared-memory phase hit distinct banks, and
+// the rest are the lowest possible unit vectors (contiguous global segments for the first/last
+// sub-group).
+static void choose_columns(const Basis& U, int k, int phase_bits, uint16_t* col) {
+    Basis S = U;
+    int nc = 0;
+    const int ncols = k - kSubDim;
+    for (int p = 0; p < phase_bits && p < k && nc < ncols; ++p) {
+        uint64_t cand = 1ull << p;
+        if (S.reduce(cand) == 0) {
+            cand = 0;
+            for (int q = k - 1; q >= phase_bits; --q) {
+                const uint64_t c2 = (1ull << p) | (1ull << q);
+                if (S.reduce(c2)) {
+                    cand = c2;
+                    break;
+                }
+            }
+        }
+        if (!cand) continue;
+        S.add(S.reduce(cand));
+        col[nc++] = (uint16_t)cand;
+    }
+    for (int q = 0; q < k && nc < ncols; ++q) {
+        const uint64_t cand = 1ull << q;
+        const uint64_t r = S.reduce(cand);
+        if (!r) continue;
+        S.add(r);
+        col[nc++] = (uint16_t)cand;
+    }
+    for (; nc < kMaxCols; ++nc) col[nc] = 0;
+}
+
 // Splits a tile pass's rotations into sub-groups of <= kSubDim-dimensional xor span (order
-// preserving) and emits DevSub / DevTRot records (see ps_internal.h).
-static void make_subgroups(const std::vector<LocalRot>& lr, int k, Plan* plan, Pass* p) {
+// preserving) and emits DevSub / DevTRot records (see ps_internal.h).  A sub-group is also closed
+// when its deferred scale would drop below 2^-20 (long runs of diagonal rotations).
+static void make_subgroups(const std::vector<LocalRot>& lr, int k, int phase_bits, Plan* plan, Pass* p) {
     p->sub_begin = (int)plan->subs.size();
     size_t b = 0;
     while (b < lr.size()) {
         Basis S;
         size_t e = b;
+        double logF = 0.0;
         for (; e < lr.size(); ++e) {
+            const double cc = std::fabs(std::cos(lr[e].phi)), ss = std::fabs(std::sin(lr[e].phi));
+            const double lf = std::log2(std::max(cc, ss));
+            if (e > b && logF + lf < -20.0) break;
             const uint64_t r = S.reduce(lr[e].x);
             if (r) {
                 if (S.dim() == kSubDim) break;
                 S.add(r);
             }
+            logF += lf;
         }
-        // pad to kSubDim dimensions with the highest free unit vectors (keeps low bits free so
-        // consecutive threads own consecutive tile-local indices: conflict-free 16-B smem access)
+        // pad to kSubDim dimensions with the highest free unit vectors
         for (int q = k - 1; q >= 0 && S.dim() < kSubDim; --q) {
             if ((S.pivots >> q) & 1) continue;
             const uint64_t r = S.reduce(1ull << q);
@@ -147,39 +187,43 @@ static void make_subgroups(const std::vector<LocalRot>& lr, int k, Plan* plan, P
         std::vector<uint64_t> u = S.v;
         std::sort(u.begin(), u.end(), [](uint64_t a, uint64_t c) { return highest_bit(a) < highest_bit(c); });
         DevSub sub{};
-        sub.piv = 0;
-        for (int t = 0; t < kSubDim; ++t) {
-            sub.u[t] = (uint32_t)u[t];
-            sub.piv |= (uint32_t)highest_bit(u[t]) << (8 * t);
-        }
+        for (int t = 0; t < kSubDim; ++t) sub.u[t] = (uint32_t)u[t];
+        choose_columns(S, k, phase_bits, sub.col);
         sub.rot_begin = (int)plan->trots.size();
         sub.nrot = (int)(e - b);
+        double F = 1.0;
         for (size_t t = b; t < e; ++t) {
             const LocalRot& L = lr[t];
             uint32_t dx = 0, dz = 0;
-            uint64_t chk = 0;
             for (int q = 0; q < kSubDim; ++q) {
-                if ((L.x >> highest_bit(u[q])) & 1) {
-                    dx |= 1u << q;
-                    chk ^= u[q];
-                }
+                if ((L.x >> highest_bit(u[q])) & 1) dx |= 1u << q;
                 if (parity64(L.z & u[q])) dz |= 1u << q;
             }
-            (void)chk;  // == L.x: the sub-group span contains every member's xor mask
             uint32_t M = 0;
             for (int d = 0; d < kSubAmps; ++d)
                 if (parity64((uint64_t)(dz & (uint32_t)d))) M |= 1u << d;
-            const DevRot r = make_rec(L.x, L.z, L.zt, L.y, L.sign, L.phi);
+            const double c = std::cos(L.phi);
+            const double s0 = std::sin(L.phi) * (double)L.sign;
+            const int e4 = (L.y + 1) & 3;                 // B = s0 * i^e4
+            const int real = (e4 & 1) ? 0 : 1;            // i^0, i^2 real; i^1, i^3 imaginary
+            const double ph = (e4 == 0 || e4 == 1) ? 1.0 : -1.0;  // B = s0 * ph * (1 or i)
             DevTRot tr{};
             tr.dx = dx;
             tr.M = M;
             tr.zr = (uint32_t)L.z;
             tr.zt = L.zt;
-            tr.c = r.c;
-            tr.b = r.b;
-            tr.real = r.real;
+            if (std::fabs(c) >= std::fabs(s0)) {
+                tr.mode = (uint32_t)real;
+                tr.t = ph * (s0 / c);
+                F *= c;
+            } else {
+                tr.mode = (uint32_t)real | 2u | (ph < 0 ? 4u : 0u);
+                tr.t = c / s0;
+                F *= s0;
+            }
             plan->trots.push_back(tr);
         }
+        sub.F = F;
         plan->subs.push_back(sub);
         b = e;
     }
@@ -211,7 +255,7 @@ static void emit_tile(const std::vector<PhysRot>& seg, size_t b, size_t e, const
         std::vector<LocalRot> lr;
         for (size_t t = b; t < e; ++t)
             lr.push_back({seg[t].x, seg[t].z & kmask, seg[t].z & p.free_mask, seg[t].y, seg[t].sign, seg[t].phi});
-        make_subgroups(lr, k, plan, &p);
+        make_subgroups(lr, k, cfg.phase_bits, plan, &p);
         plan->passes.push_back(p);
         return;
     }
@@ -267,7 +311,7 @@ static void emit_tile(const std::vector<PhysRot>& seg, size_t b, size_t e, const
         const uint64_t zl = (zc << c) | (z & cmask);
         lr.push_back({xl, zl, z & p.free_mask, seg[t].y, seg[t].sign, seg[t].phi});
     }
-    make_subgroups(lr, p.kbits, plan, &p);
+    make_subgroups(lr, p.kbits, cfg.phase_bits, plan, &p);
     plan->passes.push_back(p);
 }
 

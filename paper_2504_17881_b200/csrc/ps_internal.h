@@ -37,33 +37,45 @@ static_assert(sizeof(DevRot) == 48, "DevRot layout");
 // Tile passes (K2/K7) apply their rotations in SUB-GROUPS: consecutive rotations whose
 // tile-local xor masks span <= kSubDim dimensions.  For a sub-group with basis u_0..u_3
 // (tile-local, pivots p_0 < .. < p_3 = highest set bits, reduced row-echelon form) every thread
-// owns one coset r xor span{u}: r = its thread index with zero bits inserted at the pivots, and
-// holds the 16 amplitudes l_d = r xor U(d), U(d) = xor of u_b over the set bits b of d, in
-// registers while the sub-group's rotations are applied.
+// owns one coset r xor span{u}: r = xor of col[b] over the set bits b of its thread index (the
+// columns span a complement of span{u}, chosen so the lanes of one shared-memory phase hit
+// distinct banks), and holds the 16 amplitudes l_d = r xor U(d), U(d) = xor of u_b over the set
+// bits b of d, in registers while the sub-group's rotations are applied.
+//
+// Deferred scaling: each rotation is applied as f * (self_coef * a_self + cross_coef * a_other)
+// with the uniform factor f = cos(phi) when |cos| >= |sin| (self_coef = 1, cross_coef = +-t,
+// t = sin/cos) and f = sign*sin(phi) otherwise (self_coef = t = cos/(sign*sin), cross_coef = +-1
+// or +-i), i.e. one fused multiply-add per component; the product F of the sub-group's factors
+// is applied once before the amplitudes leave the registers.
 constexpr int kSubDim = 4;
 constexpr int kSubAmps = 1 << kSubDim;
+constexpr int kMaxCols = 12;
 
 struct DevSub {
-    uint32_t u[kSubDim];  // basis in tile-local coordinates
-    uint32_t piv;         // pivot positions p_b in byte b, ascending
-    int32_t rot_begin;    // first DevTRot of this sub-group (index into the call's table)
+    uint32_t u[kSubDim];     // basis in tile-local coordinates
+    uint16_t col[kMaxCols];  // representative columns (tile-local), one per thread-index bit
+    int32_t rot_begin;       // first DevTRot of this sub-group (index into the call's table)
     int32_t nrot;
-    uint32_t pad;
+    double F;                // product of the deferred factors
 };
-static_assert(sizeof(DevSub) == 32, "DevSub layout");
+static_assert(sizeof(DevSub) == 56, "DevSub layout");
 
 // one rotation of a sub-group: pair (d, d xor dx) of the thread's 16 registers ("i" member: bit
 // highest(dx) of d is 0), sigma = parity(zr & r) xor parity(zt & i0) xor bit d of M, with
-// M bit d = parity(Dz & d), Dz_b = parity(Z_loc & u_b); c, b, real as in DevRot.
+// M bit d = parity(Dz & d), Dz_b = parity(Z_loc & u_b).
+//   mode bit 0 (REAL): B real (y odd) or imaginary (y even), as in DevRot
+//   mode bit 1 (SFORM): factor f = sign*sin(phi) (self coefficient t = cos/f) instead of cos(phi)
+//                       (cross coefficient t = B/f up to the factor i)
+//   mode bit 2 (NEG):   SFORM only: B/f = -1 (REAL) or -i (imaginary) instead of +1 / +i
 struct DevTRot {
     uint32_t dx;   // 0: diagonal
     uint32_t M;
     uint32_t zr;   // tile-local phase mask (parity with the coset representative r)
-    uint32_t real; // as DevRot
+    uint32_t mode;
     uint64_t zt;   // phase mask on the tile-enumeration bits (parity with the tile base i0)
-    double c, b;
+    double t;      // REAL: B/f = +-t (CFORM) ; imaginary: B/f = +-i t ; SFORM: t = cos/f, B/f = +-1/+-i
 };
-static_assert(sizeof(DevTRot) == 40, "DevTRot layout");
+static_assert(sizeof(DevTRot) == 32, "DevTRot layout");
 
 // expectation term record: contribution sigma(i) * (kr * tr + ki * ti) per pair (x != 0) with
 // t = conj(a_j) a_i, or sigma(i) * kr * |a_i|^2 per element (x = 0)
@@ -123,6 +135,7 @@ struct PlanConfig {
     int fusion = 2;
     int tile_bits = 12;
     int min_chunk_bits = 4;     // coset tiles gather chunks of >= 2^min_chunk_bits amplitudes
+    int phase_bits = 3;         // log2 lanes per shared-memory phase (16-B amplitudes: 3, 8-B: 4)
     int max_pass_rots = 1 << 30;
     bool want_debug = false;
 };
