@@ -87,10 +87,12 @@ enum {
     PS_OPT_CHUNK_BYTES = 3,   /* exchange chunk size in bytes (default 256 MiB) */
     PS_OPT_MAX_PASS_ROTS = 4, /* cap on rotations fused into one tile pass (default 64) */
     PS_OPT_VEC256 = 5,        /* 1: 256-bit LDG/STG in K1 (default 1); 0: 128-bit */
-    PS_OPT_TILE_TMA = 6       /* tile-pass kernel: 2 = register-direct (default): first sub-group
+    PS_OPT_TILE_TMA = 6,      /* tile-pass kernel: 2 = register-direct (default): first sub-group
                                  loads from HBM, last stores to HBM, smem between sub-groups;
-                                 0 = TMA-prefetched double buffer; 1 = 3-stage TMA ring
-                                 (0 and 1 kept for A/B) */
+                                 0 = cp.async-prefetched double buffer; 1 = 3-stage TMA ring;
+                                 3 = TMA-bulk-prefetched double buffer (A/B) */
+    PS_OPT_CHUNK_BITS = 7     /* min log2 contiguous amplitudes per gathered chunk (0 = default:
+                                 4 for C128, 5 for C64, i.e. 256 B) */
 };
 
 /* ------------------------------------------------------------------------------------------ */

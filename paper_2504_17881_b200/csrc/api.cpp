@@ -79,7 +79,7 @@ struct ps_state {
     size_t xstage_bytes = 0;
     size_t chunk_bytes = 256ull << 20;
     // options
-    int profile = 0, fusion = 2, tile_bits = 11, vec256 = 1, max_pass_rots = 1 << 30, tile_tma = 2;
+    int profile = 0, fusion = 2, tile_bits = 11, vec256 = 1, max_pass_rots = 1 << 30, tile_tma = 2, chunk_bits = 0;
     ps_stats stats{};
     std::vector<PendingTiming> pending;
     std::vector<cudaEvent_t> event_pool;
@@ -332,8 +332,12 @@ extern "C" int ps_set_option(ps_handle h, int option, int64_t value) {
         h->max_pass_rots = (int)std::min<int64_t>(value, 1 << 30);
         break;
     case PS_OPT_VEC256: h->vec256 = value ? 1 : 0; break;
+    case PS_OPT_CHUNK_BITS:
+        if (value < 0 || value > 12) return fail(PS_EINVAL, "chunk bits must be 0..12 (0 = default)");
+        h->chunk_bits = (int)value;
+        break;
     case PS_OPT_TILE_TMA:
-        if (value < 0 || value > 2) return fail(PS_EINVAL, "tile mode must be 0, 1 or 2");
+        if (value < 0 || value > 3) return fail(PS_EINVAL, "tile mode must be 0..3");
         h->tile_tma = (int)value;
         break;
     default: return fail(PS_EINVAL, "unknown option");
@@ -584,7 +588,7 @@ static PlanConfig plan_config(const ps_state* h) {
     cfg.rank = h->rank;
     cfg.fusion = h->fusion;
     cfg.tile_bits = h->tile_bits;
-    cfg.min_chunk_bits = h->dtype == PS_C128 ? 4 : 5;  // >= 256-byte gathered chunks
+    cfg.min_chunk_bits = h->chunk_bits ? h->chunk_bits : (h->dtype == PS_C128 ? 4 : 5);  // >= 256-B chunks
     cfg.phase_bits = h->dtype == PS_C128 ? 3 : 4;      // 16-B vs 8-B shared-memory accesses
     cfg.max_pass_rots = h->max_pass_rots;
     return cfg;

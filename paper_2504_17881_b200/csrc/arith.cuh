@@ -49,9 +49,12 @@ __device__ __forceinline__ void rot_diag(T& r, T& i, T c, T b) {
     }
 }
 
-template <typename T>
-__device__ __forceinline__ T flip(T v, int neg) {
-    return neg ? -v : v;
+// exact sign flip when neg == 1: one LOP3 on the high word (no select, no DADD)
+__device__ __forceinline__ double flip(double v, int neg) {
+    return __hiloint2double(__double2hiint(v) ^ (int)((unsigned)neg << 31), __double2loint(v));
+}
+__device__ __forceinline__ float flip(float v, int neg) {
+    return __int_as_float(__float_as_int(v) ^ (int)((unsigned)neg << 31));
 }
 
 __device__ __forceinline__ int par64(uint64_t v) { return __popcll(v) & 1; }

@@ -299,13 +299,15 @@ __device__ __forceinline__ void dpair(T& ir, T& ii, T& jr, T& ji, T t, int neg) 
             ir = nir; ii = nii; jr = njr; ji = nji;
         }
     } else {
+        // g = -1 when neg: cross operands carry the sign, the fixed signs ride on the FMA
+        const T gjr = flip(jr, neg), gji = flip(ji, neg), gir = flip(ir, neg), gii = flip(ii, neg);
         if (REAL) {
-            const T nir = pfma(t, ir, flip(jr, !neg)), nii = pfma(t, ii, flip(ji, !neg));
-            const T njr = pfma(t, jr, flip(ir, neg)), nji = pfma(t, ji, flip(ii, neg));
+            const T nir = pfma(t, ir, -gjr), nii = pfma(t, ii, -gji);
+            const T njr = pfma(t, jr, gir), nji = pfma(t, ji, gii);
             ir = nir; ii = nii; jr = njr; ji = nji;
         } else {
-            const T nir = pfma(t, ir, flip(ji, !neg)), nii = pfma(t, ii, flip(jr, neg));
-            const T njr = pfma(t, jr, flip(ii, !neg)), nji = pfma(t, ji, flip(ir, neg));
+            const T nir = pfma(t, ir, -gji), nii = pfma(t, ii, gjr);
+            const T njr = pfma(t, jr, -gii), nji = pfma(t, ji, gir);
             ir = nir; ii = nii; jr = njr; ji = nji;
         }
     }
@@ -324,11 +326,12 @@ __device__ __forceinline__ void ddiag(T& r, T& i, T t, int neg) {
             r = nr; i = ni;
         }
     } else {
+        const T gr = flip(r, neg), gi = flip(i, neg);
         if (REAL) {
-            const T nr = pfma(t, r, flip(r, !neg)), ni = pfma(t, i, flip(i, !neg));
+            const T nr = pfma(t, r, -gr), ni = pfma(t, i, -gi);
             r = nr; i = ni;
         } else {
-            const T nr = pfma(t, r, flip(i, !neg)), ni = pfma(t, i, flip(r, neg));
+            const T nr = pfma(t, r, -gi), ni = pfma(t, i, gr);
             r = nr; i = ni;
         }
     }
@@ -453,6 +456,41 @@ struct SmemAmp<float> {
     using V = float2;
 };
 
+// free_mask as maximal runs of consecutive set bits: i0 = pdep(tau, free_mask) in a few ops per run
+struct BitRuns {
+    uint32_t n;
+    uint8_t pos[32];
+    uint8_t len[32];
+};
+
+BitRuns make_runs(uint64_t mask) {
+    BitRuns r{};
+    int q = 0;
+    while (mask >> q) {
+        if (!((mask >> q) & 1)) {
+            ++q;
+            continue;
+        }
+        int l = 0;
+        while (q + l < 64 && ((mask >> (q + l)) & 1)) ++l;
+        r.pos[r.n] = (uint8_t)q;
+        r.len[r.n] = (uint8_t)l;
+        ++r.n;
+        q += l;
+    }
+    return r;
+}
+
+__device__ __forceinline__ uint64_t deposit(uint64_t tau, const BitRuns& runs) {
+    uint64_t out = 0;
+    for (uint32_t k = 0; k < runs.n; ++k) {
+        const uint32_t l = runs.len[k];
+        out |= (tau & ((1ull << l) - 1)) << runs.pos[k];
+        tau >>= l;
+    }
+    return out;
+}
+
 __device__ __forceinline__ uint64_t pdep64(uint64_t v, uint64_t mask) {
     uint64_t out = 0;
     for (uint64_t m = mask; m; m &= m - 1) {
@@ -481,7 +519,7 @@ __host__ __device__ inline size_t coset_off_bytes(int hbits) {
 
 template <typename T>
 __global__ void __launch_bounds__(kCosetThreads, 2)
-    k_coset(T* __restrict__ a, int kbits, int cbits, uint64_t free_mask, const uint64_t* __restrict__ offs,
+    k_coset(T* __restrict__ a, int kbits, int cbits, const __grid_constant__ BitRuns runs, const uint64_t* __restrict__ offs,
             uint64_t ntiles, const DevSub* __restrict__ subs, int nsub, const DevTRot* __restrict__ trots) {
     using V2 = typename SmemAmp<T>::V;
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -494,7 +532,7 @@ __global__ void __launch_bounds__(kCosetThreads, 2)
     __syncthreads();
     V2* g = reinterpret_cast<V2*>(a);
     for (uint64_t tau = blockIdx.x; tau < ntiles; tau += gridDim.x) {
-        const uint64_t i0 = pdep64(tau, free_mask);
+        const uint64_t i0 = deposit(tau, runs);
         T vr[kSubAmps], vi[kSubAmps];
         for (int s = 0; s < nsub; ++s) {
             const SubHdr h = load_sub(subs + s, tid, kbits - kSubDim);
@@ -570,8 +608,8 @@ __device__ __forceinline__ void mbar_wait_parity(uint64_t* bar, uint32_t parity)
     }
 }
 
-template <typename T>
-__global__ void __launch_bounds__(kCosetThreads, 1)
+template <typename T, int CPASYNC>
+__global__ void __launch_bounds__(kCosetThreads, 2)
     k_coset_pf(T* __restrict__ a, int kbits, int cbits, uint64_t free_mask, const uint64_t* __restrict__ offs,
                uint64_t ntiles, const DevSub* __restrict__ subs, int nsub, const DevTRot* __restrict__ trots) {
     using V2 = typename SmemAmp<T>::V;
@@ -597,6 +635,20 @@ __global__ void __launch_bounds__(kCosetThreads, 1)
         const uint64_t i0 = pdep64((uint64_t)blockIdx.x + m * gridDim.x, free_mask);
         const int b = (int)(m & 1);
         unsigned char* dst = bufs + (size_t)b * tile_bytes;
+        if (CPASYNC) {
+            // 16-byte cp.async (LDGSTS) units: one fp64 amplitude or two fp32 amplitudes
+            constexpr uint32_t per = 16 / (2 * sizeof(T));
+            const uint32_t units = (1u << kbits) / per;
+            for (uint32_t q = tid; q < units; q += blockDim.x) {
+                const uint32_t l = q * per;
+                const T* src = a + 2 * ((i0 ^ soff[l >> cbits]) | (l & cmask));
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr(dst + (size_t)q * 16)),
+                             "l"(src)
+                             : "memory");
+            }
+            asm volatile("cp.async.commit_group;" ::: "memory");
+            return;
+        }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         if (tid == 0)
             asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(&mbar[b])),
@@ -614,9 +666,18 @@ __global__ void __launch_bounds__(kCosetThreads, 1)
     V2* g = reinterpret_cast<V2*>(a);
     if (my_tiles > 0) prefetch(0);
     for (uint64_t m = 0; m < my_tiles; ++m) {
-        if (m + 1 < my_tiles) prefetch(m + 1);  // buffer (m+1)&1 was released by the barrier ending tile m-1
+        const bool more = m + 1 < my_tiles;
+        if (more) prefetch(m + 1);  // buffer (m+1)&1 was released by the barrier ending tile m-1
         const int b = (int)(m & 1);
-        mbar_wait_parity(&mbar[b], (uint32_t)((m >> 1) & 1));
+        if (CPASYNC) {
+            if (more)
+                asm volatile("cp.async.wait_group 1;" ::: "memory");
+            else
+                asm volatile("cp.async.wait_group 0;" ::: "memory");
+            __syncthreads();
+        } else {
+            mbar_wait_parity(&mbar[b], (uint32_t)((m >> 1) & 1));
+        }
         V2* tile = reinterpret_cast<V2*>(bufs + (size_t)b * tile_bytes);
         const uint64_t i0 = pdep64((uint64_t)blockIdx.x + m * gridDim.x, free_mask);
         for (int s = 0; s < nsub; ++s) {
@@ -985,29 +1046,29 @@ cudaError_t launch_coset_t(T* a, int nl, const Pass& p, const DevSub* d_subs, co
     const uint64_t ntiles = 1ull << (nl - p.kbits);
     const uint64_t cap = (uint64_t)num_sms() * (uint64_t)occ * 4;
     const unsigned grid = (unsigned)(ntiles < cap ? ntiles : cap);
-    k_coset<T><<<grid, threads, smem, s>>>(a, p.kbits, p.cbits, p.free_mask, d_offs + p.off_begin, ntiles,
+    k_coset<T><<<grid, threads, smem, s>>>(a, p.kbits, p.cbits, make_runs(p.free_mask), d_offs + p.off_begin, ntiles,
                                            d_subs + p.sub_begin, p.sub_count, d_trots);
     return cudaGetLastError();
 }
 
-template <typename T>
+template <typename T, int CPASYNC>
 cudaError_t launch_coset_pf_t(T* a, int nl, const Pass& p, const DevSub* d_subs, const DevTRot* d_trots,
                               const uint64_t* d_offs, cudaStream_t s) {
     const size_t smem = coset_off_bytes(p.kbits - p.cbits) + 2 * ((size_t)(2 * sizeof(T)) << p.kbits);
     static bool attr_done[2] = {false, false};
     const int which = sizeof(T) == 8 ? 0 : 1;
     if (!attr_done[which]) {
-        cudaFuncSetAttribute(k_coset_pf<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        cudaFuncSetAttribute(k_coset_pf<T, CPASYNC>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         attr_done[which] = true;
     }
     const int threads = 1 << (p.kbits - kSubDim);
     int occ = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_coset_pf<T>, threads, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_coset_pf<T, CPASYNC>, threads, smem);
     if (occ < 1) occ = 1;
     const uint64_t ntiles = 1ull << (nl - p.kbits);
     const uint64_t cap = (uint64_t)num_sms() * (uint64_t)occ;
     const unsigned grid = (unsigned)(ntiles < cap ? ntiles : cap);
-    k_coset_pf<T><<<grid, threads, smem, s>>>(a, p.kbits, p.cbits, p.free_mask, d_offs + p.off_begin, ntiles,
+    k_coset_pf<T, CPASYNC><<<grid, threads, smem, s>>>(a, p.kbits, p.cbits, p.free_mask, d_offs + p.off_begin, ntiles,
                                               d_subs + p.sub_begin, p.sub_count, d_trots);
     return cudaGetLastError();
 }
@@ -1069,8 +1130,12 @@ cudaError_t launch_tile(int dtype, void* a, int nl, const Pass& p, const DevSub*
         if (dtype == PS_C128) return launch_coset_t<double>((double*)a, nl, p, d_subs, d_trots, d_offs, s);
         return launch_coset_t<float>((float*)a, nl, p, d_subs, d_trots, d_offs, s);
     }
-    if (dtype == PS_C128) return launch_coset_pf_t<double>((double*)a, nl, p, d_subs, d_trots, d_offs, s);
-    return launch_coset_pf_t<float>((float*)a, nl, p, d_subs, d_trots, d_offs, s);
+    if (use_tma == 3) {
+        if (dtype == PS_C128) return launch_coset_pf_t<double, 0>((double*)a, nl, p, d_subs, d_trots, d_offs, s);
+        return launch_coset_pf_t<float, 0>((float*)a, nl, p, d_subs, d_trots, d_offs, s);
+    }
+    if (dtype == PS_C128) return launch_coset_pf_t<double, 1>((double*)a, nl, p, d_subs, d_trots, d_offs, s);
+    return launch_coset_pf_t<float, 1>((float*)a, nl, p, d_subs, d_trots, d_offs, s);
 }
 
 cudaError_t launch_full_update(int dtype, void* a, const void* stage, uint64_t base, uint64_t count, uint64_t pbase,

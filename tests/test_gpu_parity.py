@@ -78,7 +78,7 @@ def test_fusion_levels_agree(dtype, kind):
     n = 16
     codes, ang = workloads.random_layer(n, 400, seed=3, kind=kind)
     outs = {}
-    for fusion, tb, mode in ((0, None, 2), (1, None, 2), (2, None, 2), (2, 7, 2), (2, None, 0), (2, 9, 1)):
+    for fusion, tb, mode in ((0, None, 2), (1, None, 2), (2, None, 2), (2, 7, 2), (2, None, 0), (2, 9, 1), (2, None, 3)):
         x, z = P.pauli_encode_codes(codes)
         with P.State(n, dtype) as st:
             st.set_option(ps.OPT_FUSION, fusion)
