@@ -50,6 +50,7 @@ def parse():
     ap.add_argument("--tile-mode", type=int, default=2,
                     help="0 cp.async prefetch, 1 TMA ring, 2 register-direct, 3 TMA-bulk prefetch")
     ap.add_argument("--chunk-bits", type=int, default=0)
+    ap.add_argument("--tile-tune", type=int, default=-1)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     return ap.parse_args()
@@ -231,6 +232,8 @@ def run_ours(args):
     st.set_option(ps.OPT_TILE_TMA, args.tile_mode)
     if args.chunk_bits:
         st.set_option(ps.OPT_CHUNK_BITS, args.chunk_bits)
+    if args.tile_tune >= 0:
+        st.set_option(ps.OPT_TILE_TUNE, args.tile_tune)
     st.set_option(ps.OPT_PROFILE, 1)
     lay = layers(args, args.warmup + args.steps)
     enc = [P.pauli_encode_codes(c) + (a,) for c, a in lay]

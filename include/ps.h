@@ -91,8 +91,10 @@ enum {
                                  loads from HBM, last stores to HBM, smem between sub-groups;
                                  0 = cp.async-prefetched double buffer; 1 = 3-stage TMA ring;
                                  3 = TMA-bulk-prefetched double buffer (A/B) */
-    PS_OPT_CHUNK_BITS = 7     /* min log2 contiguous amplitudes per gathered chunk (0 = default:
+    PS_OPT_CHUNK_BITS = 7,    /* min log2 contiguous amplitudes per gathered chunk (0 = default:
                                  4 for C128, 5 for C64, i.e. 256 B) */
+    PS_OPT_TILE_TUNE = 8      /* register-direct tile kernel tuning: bit 0 = L2 prefetch of the next
+                                 tile, bits 4.. = persistent-grid multiplier (0 = default) */
 };
 
 /* ------------------------------------------------------------------------------------------ */

@@ -21,7 +21,7 @@ int kernel_max_red_blocks();
 cudaError_t launch_stream(int dtype, void* a, int nl, const Pass& p, const DevRot* d_rots, int vec256,
                           cudaStream_t s);
 cudaError_t launch_tile(int dtype, void* a, int nl, const Pass& p, const DevSub* d_subs, const DevTRot* d_trots,
-                        const uint64_t* d_offs, int use_tma, cudaStream_t s);
+                        const uint64_t* d_offs, int use_tma, int tune, cudaStream_t s);
 cudaError_t launch_full_update(int dtype, void* a, const void* stage, uint64_t base, uint64_t count, uint64_t pbase,
                                const DevRot* rec, cudaStream_t s);
 cudaError_t launch_norm(int dtype, const void* a, uint64_t n, double* d_partial, double* d_out, cudaStream_t s);
@@ -79,7 +79,7 @@ struct ps_state {
     size_t xstage_bytes = 0;
     size_t chunk_bytes = 256ull << 20;
     // options
-    int profile = 0, fusion = 2, tile_bits = 11, vec256 = 1, max_pass_rots = 1 << 30, tile_tma = 2, chunk_bits = 0;
+    int profile = 0, fusion = 2, tile_bits = 11, vec256 = 1, max_pass_rots = 1 << 30, tile_tma = 2, chunk_bits = 0, tile_tune = 0;
     ps_stats stats{};
     std::vector<PendingTiming> pending;
     std::vector<cudaEvent_t> event_pool;
@@ -332,6 +332,7 @@ extern "C" int ps_set_option(ps_handle h, int option, int64_t value) {
         h->max_pass_rots = (int)std::min<int64_t>(value, 1 << 30);
         break;
     case PS_OPT_VEC256: h->vec256 = value ? 1 : 0; break;
+    case PS_OPT_TILE_TUNE: h->tile_tune = (int)value; break;
     case PS_OPT_CHUNK_BITS:
         if (value < 0 || value > 12) return fail(PS_EINVAL, "chunk bits must be 0..12 (0 = default)");
         h->chunk_bits = (int)value;
@@ -616,7 +617,7 @@ extern "C" int ps_apply_rotations(ps_handle h, const uint64_t* xmask, const uint
         case PASS_TILE:
         case PASS_COSET: {
             Timed t(h, p.kind);
-            CUDA_TRY(h, launch_tile(h->dtype, h->d_state, h->nl, p, h->d_subs, h->d_trots, h->d_offs, h->tile_tma, h->stream));
+            CUDA_TRY(h, launch_tile(h->dtype, h->d_state, h->nl, p, h->d_subs, h->d_trots, h->d_offs, h->tile_tma, h->tile_tune, h->stream));
             break;
         }
         case PASS_EXCHANGE: {

@@ -517,10 +517,11 @@ __host__ __device__ inline size_t coset_off_bytes(int hbits) {
     return ((sizeof(uint64_t) << hbits) + 127) & ~(size_t)127;
 }
 
-template <typename T>
-__global__ void __launch_bounds__(kCosetThreads, 2)
+template <typename T, int MAXT, int MINB>
+__global__ void __launch_bounds__(MAXT, MINB)
     k_coset(T* __restrict__ a, int kbits, int cbits, const __grid_constant__ BitRuns runs, const uint64_t* __restrict__ offs,
-            uint64_t ntiles, const DevSub* __restrict__ subs, int nsub, const DevTRot* __restrict__ trots) {
+            uint64_t ntiles, const DevSub* __restrict__ subs, int nsub, const DevTRot* __restrict__ trots,
+            int l2_prefetch) {
     using V2 = typename SmemAmp<T>::V;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int hbits = kbits - cbits;
@@ -531,6 +532,7 @@ __global__ void __launch_bounds__(kCosetThreads, 2)
     for (uint32_t u = tid; u < (1u << hbits); u += blockDim.x) soff[u] = __ldg(&offs[u]);
     __syncthreads();
     V2* g = reinterpret_cast<V2*>(a);
+    const uint32_t chunk_bytes = (uint32_t)(2 * sizeof(T)) << cbits;
     for (uint64_t tau = blockIdx.x; tau < ntiles; tau += gridDim.x) {
         const uint64_t i0 = deposit(tau, runs);
         T vr[kSubAmps], vi[kSubAmps];
@@ -558,6 +560,15 @@ __global__ void __launch_bounds__(kCosetThreads, 2)
                     vr[d] = v.x;
                     vi[d] = v.y;
                 }
+            }
+            if (s == 0 && l2_prefetch && tau + gridDim.x < ntiles) {
+                // this tile's loads have landed (sub_apply consumes them): warm L2 with the CTA's next
+                // tile while the rest of this one is computed and stored
+                const uint64_t i1 = deposit(tau + gridDim.x, runs);
+                for (uint32_t u = tid; u < (1u << hbits); u += blockDim.x)
+                    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a + 2 * (i1 ^ soff[u])),
+                                 "r"(chunk_bytes)
+                                 : "memory");
             }
             sub_apply<T>(vr, vi, trots, h.rb, h.nr, h.r, i0);
             sub_scale<T>(vr, vi, (T)h.F);
@@ -1028,27 +1039,38 @@ cudaError_t launch_stream_t(T* a, int nl, const Pass& p, const DevRot* d_rots, c
     return cudaGetLastError();
 }
 
-template <typename T>
-cudaError_t launch_coset_t(T* a, int nl, const Pass& p, const DevSub* d_subs, const DevTRot* d_trots,
-                           const uint64_t* d_offs, cudaStream_t s) {
+template <typename T, int MAXT, int MINB>
+cudaError_t launch_coset_k(T* a, int nl, const Pass& p, const DevSub* d_subs, const DevTRot* d_trots,
+                           const uint64_t* d_offs, int l2_prefetch, int grid_mult, cudaStream_t s) {
     const size_t smem = coset_off_bytes(p.kbits - p.cbits) + ((size_t)(2 * sizeof(T)) << p.kbits);
-    static bool attr_done[2] = {false, false};
-    const int which = sizeof(T) == 8 ? 0 : 1;
-    if (!attr_done[which]) {
-        cudaFuncSetAttribute(k_coset<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        attr_done[which] = true;
+    static bool attr_done = false;
+    if (!attr_done) {
+        cudaFuncSetAttribute(k_coset<T, MAXT, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        attr_done = true;
     }
     const int threads = 1 << (p.kbits - kSubDim);
-    if (threads > kCosetThreads) return cudaErrorInvalidValue;
+    if (threads > MAXT) return cudaErrorInvalidValue;
     int occ = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_coset<T>, threads, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_coset<T, MAXT, MINB>, threads, smem);
     if (occ < 1) occ = 1;
     const uint64_t ntiles = 1ull << (nl - p.kbits);
-    const uint64_t cap = (uint64_t)num_sms() * (uint64_t)occ * 4;
+    const uint64_t cap = (uint64_t)num_sms() * (uint64_t)occ * (uint64_t)(grid_mult > 0 ? grid_mult : 1);
     const unsigned grid = (unsigned)(ntiles < cap ? ntiles : cap);
-    k_coset<T><<<grid, threads, smem, s>>>(a, p.kbits, p.cbits, make_runs(p.free_mask), d_offs + p.off_begin, ntiles,
-                                           d_subs + p.sub_begin, p.sub_count, d_trots);
+    k_coset<T, MAXT, MINB><<<grid, threads, smem, s>>>(a, p.kbits, p.cbits, make_runs(p.free_mask),
+                                                        d_offs + p.off_begin, ntiles, d_subs + p.sub_begin,
+                                                        p.sub_count, d_trots, l2_prefetch);
     return cudaGetLastError();
+}
+
+// occupancy variants: tune bits 1..3 (>> 1) select the register cap for 128-thread CTAs
+template <typename T>
+cudaError_t launch_coset_t(T* a, int nl, const Pass& p, const DevSub* d_subs, const DevTRot* d_trots,
+                           const uint64_t* d_offs, int l2_prefetch, int grid_mult, int occ_sel, cudaStream_t s) {
+    const int threads = 1 << (p.kbits - kSubDim);
+    if (threads <= 128 && occ_sel == 1) return launch_coset_k<T, 128, 5>(a, nl, p, d_subs, d_trots, d_offs, l2_prefetch, grid_mult, s);
+    if (threads <= 128 && occ_sel == 2) return launch_coset_k<T, 128, 6>(a, nl, p, d_subs, d_trots, d_offs, l2_prefetch, grid_mult, s);
+    if (threads <= 128 && occ_sel == 3) return launch_coset_k<T, 128, 8>(a, nl, p, d_subs, d_trots, d_offs, l2_prefetch, grid_mult, s);
+    return launch_coset_k<T, kCosetThreads, 2>(a, nl, p, d_subs, d_trots, d_offs, l2_prefetch, grid_mult, s);
 }
 
 template <typename T, int CPASYNC>
@@ -1121,14 +1143,18 @@ cudaError_t launch_stream(int dtype, void* a, int nl, const Pass& p, const DevRo
 }
 
 cudaError_t launch_tile(int dtype, void* a, int nl, const Pass& p, const DevSub* d_subs, const DevTRot* d_trots,
-                        const uint64_t* d_offs, int use_tma, cudaStream_t s) {
+                        const uint64_t* d_offs, int use_tma, int tune, cudaStream_t s) {
+    // tune: bit 0 = L2 prefetch of the next tile (register-direct kernel); bits 4.. = grid multiplier
+    const int l2p = tune & 1;
+    const int occ_sel = (tune >> 1) & 7;
+    const int gm = (tune >> 4) ? (tune >> 4) : 4;
     if (use_tma == 1) {
         if (dtype == PS_C128) return launch_tile_t<double>((double*)a, nl, p, d_subs, d_trots, d_offs, s);
         return launch_tile_t<float>((float*)a, nl, p, d_subs, d_trots, d_offs, s);
     }
     if (use_tma == 2) {
-        if (dtype == PS_C128) return launch_coset_t<double>((double*)a, nl, p, d_subs, d_trots, d_offs, s);
-        return launch_coset_t<float>((float*)a, nl, p, d_subs, d_trots, d_offs, s);
+        if (dtype == PS_C128) return launch_coset_t<double>((double*)a, nl, p, d_subs, d_trots, d_offs, l2p, gm, occ_sel, s);
+        return launch_coset_t<float>((float*)a, nl, p, d_subs, d_trots, d_offs, l2p, gm, occ_sel, s);
     }
     if (use_tma == 3) {
         if (dtype == PS_C128) return launch_coset_pf_t<double, 0>((double*)a, nl, p, d_subs, d_trots, d_offs, s);

@@ -17,7 +17,7 @@ LIB_PATH = os.path.join(_HERE, "libps.so")
 C128, C64 = 0, 1
 K_STREAM, K_TILE, K_COSET, K_REDUCE, K_INIT, K_EXCHANGE = range(6)
 KERNEL_NAMES = ["stream", "tile", "coset", "reduce", "init", "exchange"]
-OPT_PROFILE, OPT_FUSION, OPT_TILE_BITS, OPT_CHUNK_BYTES, OPT_MAX_PASS_ROTS, OPT_VEC256, OPT_TILE_TMA, OPT_CHUNK_BITS = range(8)
+OPT_PROFILE, OPT_FUSION, OPT_TILE_BITS, OPT_CHUNK_BYTES, OPT_MAX_PASS_ROTS, OPT_VEC256, OPT_TILE_TMA, OPT_CHUNK_BITS, OPT_TILE_TUNE = range(9)
 
 
 class PsError(RuntimeError):
