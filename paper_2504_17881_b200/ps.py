@@ -198,6 +198,20 @@ def plan_describe(n: int, x, z, angles, world: int = 1, rank: int = 0, fusion: i
     return op_list, rot_list
 
 
+def bootstrap_nccl_id(rank: int, group=None) -> bytes:
+    """Rank 0 creates an ncclUniqueId (ps_get_unique_id); torch.distributed (any backend, e.g.
+    gloo or nccl) broadcasts the 128 bytes to every rank of `group`."""
+    import torch.distributed as dist
+    obj = [None]
+    if rank == 0:
+        buf = ctypes.create_string_buffer(128)
+        _check("ps_get_unique_id", lib().ps_get_unique_id(buf))
+        obj = [bytes(buf.raw)]
+    dist.broadcast_object_list(obj, src=0, group=group)
+    assert isinstance(obj[0], bytes) and len(obj[0]) == 128
+    return obj[0]
+
+
 # ---------------------------------------------------------------------------------- the state
 
 class State:
@@ -220,14 +234,7 @@ class State:
         L = lib()
         nid = None
         if self.world > 1:
-            import torch.distributed as dist
-            obj = [None]
-            if self.rank == 0:
-                buf = ctypes.create_string_buffer(128)
-                _check("ps_get_unique_id", L.ps_get_unique_id(buf))
-                obj = [bytes(buf.raw)]
-            dist.broadcast_object_list(obj, src=0, group=group)
-            nid = ctypes.create_string_buffer(obj[0], 128)
+            nid = ctypes.create_string_buffer(bootstrap_nccl_id(self.rank, group), 128)
         dev_ptr, nbytes, stream = None, 0, None
         if torch_memory:
             import torch

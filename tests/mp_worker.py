@@ -1,0 +1,150 @@
+"""Multi-GPU parity worker: run under torchrun, one rank per GPU (tests/test_multigpu.py).
+
+Every check compares the sharded CUDA path (NCCL half-vector exchanges, per-rank signs) with the
+CPU oracle or with a single-GPU run; rank 0 writes a JSON report and exits non-zero on failure.
+"""
+from __future__ import annotations
+
+import json
+import os
+import sys
+import traceback
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import oracle  # noqa: E402
+import workloads  # noqa: E402
+import paper_2504_17881_b200 as P  # noqa: E402
+from paper_2504_17881_b200 import ps  # noqa: E402
+
+SEED = 250417881
+
+
+def layer_with_global(n, count, seed, world):
+    """R10 layer plus runs of rotations with X on the top (global) qubits and Z-only global terms."""
+    codes, ang = workloads.random_layer(n, count, seed=seed, kind="R10")
+    rng = np.random.default_rng(seed)
+    m = world.bit_length() - 1
+    for l in range(0, count, 7):
+        q = n - 1 - int(rng.integers(0, m))
+        codes[l, q] = rng.integers(1, 4)
+    for l in range(3, count, 11):  # a run sharing an upper X-part
+        codes[l:l + 4, n - 1] = 1
+    return codes, ang
+
+
+def main():
+    world = int(os.environ["WORLD_SIZE"])
+    rank = int(os.environ["RANK"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    report = {"world": world, "checks": []}
+    ok = True
+
+    def check(name, err, tol):
+        nonlocal ok
+        good = bool(err <= tol)
+        ok &= good
+        report["checks"].append({"name": name, "err": float(err), "tol": tol, "ok": good})
+
+    try:
+        # (a) small n against the oracle, all fusion levels, small exchange chunks
+        for n in (6, 10, 13):
+            codes, ang = layer_with_global(n, 300, n, world)
+            x, z = P.pauli_encode_codes(codes)
+            want = oracle.apply(n, oracle.random_state(SEED, n), codes, ang) if rank == 0 else None
+            for fusion in (0, 1, 2):
+                for chunk in (4096, 1 << 28):
+                    with P.State(n, "c128", world=world, rank=rank) as st:
+                        st.set_option(ps.OPT_FUSION, fusion)
+                        st.set_option(ps.OPT_TILE_BITS, 6)
+                        st.set_option(ps.OPT_CHUNK_BYTES, chunk)
+                        st.init_random(SEED)
+                        st.apply_rotations(x, z, ang)
+                        got = st.get_amplitudes()
+                        stats = st.stats()
+                    if rank == 0:
+                        check(f"oracle n={n} fusion={fusion} chunk={chunk} exch={stats['exchanges']}",
+                              np.max(np.abs(got - want)), 1e-10)
+        # (b) full-exchange fallback: local X-part covering every local bit
+        n = world.bit_length() - 1 + 3
+        words = ["X" * n, "Y" + "X" * (n - 2) + "Z", "Z" * n, "XY" * (n // 2) + "X" * (n % 2), "I" + "X" * (n - 1)]
+        codes = oracle.words_to_factors(words)
+        x, z = P.pauli_encode_codes(codes)
+        ang = np.array([0.3, -1.2, 0.7, 2.0, -0.5])
+        with P.State(n, "c128", world=world, rank=rank) as st:
+            st.init_random(SEED)
+            st.apply_rotations(x, z, ang)
+            got = st.get_amplitudes()
+        if rank == 0:
+            check(f"full-exchange fallback n={n}", np.max(np.abs(got - oracle.apply(n, oracle.random_state(SEED, n), codes, ang))), 1e-12)
+        # (c) JW-shaped first-order Trotter step, x-major order for this world size
+        n = 16
+        m = world.bit_length() - 1
+        hc, hco = workloads.jw_hamiltonian(n, 3000, 27.0, seed=1, n_local=n - m)
+        ang = workloads.trotter1_angles(hco, 0.5)
+        x, z = P.pauli_encode_codes(hc)
+        want = oracle.apply(n, oracle.random_state(SEED, n), hc, ang) if rank == 0 else None
+        with P.State(n, "c128", world=world, rank=rank) as st:
+            st.init_random(SEED)
+            st.apply_rotations(x, z, ang)
+            got = st.get_amplitudes()
+            stats = st.stats()
+            # (d) expectation of the same Hamiltonian (global-X terms need exchanges), norm, inner
+            e = st.expectation(x, z, hco)
+            nrm = st.norm()
+            with P.State(n, "c128", world=world, rank=rank) as st2:
+                st2.init_random(SEED + 1)
+                ip = st.inner(st2)
+        if rank == 0:
+            check(f"JW Trotter n=16 ({len(ang)} terms, {stats['exchanges']} exchanges)", np.max(np.abs(got - want)), 1e-10)
+            check("expectation", abs(e - oracle.expectation(n, want, hc, hco)), 1e-9)
+            check("norm", abs(nrm - oracle.norm(n, want)) / oracle.norm(n, want), 1e-12)
+            check("inner", abs(ip - oracle.inner(n, want, oracle.random_state(SEED + 1, n))), 1e-9)
+        # (e) fp32 against the oracle
+        n = 12
+        codes, ang = layer_with_global(n, 400, 5, world)
+        x, z = P.pauli_encode_codes(codes)
+        with P.State(n, "c64", world=world, rank=rank) as st:
+            st.init_random(SEED)
+            st.apply_rotations(x, z, ang)
+            got = st.get_amplitudes()
+        if rank == 0:
+            check("fp32 n=12", np.max(np.abs(got - oracle.apply(n, oracle.random_state(SEED, n), codes, ang))), 1e-4)
+        # (f) G-invariance at 24 qubits against a single-GPU run of the same layer
+        n = 24
+        codes, ang = layer_with_global(n, 500, 24, world)
+        x, z = P.pauli_encode_codes(codes)
+        with P.State(n, "c128", world=world, rank=rank) as st:
+            st.init_random(SEED)
+            st.apply_rotations(x, z, ang)
+            got = st.get_amplitudes()
+        if rank == 0:
+            with P.State(n, "c128") as one:
+                one.init_random(SEED)
+                one.apply_rotations(x, z, ang)
+                ref = one.get_amplitudes()
+            check("G-invariance n=24 vs 1 GPU", np.max(np.abs(got - ref)), 1e-12)
+    except Exception:  # noqa: BLE001
+        ok = False
+        report["error"] = traceback.format_exc()
+    report["ok"] = ok
+    flags = [None] * world
+    dist.all_gather_object(flags, ok)
+    if rank == 0:
+        path = os.environ.get("PS_MP_REPORT", "mp_report.json")
+        with open(path, "w") as fh:
+            json.dump(report, fh, indent=1)
+        print(json.dumps(report))
+    dist.destroy_process_group()
+    sys.exit(0 if all(flags) else 1)
+
+
+if __name__ == "__main__":
+    main()
