@@ -51,6 +51,8 @@ def parse():
                     help="0 cp.async prefetch, 1 TMA ring, 2 register-direct, 3 TMA-bulk prefetch")
     ap.add_argument("--chunk-bits", type=int, default=0)
     ap.add_argument("--tile-tune", type=int, default=-1)
+    ap.add_argument("--layout", type=int, default=1, help="world > 1: 1 lazy qubit swaps, 0 runs + swap-back")
+    ap.add_argument("--transport", type=int, default=1, help="world > 1: 1 NVLink P2P, 0 NCCL send/recv")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     return ap.parse_args()
@@ -234,6 +236,8 @@ def run_ours(args):
         st.set_option(ps.OPT_CHUNK_BITS, args.chunk_bits)
     if args.tile_tune >= 0:
         st.set_option(ps.OPT_TILE_TUNE, args.tile_tune)
+    st.set_option(ps.OPT_LAYOUT, args.layout)
+    st.set_option(ps.OPT_TRANSPORT, args.transport)
     st.set_option(ps.OPT_PROFILE, 1)
     lay = layers(args, args.warmup + args.steps)
     enc = [P.pauli_encode_codes(c) + (a,) for c, a in lay]
@@ -323,6 +327,7 @@ def run_ours(args):
             "data": "synthetic",
             "config": {"workload": workload_name(args), "n_qubits": args.n, "rotations_per_step": args.layer,
                        "fusion": args.fusion, "tile_mode": args.tile_mode, "tile_bits": args.tile_bits or 11,
+                       "layout": args.layout, "transport": args.transport,
                        "parallelism": f"state sharded over {world} GPU(s) by top qubits",
                        "l2": "inputs larger than L2 (state %.1f GiB per GPU)" % (local_state / 2 ** 30)},
             "hbm_gbs": hbm_alg,
@@ -331,6 +336,9 @@ def run_ours(args):
             "rotations_per_pass": rotations / passes,
             "passes": {k: stats["launches"][k] for k in ("stream", "tile", "coset")},
             "exchanges": stats["exchanges"],
+            "exchange_ms": stats["kernel_ms"]["exchange"],
+            "nvlink_gbs": (stats["nvlink_bytes"] / (stats["kernel_ms"]["exchange"] / 1e3) / 1e9
+                           if stats["kernel_ms"]["exchange"] > 0 else None),
             "roofline": {"bound": "hbm", "kernel": fam, "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "peak_source": peak_src,
                          "algorithmic_bytes_per_launch": bytes_per_launch,

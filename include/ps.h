@@ -64,8 +64,9 @@ enum {
     PS_K_COSET = 2,    /* K7: coset-tile fused pass (gathered 2^k tile)                       */
     PS_K_REDUCE = 3,   /* K5: norm / expectation / inner-product reductions                   */
     PS_K_INIT = 4,     /* K6: state initialisation                                            */
-    PS_K_EXCHANGE = 5, /* K3: half-vector exchange (staging copies + NCCL send/recv)          */
-    PS_K_COUNT = 6
+    PS_K_EXCHANGE = 5, /* K3: half-vector exchange (NVLink P2P swap or NCCL send/recv)       */
+    PS_K_PERMUTE = 6,  /* local qubit transposition pass (restoring the canonical layout)     */
+    PS_K_COUNT = 7
 };
 
 typedef struct ps_stats {
@@ -93,8 +94,13 @@ enum {
                                  3 = TMA-bulk-prefetched double buffer (A/B) */
     PS_OPT_CHUNK_BITS = 7,    /* min log2 contiguous amplitudes per gathered chunk (0 = default:
                                  4 for C128, 5 for C64, i.e. 256 B) */
-    PS_OPT_TILE_TUNE = 8      /* register-direct tile kernel tuning: bit 0 = L2 prefetch of the next
+    PS_OPT_TILE_TUNE = 8,     /* register-direct tile kernel tuning: bit 0 = L2 prefetch of the next
                                  tile, bits 4.. = persistent-grid multiplier (0 = default) */
+    PS_OPT_LAYOUT = 9,        /* world > 1: 1 = lazy qubit-swap layout kept across calls, swaps chosen
+                                 by furthest next use (default); 0 = one half-vector exchange per run
+                                 sharing the upper X-part, swapped back at once (Eq. (1) economy) */
+    PS_OPT_TRANSPORT = 10     /* world > 1: 1 = NVLink P2P swap kernel on CUDA-IPC peer pointers when
+                                 available (default); 0 = NCCL send/recv with staging */
 };
 
 /* ------------------------------------------------------------------------------------------ */
@@ -217,15 +223,17 @@ int ps_gate_to_rotations(const char *gate, const int *qubits, int n_qubits_gate,
                          double *angle, size_t cap, size_t *n_out);
 
 /* Planner dump (host only; for tests and plan inspection).  Plans `count` rotations for an
- * n-qubit state on `world` GPUs as seen by `rank`, with the given fusion level and tile bits,
- * and writes up to cap ops.  Each op is one HBM pass or one exchange; for a pass, the
- * rotations it applies are given in PHYSICAL local coordinates. */
+ * n-qubit state on `world` GPUs as seen by `rank`, with the given fusion level, tile bits and
+ * layout policy (PS_OPT_LAYOUT), starting from and returning to the canonical layout, and writes
+ * up to cap ops.  Each op is one HBM pass, one exchange or one local transposition; for a pass,
+ * the rotations it applies are given in PHYSICAL local coordinates. */
 typedef struct ps_plan_op {
-    int32_t kind;        /* PS_K_STREAM, PS_K_TILE, PS_K_COSET or PS_K_EXCHANGE */
+    int32_t kind;        /* PS_K_STREAM, PS_K_TILE, PS_K_COSET, PS_K_EXCHANGE or PS_K_PERMUTE */
     int32_t first_rot;   /* index of the first input rotation covered */
-    int32_t n_rot;       /* input rotations covered */
-    int32_t exch_bit;    /* EXCHANGE: local pivot bit l swapped with the partner */
-    uint64_t exch_gx;    /* EXCHANGE: partner = rank xor exch_gx */
+    int32_t n_rot;       /* rotations applied by this op (EXCHANGE: 0, or 1 for a full exchange) */
+    int32_t exch_bit;    /* EXCHANGE: local pivot bit l swapped with the partner (-1: full exchange);
+                            PERMUTE: first local bit of the transposition */
+    uint64_t exch_gx;    /* EXCHANGE: partner = rank xor exch_gx; PERMUTE: second local bit */
     uint32_t tile_bits;  /* TILE/COSET: log2 tile size */
     uint32_t pad;
 } ps_plan_op;
@@ -239,7 +247,7 @@ typedef struct ps_plan_rot {
     double angle; /* phi */
 } ps_plan_rot;
 
-int ps_plan_describe(int n_qubits, int world, int rank, int fusion, int tile_bits,
+int ps_plan_describe(int n_qubits, int world, int rank, int fusion, int tile_bits, int layout,
                      const uint64_t *xmask, const uint64_t *zmask, const double *angle,
                      size_t count, ps_plan_op *ops, size_t ops_cap, size_t *n_ops,
                      ps_plan_rot *rots, size_t rots_cap, size_t *n_rots);

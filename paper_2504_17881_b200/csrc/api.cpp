@@ -1,6 +1,7 @@
 // api.cpp -- the C ABI of libps (include/ps.h): handles, device memory, streams, NCCL, and the
 // execution of plans produced by planner.cpp.  Argument marshalling and orchestration only;
 // every step of the path runs in the kernels of kernels.cu (or NCCL for exchanges).
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <nccl.h>
 
@@ -32,6 +33,9 @@ cudaError_t launch_expect(int dtype, const void* a, uint64_t n, uint64_t x0, con
 cudaError_t launch_init_random(int dtype, void* a, uint64_t n, uint64_t seed, uint64_t goff, cudaStream_t s);
 cudaError_t launch_set_one(int dtype, void* a, uint64_t idx, cudaStream_t s);
 cudaError_t launch_scale(int dtype, void* a, uint64_t n, double f, cudaStream_t s);
+cudaError_t launch_permute(int dtype, void* a, int nl, int b1, int b2, cudaStream_t s);
+cudaError_t launch_p2p_swap(int dtype, void* local, void* peer, uint64_t rows, uint64_t row_amps, uint64_t my_off,
+                            uint64_t peer_off, uint64_t e0, uint64_t e1, cudaStream_t s);
 
 static thread_local std::string g_last_error;
 void set_last_error(const std::string& msg) { g_last_error = msg; }
@@ -78,6 +82,13 @@ struct ps_state {
     void* d_xstage[2] = {nullptr, nullptr};
     size_t xstage_bytes = 0;
     size_t chunk_bytes = 256ull << 20;
+    // layout (world > 1): physical bit -> logical qubit; identity = canonical
+    std::vector<int> perm;
+    int* d_barrier = nullptr;
+    std::vector<void*> peers;  // CUDA-IPC peer pointers to every rank's local slice (P2P transport)
+    std::vector<void*> peer_bases;
+    bool p2p = false;
+    int layout = 1, transport = 1;
     // options
     int profile = 0, fusion = 2, tile_bits = 11, vec256 = 1, max_pass_rots = 1 << 30, tile_tma = 2, chunk_bits = 0, tile_tune = 0;
     ps_stats stats{};
@@ -192,6 +203,9 @@ static void free_state(ps_state* h) {
     if (h->stream) cudaStreamSynchronize(h->stream);
     drain_timings(h);
     for (auto e : h->event_pool) cudaEventDestroy(e);
+    for (void* b : h->peer_bases)
+        if (b) cudaIpcCloseMemHandle(b);
+    if (h->d_barrier) cudaFree(h->d_barrier);
     if (h->comm) ncclCommDestroy(h->comm);
     for (int t = 0; t < 2; ++t) {
         if (h->d_xstage[t]) cudaFree(h->d_xstage[t]);
@@ -212,6 +226,75 @@ static void free_state(ps_state* h) {
 }
 
 extern "C" int ps_init_basis(ps_handle h, uint64_t index);
+static void reset_layout(ps_state* h);
+static int restore_layout(ps_state* h);
+
+// CUDA-IPC peer pointers to every rank's local slice: the allocation base is exported with its
+// offset (cuMemGetAddressRange through the runtime's driver entry point), all-gathered with NCCL
+struct IpcRec {
+    cudaIpcMemHandle_t handle;
+    uint64_t offset;
+    int32_t ok;
+    int32_t pad;
+};
+
+static void setup_p2p(ps_state* h) {
+    h->p2p = false;
+    IpcRec mine{};
+    mine.ok = 0;
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) == cudaSuccess && fn) {
+        typedef CUresult (*GetRange)(CUdeviceptr*, size_t*, CUdeviceptr);
+        CUdeviceptr base = 0;
+        size_t size = 0;
+        if (((GetRange)fn)(&base, &size, (CUdeviceptr)h->d_state) == CUDA_SUCCESS &&
+            cudaIpcGetMemHandle(&mine.handle, (void*)base) == cudaSuccess) {
+            mine.offset = (uint64_t)((CUdeviceptr)h->d_state - base);
+            mine.ok = 1;
+        }
+    }
+    cudaGetLastError();
+    IpcRec* d_all = nullptr;
+    if (cudaMalloc(&d_all, sizeof(IpcRec) * (h->world + 1)) != cudaSuccess) return;
+    std::vector<IpcRec> all(h->world);
+    bool ok = cudaMemcpyAsync(d_all + h->world, &mine, sizeof(IpcRec), cudaMemcpyHostToDevice, h->stream) == cudaSuccess &&
+              ncclAllGather(d_all + h->world, d_all, sizeof(IpcRec), ncclChar, h->comm, h->stream) == ncclSuccess &&
+              cudaMemcpyAsync(all.data(), d_all, sizeof(IpcRec) * h->world, cudaMemcpyDeviceToHost, h->stream) ==
+                  cudaSuccess &&
+              cudaStreamSynchronize(h->stream) == cudaSuccess;
+    cudaFree(d_all);
+    int my_ok = ok ? 1 : 0;
+    h->peers.assign(h->world, nullptr);
+    h->peer_bases.assign(h->world, nullptr);
+    for (int r = 0; r < h->world && my_ok; ++r) {
+        if (!all[r].ok) {
+            my_ok = 0;
+            break;
+        }
+        if (r == h->rank) {
+            h->peers[r] = h->d_state;
+            continue;
+        }
+        void* b = nullptr;
+        if (cudaIpcOpenMemHandle(&b, all[r].handle, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+            cudaGetLastError();
+            my_ok = 0;
+            break;
+        }
+        h->peer_bases[r] = b;
+        h->peers[r] = (char*)b + all[r].offset;
+    }
+    // every rank must agree (the transport is collective)
+    int* d_flag = h->d_barrier;
+    int agree = my_ok;
+    if (cudaMemcpyAsync(d_flag, &agree, sizeof(int), cudaMemcpyHostToDevice, h->stream) == cudaSuccess &&
+        ncclAllReduce(d_flag, d_flag, 1, ncclInt32, ncclMin, h->comm, h->stream) == ncclSuccess &&
+        cudaMemcpyAsync(&agree, d_flag, sizeof(int), cudaMemcpyDeviceToHost, h->stream) == cudaSuccess &&
+        cudaStreamSynchronize(h->stream) == cudaSuccess)
+        h->p2p = agree == 1;
+    cudaMemsetAsync(d_flag, 0, sizeof(int), h->stream);
+}
 
 extern "C" int ps_create_ex(int n_qubits, int dtype, void* dev_buf, size_t bytes, void* stream, int rank,
                             int world, const void* nccl_id, ps_handle* out) {
@@ -268,11 +351,17 @@ extern "C" int ps_create_ex(int n_qubits, int dtype, void* dev_buf, size_t bytes
         if ((e = cudaEventCreateWithFlags(&h->h_stage_ev[t], cudaEventDisableTiming)) != cudaSuccess)
             return bail(PS_ECUDA, std::string("event: ") + cudaGetErrorString(e));
     }
+    h->perm.resize(n_qubits);
+    for (int q = 0; q < n_qubits; ++q) h->perm[q] = q;
     if (world > 1) {
         ncclUniqueId id;
         std::memcpy(&id, nccl_id, 128);
         ncclResult_t r = ncclCommInitRank(&h->comm, world, id, rank);
         if (r != ncclSuccess) return bail(PS_ENCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
+        if ((e = cudaMalloc(&h->d_barrier, sizeof(int) * 4)) != cudaSuccess)
+            return bail(PS_ENOMEM, std::string("barrier: ") + cudaGetErrorString(e));
+        cudaMemset(h->d_barrier, 0, sizeof(int) * 4);
+        setup_p2p(h);  // best effort; NCCL send/recv otherwise
     }
     rc = ps_init_basis(h, 0);
     if (rc) {
@@ -333,6 +422,11 @@ extern "C" int ps_set_option(ps_handle h, int option, int64_t value) {
         break;
     case PS_OPT_VEC256: h->vec256 = value ? 1 : 0; break;
     case PS_OPT_TILE_TUNE: h->tile_tune = (int)value; break;
+    case PS_OPT_LAYOUT:
+        if (value < 0 || value > 1) return fail(PS_EINVAL, "layout must be 0 or 1");
+        h->layout = (int)value;
+        break;
+    case PS_OPT_TRANSPORT: h->transport = value ? 1 : 0; break;
     case PS_OPT_CHUNK_BITS:
         if (value < 0 || value > 12) return fail(PS_EINVAL, "chunk bits must be 0..12 (0 = default)");
         h->chunk_bits = (int)value;
@@ -354,6 +448,7 @@ static uint64_t local_amps(const ps_state* h) { return 1ull << h->nl; }
 extern "C" int ps_init_basis(ps_handle h, uint64_t index) {
     CHECK_HANDLE(h);
     if (h->n < 64 && index >> h->n) return fail(PS_ERANGE, "basis index >= 2^n");
+    reset_layout(h);  // the whole state is overwritten
     Timed t(h, PS_K_INIT);
     CUDA_TRY(h, cudaMemsetAsync(h->d_state, 0, h->amp_bytes * local_amps(h), h->stream));
     if ((index >> h->nl) == (uint64_t)h->rank) CUDA_TRY(h, launch_set_one(h->dtype, h->d_state, index & (local_amps(h) - 1), h->stream));
@@ -363,6 +458,7 @@ extern "C" int ps_init_basis(ps_handle h, uint64_t index) {
 
 extern "C" int ps_init_random(ps_handle h, uint64_t seed) {
     CHECK_HANDLE(h);
+    reset_layout(h);  // the whole state is overwritten
     Timed t(h, PS_K_INIT);
     CUDA_TRY(h, launch_init_random(h->dtype, h->d_state, local_amps(h), seed, (uint64_t)h->rank << h->nl, h->stream));
     h->stats.launches[PS_K_INIT] += 1;
@@ -395,6 +491,10 @@ extern "C" int ps_set_state(ps_handle h, uint64_t first, uint64_t count, const v
     if (count && !amps) return fail(PS_EINVAL, "NULL amps with count > 0");
     int rc = check_range(h, first, count);
     if (rc) return rc;
+    if (first == 0 && h->n < 64 && count == (1ull << h->n))
+        reset_layout(h);  // the whole state is overwritten
+    else if ((rc = restore_layout(h)))
+        return rc;
     const uint64_t lo = (uint64_t)h->rank << h->nl, hi = lo + local_amps(h);
     const uint64_t a = std::max(lo, first), b = std::min(hi, first + count);
     if (a < b) {
@@ -424,6 +524,7 @@ extern "C" int ps_get_amplitudes(ps_handle h, uint64_t first, uint64_t count, vo
     if (count && !amps_out) return fail(PS_EINVAL, "NULL amps_out with count > 0");
     int rc = check_range(h, first, count);
     if (rc) return rc;
+    if ((rc = restore_layout(h))) return rc;
     if (h->world == 1) {
         if (count)
             CUDA_TRY(h, cudaMemcpyAsync(amps_out, (const char*)h->d_state + first * h->amp_bytes, count * h->amp_bytes,
@@ -456,6 +557,11 @@ extern "C" int ps_get_amplitudes(ps_handle h, uint64_t first, uint64_t count, vo
 // ------------------------------------------------------------------------------------------
 // exchanges (K3): half-vector swap of slots with bit ell == 1-keep with partner rank^gx
 
+static int barrier(ps_state* h) {
+    NCCL_TRY(h, ncclAllReduce(h->d_barrier, h->d_barrier, 1, ncclInt32, ncclSum, h->comm, h->stream));
+    return PS_OK;
+}
+
 static int exchange_half(ps_state* h, const Pass& p) {
     const int partner = h->rank ^ (int)p.gx;
     const size_t s = h->amp_bytes;
@@ -463,6 +569,22 @@ static int exchange_half(ps_state* h, const Pass& p) {
     const size_t row_bytes = s << p.ell;
     const size_t start = (size_t)(1 - p.keep) * row_bytes;
     const size_t chunk = h->chunk_bytes;
+    if (h->p2p && h->transport) {
+        // both ranks of the pair swap their regions in place through NVLink peer pointers, each
+        // doing half of the elements; barriers order it against all earlier and later work
+        const uint64_t row_amps = 1ull << p.ell, total = rows * row_amps;
+        const uint64_t e0 = p.keep ? total / 2 : 0, e1 = p.keep ? total : total / 2;
+        int rc = barrier(h);
+        if (rc) return rc;
+        CUDA_TRY(h, launch_p2p_swap(h->dtype, h->d_state, h->peers[partner], rows, row_amps,
+                                    (uint64_t)(1 - p.keep) * row_amps, (uint64_t)p.keep * row_amps, e0, e1, h->stream));
+        rc = barrier(h);
+        if (rc) return rc;
+        h->stats.nvlink_bytes += (double)(rows * row_bytes);
+        h->stats.exchanges += 1;
+        h->stats.algo_bytes[PS_K_EXCHANGE] += (double)(rows * row_bytes) * 2.0;
+        return PS_OK;
+    }
     int rc = ensure_xstage(h, std::min(chunk, row_bytes * rows));
     if (rc) return rc;
     char* base = (char*)h->d_state;
@@ -592,19 +714,13 @@ static PlanConfig plan_config(const ps_state* h) {
     cfg.min_chunk_bits = h->chunk_bits ? h->chunk_bits : (h->dtype == PS_C128 ? 4 : 5);  // >= 256-B chunks
     cfg.phase_bits = h->dtype == PS_C128 ? 3 : 4;      // 16-B vs 8-B shared-memory accesses
     cfg.max_pass_rots = h->max_pass_rots;
+    cfg.layout = h->layout;
+    cfg.perm = h->perm;
     return cfg;
 }
 
-extern "C" int ps_apply_rotations(ps_handle h, const uint64_t* xmask, const uint64_t* zmask, const double* angle,
-                                  size_t count) {
-    CHECK_HANDLE(h);
-    std::string err;
-    int rc = validate_rotations(h->n, xmask, zmask, angle, count, &err);
-    if (rc) return fail(rc, "ps_apply_rotations: " + err);
-    if (count == 0) return PS_OK;
-    Plan& plan = h->plan;
-    make_plan(plan_config(h), xmask, zmask, angle, count, &plan);
-    rc = upload_plan(h, plan);
+static int execute_plan(ps_state* h, const Plan& plan) {
+    int rc = upload_plan(h, plan);
     if (rc) return rc;
     const double pass_bytes = 2.0 * (double)h->amp_bytes * (double)local_amps(h);
     for (const Pass& p : plan.passes) {
@@ -617,8 +733,16 @@ extern "C" int ps_apply_rotations(ps_handle h, const uint64_t* xmask, const uint
         case PASS_TILE:
         case PASS_COSET: {
             Timed t(h, p.kind);
-            CUDA_TRY(h, launch_tile(h->dtype, h->d_state, h->nl, p, h->d_subs, h->d_trots, h->d_offs, h->tile_tma, h->tile_tune, h->stream));
+            CUDA_TRY(h, launch_tile(h->dtype, h->d_state, h->nl, p, h->d_subs, h->d_trots, h->d_offs, h->tile_tma,
+                                    h->tile_tune, h->stream));
             break;
+        }
+        case PASS_PERMUTE: {
+            Timed t(h, PS_K_PERMUTE);
+            CUDA_TRY(h, launch_permute(h->dtype, h->d_state, h->nl, p.ell, p.ell2, h->stream));
+            h->stats.launches[PS_K_PERMUTE] += 1;
+            h->stats.algo_bytes[PS_K_PERMUTE] += pass_bytes / 2;  // half the amplitudes move
+            continue;
         }
         case PASS_EXCHANGE: {
             Timed t(h, PS_K_EXCHANGE);
@@ -638,6 +762,46 @@ extern "C" int ps_apply_rotations(ps_handle h, const uint64_t* xmask, const uint
         h->stats.algo_bytes[p.kind] += pass_bytes;
         h->stats.passes += 1;
     }
+    return PS_OK;
+}
+
+static bool layout_canonical(const ps_state* h) {
+    for (int q = 0; q < (int)h->perm.size(); ++q)
+        if (h->perm[q] != q) return false;
+    return true;
+}
+
+static void reset_layout(ps_state* h) {
+    for (int q = 0; q < (int)h->perm.size(); ++q) h->perm[q] = q;
+}
+
+// brings the state back to the canonical layout (rank = top qubits, identity within ranks)
+static int restore_layout(ps_state* h) {
+    if (h->world == 1 || layout_canonical(h)) return PS_OK;
+    PlanConfig cfg = plan_config(h);
+    Plan rp;
+    make_restore_plan(cfg, h->perm, &rp);
+    int rc = execute_plan(h, rp);
+    if (rc) return rc;
+    reset_layout(h);
+    return PS_OK;
+}
+
+extern "C" int ps_apply_rotations(ps_handle h, const uint64_t* xmask, const uint64_t* zmask, const double* angle,
+                                  size_t count) {
+    CHECK_HANDLE(h);
+    std::string err;
+    int rc = validate_rotations(h->n, xmask, zmask, angle, count, &err);
+    if (rc) return fail(rc, "ps_apply_rotations: " + err);
+    if (count == 0) return PS_OK;
+    Plan& plan = h->plan;
+    make_plan(plan_config(h), xmask, zmask, angle, count, &plan);
+    rc = execute_plan(h, plan);
+    if (rc) return rc;
+    if (plan.perm_out.size() == h->perm.size())
+        h->perm = plan.perm_out;
+    else
+        reset_layout(h);
     h->stats.rotations += count;
     return PS_OK;
 }
@@ -678,6 +842,9 @@ extern "C" int ps_inner(ps_handle a, ps_handle b, double* out) {
     if (!out) return fail(PS_EINVAL, "NULL out");
     if (a->n != b->n || a->dtype != b->dtype || a->world != b->world || a->rank != b->rank || a->device != b->device)
         return fail(PS_EINVAL, "ps_inner: handles differ in n, dtype, world, rank or device");
+    int rc0 = restore_layout(a);
+    if (!rc0) rc0 = restore_layout(b);
+    if (rc0) return rc0;
     if (b->stream != a->stream) {
         CUDA_TRY(b, cudaStreamSynchronize(b->stream));
     }
@@ -704,6 +871,7 @@ extern "C" int ps_expectation(ps_handle h, const uint64_t* xmask, const uint64_t
     if (rc) return fail(rc, "ps_expectation: " + err);
     *out = 0.0;
     if (count == 0) return PS_OK;
+    if ((rc = restore_layout(h))) return rc;
     const int nl = h->nl;
     const uint64_t lmask = (1ull << nl) - 1;
     const uint64_t rank = (uint64_t)h->rank;

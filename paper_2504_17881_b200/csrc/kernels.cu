@@ -1001,6 +1001,53 @@ __global__ void k_scale(T* __restrict__ a, uint64_t n, double f) {
         a[i] = (T)((double)a[i] * f);
 }
 
+// local transposition of bits b1 < b2: swap a[i] <-> a[i ^ (2^b1 | 2^b2)] for bit b1 = 0, b2 = 1
+template <typename T>
+__global__ void k_permute(T* __restrict__ a, uint64_t quarter, int b1, int b2) {
+    using V2 = typename SmemAmp<T>::V;
+    V2* g = reinterpret_cast<V2*>(a);
+    const uint64_t m = (1ull << b1) | (1ull << b2);
+    for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < quarter; t += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t i = insert0(insert0(t, b1), b2) | (1ull << b2);
+        const uint64_t j = i ^ m;
+        const V2 u = g[i], v = g[j];
+        g[i] = v;
+        g[j] = u;
+    }
+}
+
+// NVLink P2P half swap: local region element e (row, col) <-> the partner's matching element
+template <typename T>
+__global__ void k_p2p_swap(T* __restrict__ local, T* __restrict__ peer, uint64_t row_amps, uint64_t my_off,
+                           uint64_t peer_off, uint64_t e0, uint64_t e1) {
+    using V2 = typename SmemAmp<T>::V;
+    V2* L = reinterpret_cast<V2*>(local);
+    V2* R = reinterpret_cast<V2*>(peer);
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t e = e0 + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < e1; e += 2 * stride) {
+        const uint64_t e2 = e + stride;
+        const uint64_t row = e / row_amps, col = e - row * row_amps;
+        const uint64_t li = row * 2 * row_amps + my_off + col, ri = row * 2 * row_amps + peer_off + col;
+        const V2 u = L[li], v = __ldcv(&R[ri]);
+        V2 u2, v2;
+        uint64_t li2 = 0, ri2 = 0;
+        const bool has2 = e2 < e1;
+        if (has2) {
+            const uint64_t r2 = e2 / row_amps, c2 = e2 - r2 * row_amps;
+            li2 = r2 * 2 * row_amps + my_off + c2;
+            ri2 = r2 * 2 * row_amps + peer_off + c2;
+            u2 = L[li2];
+            v2 = __ldcv(&R[ri2]);
+        }
+        L[li] = v;
+        __stcg(&R[ri], u);
+        if (has2) {
+            L[li2] = v2;
+            __stcg(&R[ri2], u2);
+        }
+    }
+}
+
 int g_num_sms = 0;
 int num_sms() {
     if (g_num_sms == 0) {
@@ -1221,6 +1268,29 @@ cudaError_t launch_set_one(int dtype, void* a, uint64_t idx, cudaStream_t s) {
         k_set_one<double><<<1, 1, 0, s>>>((double*)a, idx);
     else
         k_set_one<float><<<1, 1, 0, s>>>((float*)a, idx);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_permute(int dtype, void* a, int nl, int b1, int b2, cudaStream_t s) {
+    const uint64_t quarter = 1ull << (nl - 2);
+    const unsigned grid = red_grid(quarter) * 2;
+    if (b1 > b2) { const int t = b1; b1 = b2; b2 = t; }
+    if (dtype == PS_C128)
+        k_permute<double><<<grid, kRedThreads, 0, s>>>((double*)a, quarter, b1, b2);
+    else
+        k_permute<float><<<grid, kRedThreads, 0, s>>>((float*)a, quarter, b1, b2);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_p2p_swap(int dtype, void* local, void* peer, uint64_t rows, uint64_t row_amps, uint64_t my_off,
+                            uint64_t peer_off, uint64_t e0, uint64_t e1, cudaStream_t s) {
+    (void)rows;
+    if (e1 <= e0) return cudaSuccess;
+    const unsigned grid = (unsigned)num_sms() * 4;
+    if (dtype == PS_C128)
+        k_p2p_swap<double><<<grid, 512, 0, s>>>((double*)local, (double*)peer, row_amps, my_off, peer_off, e0, e1);
+    else
+        k_p2p_swap<float><<<grid, 512, 0, s>>>((float*)local, (float*)peer, row_amps, my_off, peer_off, e0, e1);
     return cudaGetLastError();
 }
 

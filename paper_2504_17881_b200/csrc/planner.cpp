@@ -386,8 +386,7 @@ static void form_passes(const std::vector<PhysRot>& seg, const PlanConfig& cfg, 
 // ------------------------------------------------------------------------------------------
 // full plan: layout (exchanges) then passes
 
-void make_plan(const PlanConfig& cfg, const uint64_t* x, const uint64_t* z, const double* angle,
-               size_t count, Plan* plan) {
+static void clear_plan(Plan* plan) {
     plan->passes.clear();
     plan->rots.clear();
     plan->offsets.clear();
@@ -395,6 +394,201 @@ void make_plan(const PlanConfig& cfg, const uint64_t* x, const uint64_t* z, cons
     plan->trots.clear();
     plan->debug_rots.clear();
     plan->exchanges = 0;
+}
+
+static void push_debug_rot(const PlanConfig& cfg, Plan* plan, const PhysRot& pr) {
+    if (!cfg.want_debug) return;
+    ps_plan_rot d;
+    d.x = pr.x;
+    d.z = pr.z;
+    d.y = pr.y;
+    d.sign = pr.sign;
+    d.angle = pr.phi;
+    plan->debug_rots.push_back(d);
+}
+
+// single-rotation full exchange (no free pivot): rotation given in physical coordinates
+static void emit_full_exchange(const PlanConfig& cfg, Plan* plan, uint64_t gx, const PhysRot& pr) {
+    Pass p;
+    p.kind = PASS_EXCHANGE;
+    p.full = 1;
+    p.gx = gx;
+    p.rot_begin = (int)plan->rots.size();
+    p.rot_count = 1;
+    p.first_input = pr.input;
+    p.n_input = 1;
+    push_debug_rot(cfg, plan, pr);
+    plan->rots.push_back(make_rec(pr.x, pr.z, 0, pr.y, pr.sign, pr.phi));
+    plan->passes.push_back(p);
+    plan->exchanges += 1;
+}
+
+// transposition of physical rank bit j (global bit nl + j) with local bit ell as a half-vector
+// exchange with rank r xor 2^j
+static void emit_swap_exchange(const PlanConfig& cfg, Plan* plan, int j, int ell, int first_input) {
+    Pass ex;
+    ex.kind = PASS_EXCHANGE;
+    ex.gx = 1ull << j;
+    ex.ell = ell;
+    ex.keep = (cfg.rank >> j) & 1;
+    ex.first_input = first_input;
+    ex.n_input = 0;
+    plan->passes.push_back(ex);
+    plan->exchanges += 1;
+}
+
+static void emit_permute(Plan* plan, int a, int b, int first_input) {
+    Pass p;
+    p.kind = PASS_PERMUTE;
+    p.ell = std::min(a, b);
+    p.ell2 = std::max(a, b);
+    p.first_input = first_input;
+    p.n_input = 0;
+    plan->passes.push_back(p);
+}
+
+static uint64_t map_mask(uint64_t m, const std::vector<int>& inv) {
+    uint64_t out = 0;
+    while (m) {
+        const int q = __builtin_ctzll(m);
+        m &= m - 1;
+        out |= 1ull << inv[q];
+    }
+    return out;
+}
+
+void make_restore_plan(const PlanConfig& cfg, const std::vector<int>& perm_in, Plan* plan) {
+    const int n = cfg.n, nl = cfg.n_local;
+    std::vector<int> perm = perm_in, inv(n);
+    if ((int)perm.size() != n) {
+        perm.resize(n);
+        for (int q = 0; q < n; ++q) perm[q] = q;
+    }
+    for (int p = 0; p < n; ++p) inv[perm[p]] = p;
+    auto swap_pos = [&](int a, int b) {
+        std::swap(perm[a], perm[b]);
+        inv[perm[a]] = a;
+        inv[perm[b]] = b;
+    };
+    // 1. every global position gets its canonical qubit back (exchanges)
+    for (int g = nl; g < n; ++g) {
+        if (perm[g] == g) continue;
+        int p = inv[g];
+        if (p >= nl) {  // canonical qubit sits in another global slot: move it local first
+            const int ell = nl - 1;
+            emit_swap_exchange(cfg, plan, p - nl, ell, -1);
+            swap_pos(p, ell);
+            p = ell;
+        }
+        emit_swap_exchange(cfg, plan, g - nl, p, -1);
+        swap_pos(g, p);
+    }
+    // 2. local transpositions (HBM passes)
+    for (int ell = 0; ell < nl; ++ell) {
+        if (perm[ell] == ell) continue;
+        const int p = inv[ell];
+        emit_permute(plan, ell, p, -1);
+        swap_pos(ell, p);
+    }
+    plan->perm_out.assign(n, 0);
+    for (int q = 0; q < n; ++q) plan->perm_out[q] = q;
+}
+
+// lazy qubit-swap layout: a rotation whose X-part touches a global position first swaps that
+// position's qubit with the local qubit whose next X-use is furthest in the future (Belady);
+// the layout is not restored at the end (plan->perm_out)
+static void plan_lazy(const PlanConfig& cfg, const uint64_t* x, const uint64_t* z, const double* angle,
+                      size_t count, Plan* plan) {
+    const int n = cfg.n, nl = cfg.n_local;
+    const uint64_t lmask = (1ull << nl) - 1;
+    const uint64_t rank = (uint64_t)cfg.rank;
+    std::vector<int> perm = cfg.perm, inv(n);
+    if ((int)perm.size() != n) {
+        perm.resize(n);
+        for (int q = 0; q < n; ++q) perm[q] = q;
+    }
+    for (int p = 0; p < n; ++p) inv[perm[p]] = p;
+    // next X-use per logical qubit
+    std::vector<std::vector<int>> uses(n);
+    for (size_t l = 0; l < count; ++l)
+        for (uint64_t m = x[l]; m; m &= m - 1) uses[__builtin_ctzll(m)].push_back((int)l);
+    std::vector<size_t> ptr(n, 0);
+    auto next_use = [&](int q, int after) -> long {
+        auto& u = uses[q];
+        size_t& k = ptr[q];
+        while (k < u.size() && u[k] <= after) ++k;
+        return k < u.size() ? (long)u[k] : (long)1 << 40;
+    };
+    std::vector<PhysRot> seg;
+    auto flush = [&]() {
+        form_passes(seg, cfg, plan);
+        seg.clear();
+    };
+    for (size_t l = 0; l < count; ++l) {
+        uint64_t xp = map_mask(x[l], inv);
+        bool full = false;
+        while (xp >> nl) {
+            const int g = nl + __builtin_ctzll(xp >> nl);
+            // candidate local positions whose qubit is not in this rotation's X-part
+            int best = -1;
+            long best_use = -1;
+            for (int ell = nl - 1; ell >= 0; --ell) {
+                const int q = perm[ell];
+                if ((x[l] >> q) & 1) continue;
+                long u = next_use(q, (int)l);
+                if (perm[g] == ell && q == g) u += 1;  // tie-break: swaps that restore canonical
+                if (u > best_use) {
+                    best_use = u;
+                    best = ell;
+                }
+            }
+            if (best < 0) {
+                full = true;
+                break;
+            }
+            flush();
+            emit_swap_exchange(cfg, plan, g - nl, best, (int)l);
+            std::swap(perm[g], perm[best]);
+            inv[perm[g]] = g;
+            inv[perm[best]] = best;
+            xp = map_mask(x[l], inv);
+        }
+        const uint64_t zp = map_mask(z[l], inv);
+        PhysRot pr;
+        pr.x = xp & lmask;
+        pr.z = zp & lmask;
+        pr.y = popc64(x[l] & z[l]) & 3;
+        pr.sign = parity64((zp >> nl) & rank) ? -1 : 1;
+        pr.phi = angle[l];
+        pr.input = (int)l;
+        if (full) {
+            flush();
+            emit_full_exchange(cfg, plan, xp >> nl, pr);
+            continue;
+        }
+        seg.push_back(pr);
+        push_debug_rot(cfg, plan, pr);
+    }
+    flush();
+    plan->perm_out = perm;
+}
+
+void make_plan(const PlanConfig& cfg, const uint64_t* x, const uint64_t* z, const double* angle,
+               size_t count, Plan* plan) {
+    clear_plan(plan);
+    if (cfg.world > 1 && cfg.layout == 1) {
+        plan_lazy(cfg, x, z, angle, count, plan);
+        return;
+    }
+    if ((int)cfg.perm.size() == cfg.n) {
+        for (int q = 0; q < cfg.n; ++q)
+            if (cfg.perm[q] != q) {
+                // run mode needs the canonical layout: restore first
+                make_restore_plan(cfg, cfg.perm, plan);
+                break;
+            }
+    }
+    plan->perm_out.clear();
     const int nl = cfg.n_local;
     const uint64_t lmask = (nl >= 64) ? ~0ull : ((1ull << nl) - 1);
     const uint64_t rank = (uint64_t)cfg.rank;
@@ -450,14 +644,6 @@ void make_plan(const PlanConfig& cfg, const uint64_t* x, const uint64_t* z, cons
         flush();
         if (last == count) {
             // no free pivot even for rotation i alone: single-rotation full exchange
-            Pass p;
-            p.kind = PASS_EXCHANGE;
-            p.full = 1;
-            p.gx = gx;
-            p.rot_begin = (int)plan->rots.size();
-            p.rot_count = 1;
-            p.first_input = (int)i;
-            p.n_input = 1;
             PhysRot pr;
             pr.x = x[i] & lmask;
             pr.z = z[i] & lmask;
@@ -465,10 +651,7 @@ void make_plan(const PlanConfig& cfg, const uint64_t* x, const uint64_t* z, cons
             pr.sign = parity64((z[i] >> nl) & rank) ? -1 : 1;
             pr.phi = angle[i];
             pr.input = (int)i;
-            push_debug(pr);
-            plan->rots.push_back(make_rec(pr.x, pr.z, 0, pr.y, pr.sign, pr.phi));
-            plan->passes.push_back(p);
-            plan->exchanges += 1;
+            emit_full_exchange(cfg, plan, gx, pr);
             ++i;
             continue;
         }
@@ -680,7 +863,7 @@ extern "C" int ps_gate_to_rotations(const char* gate, const int* qubits, int nq,
     return PS_OK;
 }
 
-extern "C" int ps_plan_describe(int n_qubits, int world, int rank, int fusion, int tile_bits,
+extern "C" int ps_plan_describe(int n_qubits, int world, int rank, int fusion, int tile_bits, int layout,
                                 const uint64_t* xmask, const uint64_t* zmask, const double* angle,
                                 size_t count, ps_plan_op* ops, size_t ops_cap, size_t* n_ops,
                                 ps_plan_rot* rots, size_t rots_cap, size_t* n_rots) {
@@ -708,8 +891,10 @@ extern "C" int ps_plan_describe(int n_qubits, int world, int rank, int fusion, i
     cfg.fusion = fusion;
     cfg.tile_bits = tile_bits > 0 ? tile_bits : 12;
     cfg.want_debug = true;
+    cfg.layout = layout;
     Plan plan;
     make_plan(cfg, xmask, zmask, angle, count, &plan);
+    if (!plan.perm_out.empty()) make_restore_plan(cfg, plan.perm_out, &plan);
     if (n_ops) *n_ops = plan.passes.size();
     if (n_rots) *n_rots = plan.debug_rots.size();
     if (ops) {
@@ -718,9 +903,9 @@ extern "C" int ps_plan_describe(int n_qubits, int world, int rank, int fusion, i
             ps_plan_op o{};
             o.kind = p.kind;
             o.first_rot = p.first_input;
-            o.n_rot = (p.kind == PASS_EXCHANGE && !p.full) ? 0 : p.n_input;
+            o.n_rot = (p.kind == PASS_PERMUTE || (p.kind == PASS_EXCHANGE && !p.full)) ? 0 : p.n_input;
             o.exch_bit = p.full ? -1 : p.ell;
-            o.exch_gx = p.gx;
+            o.exch_gx = p.kind == PASS_PERMUTE ? (uint64_t)p.ell2 : p.gx;
             o.tile_bits = (uint32_t)p.kbits;
             ops[t] = o;
         }

@@ -90,6 +90,7 @@ enum PassKind : int {
     PASS_TILE = PS_K_TILE,
     PASS_COSET = PS_K_COSET,
     PASS_EXCHANGE = PS_K_EXCHANGE,
+    PASS_PERMUTE = PS_K_PERMUTE,  // local transposition of physical bits ell and ell2
 };
 
 constexpr int kMaxTileHigh = 10;  // at most 2^10 gathered chunks per coset tile
@@ -115,6 +116,8 @@ struct Pass {
     int ell = 0;          // local pivot bit
     int keep = 0;         // this rank keeps slots with bit ell == keep
     int full = 0;         // 1: single-rotation full exchange (no free pivot); rot_begin/rot_count valid
+    // PERMUTE
+    int ell2 = 0;
 };
 
 struct Plan {
@@ -125,6 +128,7 @@ struct Plan {
     std::vector<DevTRot> trots;
     std::vector<ps_plan_rot> debug_rots;  // filled when requested (plan dump)
     uint64_t exchanges = 0;
+    std::vector<int> perm_out;  // layout after the plan: physical bit -> logical qubit
 };
 
 struct PlanConfig {
@@ -138,6 +142,8 @@ struct PlanConfig {
     int phase_bits = 3;         // log2 lanes per shared-memory phase (16-B amplitudes: 3, 8-B: 4)
     int max_pass_rots = 1 << 30;
     bool want_debug = false;
+    int layout = 1;             // world > 1: 1 lazy qubit swaps (Belady), 0 runs with swap-back
+    std::vector<int> perm;      // starting layout (physical bit -> logical qubit); empty = canonical
 };
 
 // planner.cpp
@@ -145,6 +151,9 @@ int validate_rotations(int n, const uint64_t* x, const uint64_t* z, const double
                        size_t count, std::string* err);
 void make_plan(const PlanConfig& cfg, const uint64_t* x, const uint64_t* z, const double* angle,
                size_t count, Plan* plan);
+// ops returning layout `perm` to the canonical one (exchanges, then local transpositions);
+// appends to plan (does not clear it) and sets plan->perm_out to the identity
+void make_restore_plan(const PlanConfig& cfg, const std::vector<int>& perm, Plan* plan);
 int popc64(uint64_t v);
 int highest_bit(uint64_t v);
 

@@ -15,9 +15,9 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libps.so")
 
 C128, C64 = 0, 1
-K_STREAM, K_TILE, K_COSET, K_REDUCE, K_INIT, K_EXCHANGE = range(6)
-KERNEL_NAMES = ["stream", "tile", "coset", "reduce", "init", "exchange"]
-OPT_PROFILE, OPT_FUSION, OPT_TILE_BITS, OPT_CHUNK_BYTES, OPT_MAX_PASS_ROTS, OPT_VEC256, OPT_TILE_TMA, OPT_CHUNK_BITS, OPT_TILE_TUNE = range(9)
+K_STREAM, K_TILE, K_COSET, K_REDUCE, K_INIT, K_EXCHANGE, K_PERMUTE = range(7)
+KERNEL_NAMES = ["stream", "tile", "coset", "reduce", "init", "exchange", "permute"]
+OPT_PROFILE, OPT_FUSION, OPT_TILE_BITS, OPT_CHUNK_BYTES, OPT_MAX_PASS_ROTS, OPT_VEC256, OPT_TILE_TMA, OPT_CHUNK_BITS, OPT_TILE_TUNE, OPT_LAYOUT, OPT_TRANSPORT = range(11)
 
 
 class PsError(RuntimeError):
@@ -31,11 +31,11 @@ class Stats(ctypes.Structure):
         ("rotations", ctypes.c_uint64),
         ("passes", ctypes.c_uint64),
         ("exchanges", ctypes.c_uint64),
-        ("launches", ctypes.c_uint64 * 6),
-        ("rotations_by", ctypes.c_uint64 * 6),
-        ("algo_bytes", ctypes.c_double * 6),
+        ("launches", ctypes.c_uint64 * 7),
+        ("rotations_by", ctypes.c_uint64 * 7),
+        ("algo_bytes", ctypes.c_double * 7),
         ("nvlink_bytes", ctypes.c_double),
-        ("kernel_ms", ctypes.c_double * 6),
+        ("kernel_ms", ctypes.c_double * 7),
     ]
 
     def as_dict(self):
@@ -106,7 +106,7 @@ def lib():
         "ps_pauli_encode": [ctypes.c_char_p, vp, vp],
         "ps_pauli_encode_codes": [vp, i32, sz, vp, vp],
         "ps_gate_to_rotations": [ctypes.c_char_p, vp, i32, vp, i32, vp, vp, vp, sz, vp],
-        "ps_plan_describe": [i32, i32, i32, i32, i32, vp, vp, vp, sz, vp, sz, vp, vp, sz, vp],
+        "ps_plan_describe": [i32, i32, i32, i32, i32, i32, vp, vp, vp, sz, vp, sz, vp, vp, sz, vp],
     }
     for name, args in sig.items():
         fn = getattr(L, name)
@@ -182,15 +182,17 @@ def circuit_to_rotations(gates):
     return np.concatenate(xs), np.concatenate(zs), np.concatenate(angs)
 
 
-def plan_describe(n: int, x, z, angles, world: int = 1, rank: int = 0, fusion: int = 2, tile_bits: int = 12):
+def plan_describe(n: int, x, z, angles, world: int = 1, rank: int = 0, fusion: int = 2, tile_bits: int = 12,
+                  layout: int = 1):
     x, z, a = _u64(x), _u64(z), _f64(angles)
     nops, nrots = ctypes.c_size_t(), ctypes.c_size_t()
-    _check("ps_plan_describe", lib().ps_plan_describe(n, world, rank, fusion, tile_bits, _p(x), _p(z), _p(a), len(a),
-                                                      None, 0, ctypes.byref(nops), None, 0, ctypes.byref(nrots)))
+    _check("ps_plan_describe", lib().ps_plan_describe(n, world, rank, fusion, tile_bits, layout, _p(x), _p(z), _p(a),
+                                                      len(a), None, 0, ctypes.byref(nops), None, 0,
+                                                      ctypes.byref(nrots)))
     ops = (PlanOp * max(1, nops.value))()
     rots = (PlanRot * max(1, nrots.value))()
-    _check("ps_plan_describe", lib().ps_plan_describe(n, world, rank, fusion, tile_bits, _p(x), _p(z), _p(a), len(a),
-                                                      ops, nops.value, ctypes.byref(nops), rots, nrots.value,
+    _check("ps_plan_describe", lib().ps_plan_describe(n, world, rank, fusion, tile_bits, layout, _p(x), _p(z), _p(a),
+                                                      len(a), ops, nops.value, ctypes.byref(nops), rots, nrots.value,
                                                       ctypes.byref(nrots)))
     op_list = [dict(kind=o.kind, first_rot=o.first_rot, n_rot=o.n_rot, exch_bit=o.exch_bit, exch_gx=int(o.exch_gx),
                     tile_bits=o.tile_bits) for o in ops[: nops.value]]

@@ -59,19 +59,28 @@ def main():
             codes, ang = layer_with_global(n, 300, n, world)
             x, z = P.pauli_encode_codes(codes)
             want = oracle.apply(n, oracle.random_state(SEED, n), codes, ang) if rank == 0 else None
-            for fusion in (0, 1, 2):
-                for chunk in (4096, 1 << 28):
-                    with P.State(n, "c128", world=world, rank=rank) as st:
-                        st.set_option(ps.OPT_FUSION, fusion)
-                        st.set_option(ps.OPT_TILE_BITS, 6)
-                        st.set_option(ps.OPT_CHUNK_BYTES, chunk)
-                        st.init_random(SEED)
-                        st.apply_rotations(x, z, ang)
-                        got = st.get_amplitudes()
-                        stats = st.stats()
-                    if rank == 0:
-                        check(f"oracle n={n} fusion={fusion} chunk={chunk} exch={stats['exchanges']}",
-                              np.max(np.abs(got - want)), 1e-10)
+            for fusion, chunk, layout, transport in ((0, 4096, 0, 0), (1, 1 << 28, 0, 1), (2, 4096, 0, 0),
+                                                     (2, 1 << 28, 1, 1), (0, 1 << 28, 1, 0), (2, 4096, 1, 1)):
+                with P.State(n, "c128", world=world, rank=rank) as st:
+                    st.set_option(ps.OPT_FUSION, fusion)
+                    st.set_option(ps.OPT_TILE_BITS, 6)
+                    st.set_option(ps.OPT_CHUNK_BYTES, chunk)
+                    st.set_option(ps.OPT_LAYOUT, layout)
+                    st.set_option(ps.OPT_TRANSPORT, transport)
+                    st.init_random(SEED)
+                    # two calls: the lazy layout persists across them; the norm needs no restore
+                    h = len(ang) // 2
+                    st.apply_rotations(x[:h], z[:h], ang[:h])
+                    nrm_mid = st.norm()
+                    st.apply_rotations(x[h:], z[h:], ang[h:])
+                    got = st.get_amplitudes()
+                    stats = st.stats()
+                if rank == 0:
+                    tag = f"n={n} fusion={fusion} chunk={chunk} layout={layout} transport={transport}"
+                    check(f"oracle {tag} exch={stats['exchanges']} perm={stats['launches']['permute']}",
+                          np.max(np.abs(got - want)), 1e-10)
+                    check(f"mid-call norm {tag}", abs(nrm_mid - oracle.norm(n, oracle.random_state(SEED, n))) /
+                          oracle.norm(n, oracle.random_state(SEED, n)), 1e-12)
         # (b) full-exchange fallback: local X-part covering every local bit
         n = world.bit_length() - 1 + 3
         words = ["X" * n, "Y" + "X" * (n - 2) + "Z", "Z" * n, "XY" * (n // 2) + "X" * (n % 2), "I" + "X" * (n - 1)]

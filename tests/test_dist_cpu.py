@@ -34,6 +34,7 @@ def _worker(rank, world, port, q):
         x, z = P.pauli_encode_codes(codes)
         ops, rots = P.plan_describe(n, x, z, ang, world=world, rank=rank, fusion=2, tile_bits=8)
         struct = [(o["kind"], o["exch_bit"], o["exch_gx"], o["first_rot"], o["n_rot"]) for o in ops]
+        assert any(o["kind"] == 5 for o in ops)
         xs = [(r["x"], r["z"], r["y"]) for r in rots]
         signs = [r["sign"] for r in rots]
         allst = [None] * world

@@ -168,10 +168,10 @@ def _apply_phys(a: np.ndarray, r: dict):
     return c * a + 1j * s * w * a[j]
 
 
-def _run_model(n, world, x, z, ang, fusion=2, tile_bits=3):
+def _run_model(n, world, x, z, ang, fusion=2, tile_bits=3, layout=1):
     m = world.bit_length() - 1
     nl = n - m
-    plans = [P.plan_describe(n, x, z, ang, world=world, rank=r, fusion=fusion, tile_bits=tile_bits)
+    plans = [P.plan_describe(n, x, z, ang, world=world, rank=r, fusion=fusion, tile_bits=tile_bits, layout=layout)
              for r in range(world)]
     kinds = [[(o["kind"], o["exch_bit"], o["exch_gx"], o["n_rot"]) for o in ops] for ops, _ in plans]
     assert all(k == kinds[0] for k in kinds), "plans must be SPMD-identical in structure"
@@ -183,7 +183,12 @@ def _execute(n, world, psi, plans, nl):
     cursors = [0] * world
     ops0 = plans[0][0]
     for t, op in enumerate(ops0):
-        if op["kind"] == ps.K_EXCHANGE and op["exch_bit"] >= 0:
+        if op["kind"] == ps.K_PERMUTE:
+            a, b = op["exch_bit"], op["exch_gx"]
+            idx = np.arange(1 << nl)
+            swp = idx ^ ((((idx >> a) ^ (idx >> b)) & 1) * ((1 << a) | (1 << b)))
+            local = [v[swp] for v in local]
+        elif op["kind"] == ps.K_EXCHANGE and op["exch_bit"] >= 0:
             ell, gx = op["exch_bit"], op["exch_gx"]
             g = (gx & -gx).bit_length() - 1
             new = [v.copy() for v in local]
@@ -219,18 +224,32 @@ def _execute(n, world, psi, plans, nl):
 
 @pytest.mark.parametrize("world", [1, 2, 4, 8])
 @pytest.mark.parametrize("kind", ["R4", "R10", "S8"])
-def test_planner_model_matches_oracle(world, kind):
-    n = 6
-    codes, ang = workloads.random_layer(n, 40, seed=world, kind=kind)
+@pytest.mark.parametrize("layout", [0, 1])
+def test_planner_model_matches_oracle(world, kind, layout):
+    n = 7
+    codes, ang = workloads.random_layer(n, 60, seed=world, kind=kind)
     x, z = P.pauli_encode_codes(codes)
     psi = oracle.random_state(3, n)
     want = oracle.apply(n, psi, codes, ang)
-    plans, nl = _run_model(n, world, x, z, ang)
+    plans, nl = _run_model(n, world, x, z, ang, layout=layout)
     got = _execute(n, world, psi, plans, nl)
     assert np.max(np.abs(got - want)) <= 1e-12
 
 
-def test_planner_full_exchange_fallback():
+def test_lazy_layout_needs_fewer_exchanges():
+    """Belady swaps keep a swapped-in qubit until its slot is needed."""
+    n, world = 16, 2
+    codes, ang = workloads.random_layer(n, 400, seed=9, kind="R10")
+    x, z = P.pauli_encode_codes(codes)
+    ex = {}
+    for layout in (0, 1):
+        ops, _ = P.plan_describe(n, x, z, ang, world=world, rank=0, layout=layout, tile_bits=8)
+        ex[layout] = sum(o["kind"] == ps.K_EXCHANGE for o in ops)
+    assert ex[1] < 0.75 * ex[0]
+
+
+@pytest.mark.parametrize("layout", [0, 1])
+def test_planner_full_exchange_fallback(layout):
     """A global-X string whose local X-part covers every local bit has no free pivot: the plan
     uses the single-rotation full exchange and still matches the oracle."""
     n, world = 4, 2
@@ -239,7 +258,7 @@ def test_planner_full_exchange_fallback():
     x, z = P.pauli_encode_codes(codes)
     ang = np.array([0.3, -1.2, 0.7, 2.0, -0.5])
     psi = oracle.random_state(5, n)
-    plans, nl = _run_model(n, world, x, z, ang)
+    plans, nl = _run_model(n, world, x, z, ang, layout=layout)
     assert any(o["kind"] == ps.K_EXCHANGE and o["exch_bit"] < 0 for o in plans[0][0])
     got = _execute(n, world, psi, plans, nl)
     assert np.max(np.abs(got - oracle.apply(n, psi, codes, ang))) <= 1e-12
@@ -256,12 +275,14 @@ def test_exchange_economy():
     codes[:, 6] = 1  # X on global qubit 6 for every rotation
     codes[:, 7] = rng.integers(0, 2, size=L) * 3  # I/Z on global qubit 7
     x, z = P.pauli_encode_codes(codes)
-    ops, _ = P.plan_describe(n, x, z, rng.uniform(-1, 1, L), world=world, rank=1)
-    assert sum(o["kind"] == ps.K_EXCHANGE for o in ops) == 2
+    for layout in (0, 1):  # one exchange in, one back (lazy layout: back at the restore)
+        ops, _ = P.plan_describe(n, x, z, rng.uniform(-1, 1, L), world=world, rank=1, layout=layout)
+        assert sum(o["kind"] == ps.K_EXCHANGE for o in ops) == 2
     codes[:, 6] = 3  # now Z only on the global qubits
     x, z = P.pauli_encode_codes(codes)
-    ops, _ = P.plan_describe(n, x, z, rng.uniform(-1, 1, L), world=world, rank=1)
-    assert sum(o["kind"] == ps.K_EXCHANGE for o in ops) == 0
+    for layout in (0, 1):
+        ops, _ = P.plan_describe(n, x, z, rng.uniform(-1, 1, L), world=world, rank=1, layout=layout)
+        assert sum(o["kind"] == ps.K_EXCHANGE for o in ops) == 0
 
 
 def test_fusion_levels_cover_every_rotation_in_order():
