@@ -6,7 +6,7 @@ resident in HBM; value = rotations / second (whole job).  N > 1 GPUs (torchrun):
 30-qubit state sharded over N ranks by its top qubits (strong scaling), exchanges over NCCL.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                  [--n 30] [--layer 1000] [--kind R10] [--dtype c128] [--fusion 2]
+                  [--qubits 30] [--layer 1000] [--kind R10] [--dtype c128] [--fusion 2]
 
 --impl reference times the CPU oracle (the slow from-definition program) on the host cores,
 on a bounded sample of the same workload (scaled to the 30-qubit metric), and prints the same
@@ -41,7 +41,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--n", type=int, default=30)
+    ap.add_argument("--qubits", dest="n", type=int, default=30)
     ap.add_argument("--layer", type=int, default=1000)
     ap.add_argument("--kind", default="R10")
     ap.add_argument("--dtype", default="c128", choices=["c128", "c64"])
