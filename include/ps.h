@@ -94,8 +94,10 @@ enum {
                                  3 = TMA-bulk-prefetched double buffer (A/B) */
     PS_OPT_CHUNK_BITS = 7,    /* min log2 contiguous amplitudes per gathered chunk (0 = default:
                                  4 for C128, 5 for C64, i.e. 256 B) */
-    PS_OPT_TILE_TUNE = 8,     /* register-direct tile kernel tuning: bit 0 = L2 prefetch of the next
-                                 tile, bits 4.. = persistent-grid multiplier (0 = default) */
+    PS_OPT_TILE_TUNE = 8,     /* register-direct tile kernel tuning bits: 0 = TMA bulk L2 prefetch of
+                                 the next tile, 1-3 = register cap for 5/6/8 CTAs per SM, 4-7 =
+                                 persistent-grid multiplier, 8 = per-thread L2 prefetch, 9 = L2::256B
+                                 sector promotion on the gathered loads (default 512 = bit 9) */
     PS_OPT_LAYOUT = 9,        /* world > 1: 1 = lazy qubit-swap layout kept across calls, swaps chosen
                                  by furthest next use (default); 0 = one half-vector exchange per run
                                  sharing the upper X-part, swapped back at once (Eq. (1) economy) */

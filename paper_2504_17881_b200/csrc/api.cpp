@@ -90,7 +90,7 @@ struct ps_state {
     bool p2p = false;
     int layout = 1, transport = 1;
     // options
-    int profile = 0, fusion = 2, tile_bits = 11, vec256 = 1, max_pass_rots = 1 << 30, tile_tma = 2, chunk_bits = 0, tile_tune = 0;
+    int profile = 0, fusion = 2, tile_bits = 11, vec256 = 1, max_pass_rots = 1 << 30, tile_tma = 2, chunk_bits = 0, tile_tune = 512;
     ps_stats stats{};
     std::vector<PendingTiming> pending;
     std::vector<cudaEvent_t> event_pool;

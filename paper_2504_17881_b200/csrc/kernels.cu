@@ -445,6 +445,17 @@ __device__ __forceinline__ uint32_t sub_local(const SubHdr& h, int d) {
     return l;
 }
 
+__device__ __forceinline__ double2 ld_l2_256(const double2* p) {
+    double2 v;
+    asm volatile("ld.global.L1::no_allocate.L2::256B.v2.f64 {%0,%1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ float2 ld_l2_256(const float2* p) {
+    float2 v;
+    asm volatile("ld.global.L1::no_allocate.L2::256B.v2.f32 {%0,%1}, [%2];" : "=f"(v.x), "=f"(v.y) : "l"(p));
+    return v;
+}
+
 template <typename T>
 struct SmemAmp;
 template <>
@@ -546,8 +557,13 @@ __global__ void __launch_bounds__(MAXT, MINB)
                     gi[d] = (i0 ^ soff[l >> cbits]) | (l & cmask);
                 }
                 V2 v[kSubAmps];
+                if (l2_prefetch & 4) {
 #pragma unroll
-                for (int d = 0; d < kSubAmps; ++d) v[d] = __ldcs(&g[gi[d]]);
+                    for (int d = 0; d < kSubAmps; ++d) v[d] = ld_l2_256(&g[gi[d]]);
+                } else {
+#pragma unroll
+                    for (int d = 0; d < kSubAmps; ++d) v[d] = __ldcs(&g[gi[d]]);
+                }
 #pragma unroll
                 for (int d = 0; d < kSubAmps; ++d) {
                     vr[d] = v[d].x;
@@ -561,7 +577,17 @@ __global__ void __launch_bounds__(MAXT, MINB)
                     vi[d] = v.y;
                 }
             }
-            if (s == 0 && l2_prefetch && tau + gridDim.x < ntiles) {
+            if (s == 0 && (l2_prefetch & 2) && tau + gridDim.x < ntiles && (tid & 7) == 0) {
+                // per-thread L2 prefetch of the lines of this thread's next-tile coset (one lane of
+                // 8 covers a 128-B line of 16-B amplitudes)
+                const uint64_t i1 = deposit(tau + gridDim.x, runs);
+#pragma unroll
+                for (int d = 0; d < kSubAmps; ++d) {
+                    const uint32_t l = sub_local(h, d);
+                    asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(&g[(i1 ^ soff[l >> cbits]) | (l & cmask)]));
+                }
+            }
+            if (s == 0 && (l2_prefetch & 1) && tau + gridDim.x < ntiles) {
                 // this tile's loads have landed (sub_apply consumes them): warm L2 with the CTA's next
                 // tile while the rest of this one is computed and stored
                 const uint64_t i1 = deposit(tau + gridDim.x, runs);
@@ -1192,7 +1218,8 @@ cudaError_t launch_stream(int dtype, void* a, int nl, const Pass& p, const DevRo
 cudaError_t launch_tile(int dtype, void* a, int nl, const Pass& p, const DevSub* d_subs, const DevTRot* d_trots,
                         const uint64_t* d_offs, int use_tma, int tune, cudaStream_t s) {
     // tune: bit 0 = L2 prefetch of the next tile (register-direct kernel); bits 4.. = grid multiplier
-    const int l2p = tune & 1;
+    // bit 0: TMA bulk L2 prefetch; bit 8: per-thread L2 prefetch; bit 9: L2::256B load hint
+    const int l2p = (tune & 1) | ((tune >> 7) & 2) | ((tune >> 7) & 4);
     const int occ_sel = (tune >> 1) & 7;
     const int gm = (tune >> 4) ? (tune >> 4) : 4;
     if (use_tma == 1) {
