@@ -43,7 +43,10 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--qubits", dest="n", type=int, default=30)
     ap.add_argument("--layer", type=int, default=1000)
-    ap.add_argument("--kind", default="R10")
+    ap.add_argument("--kind", default="R10", help="R10 R4 D S8 LOW (random layers), JW (Trotter step), QAOA, GATES")
+    ap.add_argument("--terms", type=int, default=92968, help="JW: Hamiltonian terms (Table 3: 92,968 at 32q)")
+    ap.add_argument("--lam", type=float, default=27.0, help="JW: lambda = sum |h| (Table 3)")
+    ap.add_argument("--delta", type=float, default=0.5, help="JW: Trotter step size")
     ap.add_argument("--dtype", default="c128", choices=["c128", "c64"])
     ap.add_argument("--fusion", type=int, default=2)
     ap.add_argument("--tile-bits", type=int, default=0)
@@ -66,15 +69,39 @@ def dist_env():
 
 
 def workload_name(args):
-    return (f"{args.n}q {'fp64' if args.dtype == 'c128' else 'fp32'} random Pauli-rotation layer "
+    prec = "fp64" if args.dtype == "c128" else "fp32"
+    if args.kind == "JW":
+        return (f"{args.n}q {prec} first-order Trotter step of a JW-shaped molecular Hamiltonian "
+                f"({args.terms} terms, lambda {args.lam}, delta {args.delta}, x-major order)")
+    if args.kind == "QAOA":
+        return f"{args.n}q {prec} QAOA MaxCut, random 3-regular graph, p = {args.layer} layers"
+    if args.kind == "GATES":
+        return f"{args.n}q {prec} random gate brickwork of depth {args.layer}, converted to rotations"
+    return (f"{args.n}q {prec} random Pauli-rotation layer "
             f"({args.kind}: weight 1-10, phi~U[-pi,pi)), {args.layer} rotations/step")
 
 
-def layers(args, count):
+def layers(args, count, world=1):
+    """(codes or None, x, z, angles) per step; structured workloads repeat one step."""
+    import paper_2504_17881_b200 as P
     out = []
+    if args.kind == "JW":
+        m = world.bit_length() - 1
+        codes, coeffs = workloads.jw_hamiltonian(args.n, args.terms, args.lam, seed=0, n_local=args.n - m)
+        x, z = P.pauli_encode_codes(codes)
+        ang = workloads.trotter1_angles(coeffs, args.delta)
+        return [(x, z, ang)] * count
+    if args.kind == "QAOA":
+        codes, ang = workloads.qaoa_layers(args.n, args.layer, seed=0)
+        x, z = P.pauli_encode_codes(codes)
+        return [(x, z, ang)] * count
+    if args.kind == "GATES":
+        x, z, ang = P.circuit_to_rotations(workloads.gate_circuit(args.n, args.layer, seed=0))
+        return [(x, z, ang)] * count
     for s in range(count):
         codes, ang = workloads.random_layer(args.n, args.layer, seed=1000 + s, kind=args.kind)
-        out.append((codes, ang))
+        x, z = P.pauli_encode_codes(codes)
+        out.append((x, z, ang))
     return out
 
 
@@ -239,8 +266,8 @@ def run_ours(args):
     st.set_option(ps.OPT_LAYOUT, args.layout)
     st.set_option(ps.OPT_TRANSPORT, args.transport)
     st.set_option(ps.OPT_PROFILE, 1)
-    lay = layers(args, args.warmup + args.steps)
-    enc = [P.pauli_encode_codes(c) + (a,) for c, a in lay]
+    enc = layers(args, args.warmup + args.steps, world)
+    rot_per_step = len(enc[0][2])
     st.init_random(workloads.BASE_SEED)
 
     stream = st.torch_stream  # the stream libps enqueues on
@@ -270,7 +297,7 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     ms_per_step = ms / args.steps
-    value = args.layer / (ms_per_step / 1e3)
+    value = rot_per_step / (ms_per_step / 1e3)
     amp_bytes = 16 if args.dtype == "c128" else 8
     local_state = amp_bytes << (args.n - (world.bit_length() - 1))
     hbm_alg = sum(stats["algo_bytes"][k] for k in ("stream", "tile", "coset")) / (ms / 1e3) / 1e9 * world
@@ -294,7 +321,7 @@ def run_ours(args):
         host = torch.empty(local_state // (amp_bytes // 2), dtype=tdt, pin_memory=True)
         st.init_random(workloads.BASE_SEED)
         host.copy_(st._tensor)  # the seeded initial state, staged in pinned host memory (untimed)
-        h2d = local_state + 24 * args.layer
+        h2d = local_state + 24 * rot_per_step
         e_steps = min(args.steps, 2)
         x, z, a = enc[0]
         st.set_state_ptr(host.data_ptr(), 1 << (args.n - (world.bit_length() - 1)), first=rank << st.n_local)
@@ -313,7 +340,7 @@ def run_ours(args):
             t = torch.tensor([el], device="cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             el = float(t.item())
-        e2e = {"value": args.layer * e_steps / el, "unit": UNIT, "h2d_bytes_per_step": h2d * world,
+        e2e = {"value": rot_per_step * e_steps / el, "unit": UNIT, "h2d_bytes_per_step": h2d * world,
                "d2h_bytes_per_step": 8, "steps": e_steps,
                "path": "ps_set_state(pinned host) + ps_apply_rotations(host arrays) + ps_norm -> host"}
         del host
@@ -325,7 +352,7 @@ def run_ours(args):
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64" if args.dtype == "c128" else "f32",
             "data": "synthetic",
-            "config": {"workload": workload_name(args), "n_qubits": args.n, "rotations_per_step": args.layer,
+            "config": {"workload": workload_name(args), "n_qubits": args.n, "rotations_per_step": rot_per_step,
                        "fusion": args.fusion, "tile_mode": args.tile_mode, "tile_bits": args.tile_bits or 11,
                        "layout": args.layout, "transport": args.transport,
                        "parallelism": f"state sharded over {world} GPU(s) by top qubits",

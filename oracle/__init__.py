@@ -172,6 +172,12 @@ def random_amplitudes(seed: int, first: int, count: int) -> np.ndarray:
     return out
 
 
+def random_amplitudes_at(seed: int, indices) -> np.ndarray:
+    """Generator values at arbitrary (e.g. coset) indices."""
+    idx = np.asarray(indices, dtype=np.uint64)
+    return np.array([random_amplitudes(seed, int(i), 1)[0] for i in idx], dtype=np.complex128)
+
+
 def random_state(seed: int, n: int) -> np.ndarray:
     return random_amplitudes(seed, 0, 1 << n)
 

@@ -597,7 +597,7 @@ __global__ void __launch_bounds__(MAXT, MINB)
                                  : "memory");
             }
             sub_apply<T>(vr, vi, trots, h.rb, h.nr, h.r, i0);
-            sub_scale<T>(vr, vi, (T)h.F);
+            if (h.F != 1.0) sub_scale<T>(vr, vi, (T)h.F);
             if (s == nsub - 1) {
 #pragma unroll
                 for (int d = 0; d < kSubAmps; ++d) {
@@ -727,7 +727,7 @@ __global__ void __launch_bounds__(kCosetThreads, 2)
                 vi[d] = v.y;
             }
             sub_apply<T>(vr, vi, trots, h.rb, h.nr, h.r, i0);
-            sub_scale<T>(vr, vi, (T)h.F);
+            if (h.F != 1.0) sub_scale<T>(vr, vi, (T)h.F);
             if (s == nsub - 1) {
 #pragma unroll
                 for (int d = 0; d < kSubAmps; ++d) {
@@ -854,7 +854,7 @@ __global__ void __launch_bounds__(kTileMaxThreads, 1)
                 vi[d] = v.y;
             }
             sub_apply<T>(vr, vi, trots, h.rb, h.nr, h.r, i0);
-            sub_scale<T>(vr, vi, (T)h.F);
+            if (h.F != 1.0) sub_scale<T>(vr, vi, (T)h.F);
 #pragma unroll
             for (int d = 0; d < kSubAmps; ++d) {
                 V2 v;
@@ -1221,7 +1221,7 @@ cudaError_t launch_tile(int dtype, void* a, int nl, const Pass& p, const DevSub*
     // bit 0: TMA bulk L2 prefetch; bit 8: per-thread L2 prefetch; bit 9: L2::256B load hint
     const int l2p = (tune & 1) | ((tune >> 7) & 2) | ((tune >> 7) & 4);
     const int occ_sel = (tune >> 1) & 7;
-    const int gm = (tune >> 4) ? (tune >> 4) : 4;
+    const int gm = ((tune >> 4) & 15) ? ((tune >> 4) & 15) : 4;
     if (use_tma == 1) {
         if (dtype == PS_C128) return launch_tile_t<double>((double*)a, nl, p, d_subs, d_trots, d_offs, s);
         return launch_tile_t<float>((float*)a, nl, p, d_subs, d_trots, d_offs, s);

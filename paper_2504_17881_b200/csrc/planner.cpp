@@ -228,6 +228,20 @@ static void make_subgroups(const std::vector<LocalRot>& lr, int k, int phase_bit
         b = e;
     }
     p->sub_count = (int)plan->subs.size() - p->sub_begin;
+    // defer the scale factors across sub-groups (the amplitudes stay linear in them) while the
+    // accumulated factor stays within [2^-40, 2^40]; F = 1 means "no scaling pass here"
+    double acc = 1.0;
+    for (int t = p->sub_begin; t < (int)plan->subs.size(); ++t) {
+        acc *= plan->subs[t].F;
+        const bool last = t + 1 == (int)plan->subs.size();
+        const double next = last ? 1.0 : plan->subs[t + 1].F;
+        if (last || std::fabs(std::log2(std::fabs(acc * next))) > 40.0) {
+            plan->subs[t].F = acc;
+            acc = 1.0;
+        } else {
+            plan->subs[t].F = 1.0;
+        }
+    }
 }
 
 static void emit_tile(const std::vector<PhysRot>& seg, size_t b, size_t e, const PlanConfig& cfg,

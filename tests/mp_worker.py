@@ -25,6 +25,10 @@ from paper_2504_17881_b200 import ps  # noqa: E402
 SEED = 250417881
 
 
+class _SkipSmall(Exception):
+    pass
+
+
 def layer_with_global(n, count, seed, world):
     """R10 layer plus runs of rotations with X on the top (global) qubits and Z-only global terms."""
     codes, ang = workloads.random_layer(n, count, seed=seed, kind="R10")
@@ -53,9 +57,10 @@ def main():
         ok &= good
         report["checks"].append({"name": name, "err": float(err), "tol": tol, "ok": good})
 
+    only_large = os.environ.get("PS_MP_ONLY_LARGE") == "1"
     try:
         # (a) small n against the oracle, all fusion levels, small exchange chunks
-        for n in (6, 10, 13):
+        for n in (() if only_large else (6, 10, 13)):
             codes, ang = layer_with_global(n, 300, n, world)
             x, z = P.pauli_encode_codes(codes)
             want = oracle.apply(n, oracle.random_state(SEED, n), codes, ang) if rank == 0 else None
@@ -81,6 +86,8 @@ def main():
                           np.max(np.abs(got - want)), 1e-10)
                     check(f"mid-call norm {tag}", abs(nrm_mid - oracle.norm(n, oracle.random_state(SEED, n))) /
                           oracle.norm(n, oracle.random_state(SEED, n)), 1e-12)
+        if only_large:
+            raise _SkipSmall()
         # (b) full-exchange fallback: local X-part covering every local bit
         n = world.bit_length() - 1 + 3
         words = ["X" * n, "Y" + "X" * (n - 2) + "Z", "Z" * n, "XY" * (n // 2) + "X" * (n % 2), "I" + "X" * (n - 1)]
@@ -140,6 +147,45 @@ def main():
                 one.apply_rotations(x, z, ang)
                 ref = one.get_amplitudes()
             check("G-invariance n=24 vs 1 GPU", np.max(np.abs(got - ref)), 1e-12)
+    except _SkipSmall:
+        pass
+    except Exception:  # noqa: BLE001
+        ok = False
+        report["error"] = traceback.format_exc()
+    try:
+        # (g) large n (PS_MP_LARGE=n): JW-shaped Trotter step with X-support on 16 qubits (incl. the
+        # global ones) and Z letters everywhere, checked on whole cosets by the coset oracle
+        big = int(os.environ.get("PS_MP_LARGE", "0"))
+        if big:
+            rng = np.random.default_rng(big)
+            m = world.bit_length() - 1
+            pos = sorted(set([big - 1 - j for j in range(m)]) | set(int(v) for v in rng.choice(big - m, 16 - m, replace=False)))
+            hc, hco = workloads.jw_embedded(big, pos, 2000, 20.0, seed=2, n_local=big - m)
+            ang = workloads.trotter1_angles(hco, 0.5)
+            x, z = P.pauli_encode_codes(hc)
+            import time
+            with P.State(big, "c128", world=world, rank=rank) as st:
+                st.init_random(SEED)
+                st.synchronize()
+                t0 = time.perf_counter()
+                st.apply_rotations(x, z, ang)
+                st.synchronize()
+                el = time.perf_counter() - t0
+                stats = st.stats()
+                nrm = st.norm()
+                for trial in range(2):
+                    i0 = int(rng.integers(0, 1 << big)) if trial else 0
+                    mem = oracle.coset_members(big, i0, x)
+                    sel = np.sort(rng.choice(len(mem), 200, replace=False))
+                    got = np.array([st.get_amplitudes(int(mem[k]), 1)[0] for k in sel])
+                    if rank == 0:
+                        init = oracle.random_amplitudes_at(SEED, mem)
+                        want = oracle.apply_coset(big, mem, init, hc, ang)
+                        check(f"coset oracle n={big} ({len(mem)} members, {len(ang)} terms, {stats['exchanges']} exchanges, "
+                              f"{el:.1f} s)", np.max(np.abs(got - want[sel])), 1e-10)
+                if rank == 0:
+                    n0 = float(np.sum(np.abs(oracle.random_amplitudes(SEED, 0, 1 << 20)) ** 2)) * 2 ** (big - 20)
+                    report["large_norm_ratio"] = nrm / n0
     except Exception:  # noqa: BLE001
         ok = False
         report["error"] = traceback.format_exc()

@@ -113,8 +113,11 @@ def jw_hamiltonian(n: int, n_terms: int, lam: float, seed: int = 0, n_local: int
     if base > n_terms:
         raise ValueError("n_terms below the one-body families")
     remaining = n_terms - base
-    n_hopz = remaining // 4
+    same_spin_pairs = sum(1 for p in range(n) for q in range(p + 2, n, 2))
+    n_hopz = min(remaining // 4, same_spin_pairs * (n - 2) * 2)  # all (p, q, r, letter) choices
     n_quad = remaining - n_hopz
+    if n_quad > 8 * (n * (n - 1) * (n - 2) * (n - 3) // 24):
+        raise ValueError("n_terms exceeds the JW-shaped families")
     # hopping x Z_r
     hz = set()
     while len(hz) < n_hopz:
@@ -169,6 +172,22 @@ def order_x_major(codes: np.ndarray, coeffs: np.ndarray, n_local: int):
     yz = _pack_bits(((codes == Y) | (codes == Z)).astype(np.uint8))
     order = np.lexsort((yz, allnd, hi))
     return codes[order], coeffs[order]
+
+
+def jw_embedded(n_total: int, positions, n_terms: int, lam: float, seed: int = 0, extra_z: float = 0.3,
+                n_local: int | None = None):
+    """A JW-shaped Hamiltonian on len(positions) qubits placed at `positions` of an n_total-qubit
+    register, every term additionally carrying random Z letters on the other qubits (probability
+    extra_z each).  The X/Y support stays inside `positions`, so the X-span has rank <= len(positions)
+    and the coset oracle can check any n_total (SURVEY T5 parity variant)."""
+    positions = list(positions)
+    small, coeffs = jw_hamiltonian(len(positions), n_terms, lam, seed=seed, n_local=len(positions))
+    rng = _rng(5_000_000 + n_total * 100 + seed)
+    codes = np.zeros((len(small), n_total), np.uint8)
+    others = np.array([q for q in range(n_total) if q not in set(positions)], dtype=np.int64)
+    codes[:, others] = (rng.random((len(small), len(others))) < extra_z).astype(np.uint8) * Z
+    codes[:, positions] = small
+    return order_x_major(codes, coeffs, n_local if n_local is not None else n_total)
 
 
 def trotter1_angles(coeffs: np.ndarray, delta: float) -> np.ndarray:
