@@ -178,27 +178,70 @@ static void make_subgroups(const std::vector<LocalRot>& lr, int k, int phase_bit
             }
             logF += lf;
         }
-        // pad to kSubDim dimensions with the highest free unit vectors
-        for (int q = k - 1; q >= 0 && S.dim() < kSubDim; --q) {
-            if ((S.pivots >> q) & 1) continue;
-            const uint64_t r = S.reduce(1ull << q);
-            if (r) S.add(r);
+        // basis = the sub-group's own first independent xor masks in order (so most rotations get
+        // a unit dx and only a few unrolled pair patterns are hot in the instruction cache),
+        // padded to kSubDim dimensions with the highest free unit vectors
+        std::vector<uint64_t> u;
+        {
+            Basis T;
+            for (size_t t = b; t < e && (int)u.size() < kSubDim; ++t) {
+                const uint64_t r = T.reduce(lr[t].x);
+                if (r) {
+                    T.add(r);
+                    u.push_back(lr[t].x);
+                }
+            }
+            for (int q = k - 1; q >= 0 && (int)u.size() < kSubDim; --q) {
+                const uint64_t r = T.reduce(1ull << q);
+                if (r) {
+                    T.add(r);
+                    u.push_back(1ull << q);
+                }
+            }
+            S = T;
         }
-        std::vector<uint64_t> u = S.v;
-        std::sort(u.begin(), u.end(), [](uint64_t a, uint64_t c) { return highest_bit(a) < highest_bit(c); });
         DevSub sub{};
         for (int t = 0; t < kSubDim; ++t) sub.u[t] = (uint32_t)u[t];
         choose_columns(S, k, phase_bits, sub.col);
+        // coordinates of a mask in the basis u (u is independent; solve by elimination)
+        auto coords = [&](uint64_t v) -> uint32_t {
+            uint64_t rows[kSubDim];
+            uint32_t tags[kSubDim];
+            for (int q = 0; q < kSubDim; ++q) {
+                rows[q] = u[q];
+                tags[q] = 1u << q;
+            }
+            // Gaussian elimination on (rows | tags), pivot = highest bit
+            for (int q = 0; q < kSubDim; ++q) {
+                int best = q;
+                for (int t = q; t < kSubDim; ++t)
+                    if (highest_bit(rows[t]) > highest_bit(rows[best])) best = t;
+                std::swap(rows[q], rows[best]);
+                std::swap(tags[q], tags[best]);
+                const int pq = highest_bit(rows[q]);
+                for (int t = 0; t < kSubDim; ++t)
+                    if (t != q && ((rows[t] >> pq) & 1)) {
+                        rows[t] ^= rows[q];
+                        tags[t] ^= tags[q];
+                    }
+            }
+            uint32_t c = 0;
+            for (int q = 0; q < kSubDim; ++q)
+                if ((v >> highest_bit(rows[q])) & 1) {
+                    v ^= rows[q];
+                    c ^= tags[q];
+                }
+            return v == 0 ? c : 0xffffffffu;
+        };
         sub.rot_begin = (int)plan->trots.size();
         sub.nrot = (int)(e - b);
         double F = 1.0;
         for (size_t t = b; t < e; ++t) {
             const LocalRot& L = lr[t];
-            uint32_t dx = 0, dz = 0;
-            for (int q = 0; q < kSubDim; ++q) {
-                if ((L.x >> highest_bit(u[q])) & 1) dx |= 1u << q;
+            const uint32_t dx = coords(L.x);
+            uint32_t dz = 0;
+            for (int q = 0; q < kSubDim; ++q)
                 if (parity64(L.z & u[q])) dz |= 1u << q;
-            }
             uint32_t M = 0;
             for (int d = 0; d < kSubAmps; ++d)
                 if (parity64((uint64_t)(dz & (uint32_t)d))) M |= 1u << d;
