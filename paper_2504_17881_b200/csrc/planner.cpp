@@ -169,7 +169,7 @@ static void make_subgroups(const std::vector<LocalRot>& lr, int k, int phase_bit
         double logF = 0.0;
         for (; e < lr.size(); ++e) {
             const double cc = std::fabs(std::cos(lr[e].phi)), ss = std::fabs(std::sin(lr[e].phi));
-            const double lf = std::log2(std::max(cc, ss));
+            const double lf = std::log2(cc >= std::ldexp(ss, -10) ? cc : ss);  // the factor actually deferred
             if (e > b && logF + lf < -20.0) break;
             const uint64_t r = S.reduce(lr[e].x);
             if (r) {
@@ -255,7 +255,9 @@ static void make_subgroups(const std::vector<LocalRot>& lr, int k, int phase_bit
             tr.M = M;
             tr.zr = (uint32_t)L.z;
             tr.zt = L.zt;
-            if (std::fabs(c) >= std::fabs(s0)) {
+            // CFORM (one sign flip per pair) unless cos is tiny; |tan| <= 1024 keeps a + t b accurate
+            // and SFORM keeps phi = pi/2 exact (R8)
+            if (std::fabs(c) >= std::ldexp(std::fabs(s0), -10)) {
                 tr.mode = (uint32_t)real;
                 tr.t = ph * (s0 / c);
                 F *= c;
@@ -630,8 +632,43 @@ static void plan_lazy(const PlanConfig& cfg, const uint64_t* x, const uint64_t* 
     plan->perm_out = perm;
 }
 
+static void make_plan_core(const PlanConfig& cfg, const uint64_t* x, const uint64_t* z, const double* angle,
+                           size_t count, Plan* plan);
+
+// Identity-string rotations (x = z = 0: global phases e^{i phi}, e.g. the converter's gate phases,
+// R5) commute with every rotation, so they are summed into one global-phase rotation applied
+// last; everything else keeps its order.
 void make_plan(const PlanConfig& cfg, const uint64_t* x, const uint64_t* z, const double* angle,
                size_t count, Plan* plan) {
+    size_t nid = 0;
+    for (size_t l = 0; l < count; ++l) nid += (x[l] == 0 && z[l] == 0);
+    if (nid < 2) {
+        make_plan_core(cfg, x, z, angle, count, plan);
+        return;
+    }
+    std::vector<uint64_t> xs, zs;
+    std::vector<double> as;
+    xs.reserve(count - nid + 1);
+    zs.reserve(count - nid + 1);
+    as.reserve(count - nid + 1);
+    double phase = 0.0;
+    for (size_t l = 0; l < count; ++l) {
+        if (x[l] == 0 && z[l] == 0) {
+            phase += angle[l];
+            continue;
+        }
+        xs.push_back(x[l]);
+        zs.push_back(z[l]);
+        as.push_back(angle[l]);
+    }
+    xs.push_back(0);
+    zs.push_back(0);
+    as.push_back(phase);
+    make_plan_core(cfg, xs.data(), zs.data(), as.data(), xs.size(), plan);
+}
+
+static void make_plan_core(const PlanConfig& cfg, const uint64_t* x, const uint64_t* z, const double* angle,
+                           size_t count, Plan* plan) {
     clear_plan(plan);
     if (cfg.world > 1 && cfg.layout == 1) {
         plan_lazy(cfg, x, z, angle, count, plan);

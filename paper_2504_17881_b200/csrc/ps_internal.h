@@ -43,10 +43,11 @@ static_assert(sizeof(DevRot) == 48, "DevRot layout");
 // bits b of d, in registers while the sub-group's rotations are applied.
 //
 // Deferred scaling: each rotation is applied as f * (self_coef * a_self + cross_coef * a_other)
-// with the uniform factor f = cos(phi) when |cos| >= |sin| (self_coef = 1, cross_coef = +-t,
-// t = sin/cos) and f = sign*sin(phi) otherwise (self_coef = t = cos/(sign*sin), cross_coef = +-1
-// or +-i), i.e. one fused multiply-add per component; the product F of the sub-group's factors
-// is applied once before the amplitudes leave the registers.
+// with the uniform factor f = cos(phi) when |cos| >= 2^-10 |sin| (CFORM: self_coef = 1,
+// cross_coef = +-t, t = sin/cos, |t| <= 1024) and f = sign*sin(phi) otherwise (SFORM: self_coef =
+// t = cos/(sign*sin), cross_coef = +-1 or +-i), i.e. one fused multiply-add per component; the
+// product F of the factors is applied when the amplitudes leave the registers (deferred across
+// sub-groups while it stays within [2^-40, 2^40]).
 constexpr int kSubDim = 4;
 constexpr int kSubAmps = 1 << kSubDim;
 constexpr int kMaxCols = 12;
