@@ -283,3 +283,38 @@ def test_30q_coset_oracle():
             sel = rng.choice(len(mem), 200, replace=False)
             got = np.array([st.get_amplitudes(int(mem[s]), 1)[0] for s in sel])
             assert np.max(np.abs(got - want[sel])) <= 1e-10
+
+
+# ------------------------------------------------------------------ NEXT-3: RPE signals
+
+def test_rpe_signal_matches_oracle():
+    """Z_m = <psi|e^{i delta H~ 2^m}|psi> for the second-order partially randomized
+    method, through ps_apply_rotations + ps_inner, against the oracle applying the same stream."""
+    from paper_2504_17881_b200 import formulas, rpe
+    n = 10
+    codes, _ = workloads.random_layer(n, 80, seed=21, kind="R10")
+    codes = np.unique(codes, axis=0)
+    coeffs = np.random.default_rng(21).uniform(-1, 1, len(codes))
+    x, z = P.pauli_encode_codes(codes)
+    H = formulas.from_masks(n, x, z, coeffs)
+    HD, HR = formulas.split_deterministic(H, 30)
+    delta = 0.3
+    r = formulas.sample_count(HR.lam, delta, 3)
+    psi0 = oracle.random_state(SEED, n)
+    psi0 = psi0 / np.sqrt(oracle.norm(n, psi0))
+    for m in (0, 2, 3):
+        got = rpe.signal(n, HD, HR, delta, m, r, seed=7)
+        sx, sz, sa = formulas.evolution_stream(HD, HR, delta, 2 ** m, r, 7)
+        want = oracle.inner(n, psi0, oracle.apply_masks(n, psi0, sx, sz, sa))
+        assert abs(got - want) <= 1e-10
+        assert abs(got) <= 1 + 1e-9
+
+
+def test_rpe_eigenstate_signal():
+    """H = {h Z}, psi = |1> -> Z_m = e^{-i delta h 2^m} exactly (up to rounding)."""
+    from paper_2504_17881_b200 import formulas, rpe
+    H = formulas.from_masks(1, [0], [1], [0.7])
+    empty = H.take([])
+    for m in (0, 3, 6):
+        got = rpe.signal(1, H, empty, 0.4, m, 0, seed=1, init=1)
+        assert abs(got - np.exp(-1j * 0.4 * 0.7 * 2 ** m)) <= 1e-12
