@@ -147,6 +147,24 @@ def main():
                 one.apply_rotations(x, z, ang)
                 ref = one.get_amplitudes()
             check("G-invariance n=24 vs 1 GPU", np.max(np.abs(got - ref)), 1e-12)
+        # (h) NEXT-3: RPE signal of the partially randomized second-order method, sharded
+        from paper_2504_17881_b200 import formulas, rpe
+        n = 12
+        codes, _ = workloads.random_layer(n, 120, seed=31, kind="R10")
+        codes = np.unique(codes, axis=0)
+        coeffs = np.random.default_rng(31).uniform(-1, 1, len(codes))
+        hx, hz = P.pauli_encode_codes(codes)
+        H = formulas.from_masks(n, hx, hz, coeffs)
+        HD, HR = formulas.split_deterministic(H, 40, n_local=n - (world.bit_length() - 1))
+        r = formulas.sample_count(HR.lam, 0.3, 2)
+        for m in (0, 2):
+            zm = rpe.signal(n, HD, HR, 0.3, m, r, seed=3, world=world, rank=rank)
+            if rank == 0:
+                psi0 = oracle.random_state(SEED, n)
+                psi0 = psi0 / np.sqrt(oracle.norm(n, psi0))
+                sx, sz, sa = formulas.evolution_stream(HD, HR, 0.3, 2 ** m, r, 3)
+                want = oracle.inner(n, psi0, oracle.apply_masks(n, psi0, sx, sz, sa))
+                check(f"RPE Z_{m} (r={r})", abs(zm - want), 1e-10)
     except _SkipSmall:
         pass
     except Exception:  # noqa: BLE001
