@@ -237,7 +237,7 @@ typedef struct ps_plan_op {
                             PERMUTE: first local bit of the transposition */
     uint64_t exch_gx;    /* EXCHANGE: partner = rank xor exch_gx; PERMUTE: second local bit */
     uint32_t tile_bits;  /* TILE/COSET: log2 tile size */
-    uint32_t pad;
+    uint32_t n_sub;      /* TILE/COSET: register sub-groups the pass is split into */
 } ps_plan_op;
 
 /* Physical rotation record as executed (one per rotation per pass, in order). */

@@ -340,12 +340,14 @@ __device__ __forceinline__ void ddiag(T& r, T& i, T t, int neg) {
 // Ms bit d = sigma of element d (1: -1) xor the NEG bit of SFORM rotations
 template <int REAL, int SFORM, typename T, int DX>
 __device__ __forceinline__ void sub_pairs(T (&vr)[kSubAmps], T (&vi)[kSubAmps], uint32_t Ms, T t) {
-    constexpr int piv = hibit(DX);
+    if constexpr (DX < kSubAmps) {
+        constexpr int piv = hibit(DX);
 #pragma unroll
-    for (int d = 0; d < kSubAmps; ++d) {
-        if ((d >> piv) & 1) continue;
-        const int e = d ^ DX;
-        dpair<REAL, SFORM>(vr[d], vi[d], vr[e], vi[e], t, (int)((Ms >> d) & 1u));
+        for (int d = 0; d < kSubAmps; ++d) {
+            if ((d >> piv) & 1) continue;
+            const int e = d ^ DX;
+            dpair<REAL, SFORM>(vr[d], vi[d], vr[e], vi[e], t, (int)((Ms >> d) & 1u));
+        }
     }
 }
 
@@ -363,6 +365,7 @@ __device__ __forceinline__ void sub_rotation(T (&vr)[kSubAmps], T (&vi)[kSubAmps
     case 5: sub_pairs<REAL, SFORM, T, 5>(vr, vi, Ms, t); break;
     case 6: sub_pairs<REAL, SFORM, T, 6>(vr, vi, Ms, t); break;
     case 7: sub_pairs<REAL, SFORM, T, 7>(vr, vi, Ms, t); break;
+#if PS_SUBDIM >= 4
     case 8: sub_pairs<REAL, SFORM, T, 8>(vr, vi, Ms, t); break;
     case 9: sub_pairs<REAL, SFORM, T, 9>(vr, vi, Ms, t); break;
     case 10: sub_pairs<REAL, SFORM, T, 10>(vr, vi, Ms, t); break;
@@ -371,6 +374,9 @@ __device__ __forceinline__ void sub_rotation(T (&vr)[kSubAmps], T (&vi)[kSubAmps
     case 13: sub_pairs<REAL, SFORM, T, 13>(vr, vi, Ms, t); break;
     case 14: sub_pairs<REAL, SFORM, T, 14>(vr, vi, Ms, t); break;
     default: sub_pairs<REAL, SFORM, T, 15>(vr, vi, Ms, t); break;
+#else
+    default: break;
+#endif
     }
 }
 
@@ -1143,7 +1149,10 @@ cudaError_t launch_coset_t(T* a, int nl, const Pass& p, const DevSub* d_subs, co
     if (threads <= 128 && occ_sel == 1) return launch_coset_k<T, 128, 5>(a, nl, p, d_subs, d_trots, d_offs, l2_prefetch, grid_mult, s);
     if (threads <= 128 && occ_sel == 2) return launch_coset_k<T, 128, 6>(a, nl, p, d_subs, d_trots, d_offs, l2_prefetch, grid_mult, s);
     if (threads <= 128 && occ_sel == 3) return launch_coset_k<T, 128, 8>(a, nl, p, d_subs, d_trots, d_offs, l2_prefetch, grid_mult, s);
-    return launch_coset_k<T, kCosetThreads, 2>(a, nl, p, d_subs, d_trots, d_offs, l2_prefetch, grid_mult, s);
+#ifndef PS_COSET_MINB
+#define PS_COSET_MINB 2
+#endif
+    return launch_coset_k<T, kCosetThreads, PS_COSET_MINB>(a, nl, p, d_subs, d_trots, d_offs, l2_prefetch, grid_mult, s);
 }
 
 template <typename T, int CPASYNC>

@@ -1001,6 +1001,7 @@ extern "C" int ps_plan_describe(int n_qubits, int world, int rank, int fusion, i
             o.exch_bit = p.full ? -1 : p.ell;
             o.exch_gx = p.kind == PASS_PERMUTE ? (uint64_t)p.ell2 : p.gx;
             o.tile_bits = (uint32_t)p.kbits;
+            o.n_sub = (uint32_t)p.sub_count;
             ops[t] = o;
         }
     }

@@ -48,7 +48,10 @@ static_assert(sizeof(DevRot) == 48, "DevRot layout");
 // t = cos/(sign*sin), cross_coef = +-1 or +-i), i.e. one fused multiply-add per component; the
 // product F of the factors is applied when the amplitudes leave the registers (deferred across
 // sub-groups while it stays within [2^-40, 2^40]).
-constexpr int kSubDim = 4;
+#ifndef PS_SUBDIM
+#define PS_SUBDIM 4
+#endif
+constexpr int kSubDim = PS_SUBDIM;  // 4 (16 amplitudes per thread) or 3 (8; A/B build)
 constexpr int kSubAmps = 1 << kSubDim;
 constexpr int kMaxCols = 12;
 

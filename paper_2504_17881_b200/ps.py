@@ -12,7 +12,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libps.so")
+LIB_PATH = os.environ.get("PS_LIB_PATH") or os.path.join(_HERE, "libps.so")  # override for A/B builds
 
 C128, C64 = 0, 1
 K_STREAM, K_TILE, K_COSET, K_REDUCE, K_INIT, K_EXCHANGE, K_PERMUTE = range(7)
@@ -54,7 +54,7 @@ class Stats(ctypes.Structure):
 class PlanOp(ctypes.Structure):
     _fields_ = [("kind", ctypes.c_int32), ("first_rot", ctypes.c_int32), ("n_rot", ctypes.c_int32),
                 ("exch_bit", ctypes.c_int32), ("exch_gx", ctypes.c_uint64), ("tile_bits", ctypes.c_uint32),
-                ("pad", ctypes.c_uint32)]
+                ("n_sub", ctypes.c_uint32)]
 
 
 class PlanRot(ctypes.Structure):
@@ -195,7 +195,7 @@ def plan_describe(n: int, x, z, angles, world: int = 1, rank: int = 0, fusion: i
                                                       len(a), ops, nops.value, ctypes.byref(nops), rots, nrots.value,
                                                       ctypes.byref(nrots)))
     op_list = [dict(kind=o.kind, first_rot=o.first_rot, n_rot=o.n_rot, exch_bit=o.exch_bit, exch_gx=int(o.exch_gx),
-                    tile_bits=o.tile_bits) for o in ops[: nops.value]]
+                    tile_bits=o.tile_bits, n_sub=o.n_sub) for o in ops[: nops.value]]
     rot_list = [dict(x=int(r.x), z=int(r.z), y=r.y, sign=r.sign, angle=r.angle) for r in rots[: nrots.value]]
     return op_list, rot_list
 
