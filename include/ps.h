@@ -66,7 +66,15 @@ enum {
     PS_K_INIT = 4,     /* K6: state initialisation                                            */
     PS_K_EXCHANGE = 5, /* K3: half-vector exchange (NVLink P2P swap or NCCL send/recv)       */
     PS_K_PERMUTE = 6,  /* local qubit transposition pass (restoring the canonical layout)     */
-    PS_K_COUNT = 7
+    PS_K_MIRROR = 7,   /* PS_OPT_LAYOUT=2: butterfly / recombine passes of Eq. (core_state)    */
+    PS_K_COUNT = 8
+};
+
+/* extra plan-op kinds (ps_plan_describe only): the paper's three-step grouped execution */
+enum {
+    PS_OP_MIRROR_BEGIN = 8,  /* B <- conj(w_k) A_(k xor gx) (full exchange), butterfly A,B      */
+    PS_OP_MIRROR_SWITCH = 9, /* following passes act on B (with negated angles)               */
+    PS_OP_MIRROR_END = 10    /* A <- (A + B)/sqrt(2); passes act on A again                   */
 };
 
 typedef struct ps_stats {
@@ -100,7 +108,11 @@ enum {
                                  sector promotion on the gathered loads (default 512 = bit 9) */
     PS_OPT_LAYOUT = 9,        /* world > 1: 1 = lazy qubit-swap layout kept across calls, swaps chosen
                                  by furthest next use (default); 0 = one half-vector exchange per run
-                                 sharing the upper X-part, swapped back at once (Eq. (1) economy) */
+                                 sharing the upper X-part, swapped back at once (Eq. (1) economy);
+                                 2 = the paper's three-step execution: a mirror buffer
+                                 per GPU (doubles memory), one full-partition exchange per group
+                                 sharing the upper string, butterfly, U+ on A and U- on B,
+                                 recombine -- kept for A/B */
     PS_OPT_TRANSPORT = 10     /* world > 1: 1 = NVLink P2P swap kernel on CUDA-IPC peer pointers when
                                  available (default); 0 = NCCL send/recv with staging */
 };
@@ -230,7 +242,9 @@ int ps_gate_to_rotations(const char *gate, const int *qubits, int n_qubits_gate,
  * up to cap ops.  Each op is one HBM pass, one exchange or one local transposition; for a pass,
  * the rotations it applies are given in PHYSICAL local coordinates. */
 typedef struct ps_plan_op {
-    int32_t kind;        /* PS_K_STREAM, PS_K_TILE, PS_K_COSET, PS_K_EXCHANGE or PS_K_PERMUTE */
+    int32_t kind;        /* PS_K_STREAM, PS_K_TILE, PS_K_COSET, PS_K_EXCHANGE, PS_K_PERMUTE or
+                            PS_OP_MIRROR_*; MIRROR_BEGIN carries gx in exch_gx and the upper
+                            Z-part in tile_bits (low 32 bits) */
     int32_t first_rot;   /* index of the first input rotation covered */
     int32_t n_rot;       /* rotations applied by this op (EXCHANGE: 0, or 1 for a full exchange) */
     int32_t exch_bit;    /* EXCHANGE: local pivot bit l swapped with the partner (-1: full exchange);

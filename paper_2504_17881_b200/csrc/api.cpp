@@ -34,6 +34,9 @@ cudaError_t launch_init_random(int dtype, void* a, uint64_t n, uint64_t seed, ui
 cudaError_t launch_set_one(int dtype, void* a, uint64_t idx, cudaStream_t s);
 cudaError_t launch_scale(int dtype, void* a, uint64_t n, double f, cudaStream_t s);
 cudaError_t launch_permute(int dtype, void* a, int nl, int b1, int b2, cudaStream_t s);
+cudaError_t launch_butterfly(int dtype, void* A, void* B, uint64_t n, int wr, int wi, cudaStream_t s);
+cudaError_t launch_recombine(int dtype, void* A, const void* B, uint64_t n, cudaStream_t s);
+cudaError_t launch_p2p_copy(int dtype, void* dst, const void* src, uint64_t n, cudaStream_t s);
 cudaError_t launch_p2p_swap(int dtype, void* local, void* peer, uint64_t rows, uint64_t row_amps, uint64_t my_off,
                             uint64_t peer_off, uint64_t e0, uint64_t e1, cudaStream_t s);
 
@@ -88,6 +91,7 @@ struct ps_state {
     std::vector<void*> peers;  // CUDA-IPC peer pointers to every rank's local slice (P2P transport)
     std::vector<void*> peer_bases;
     bool p2p = false;
+    void* d_mirror = nullptr;  // PS_OPT_LAYOUT=2 mirror buffer B_k
     int layout = 1, transport = 1;
     // options
     int profile = 0, fusion = 2, tile_bits = 11, vec256 = 1, max_pass_rots = 1 << 30, tile_tma = 2, chunk_bits = 0, tile_tune = 512;
@@ -206,6 +210,7 @@ static void free_state(ps_state* h) {
     for (void* b : h->peer_bases)
         if (b) cudaIpcCloseMemHandle(b);
     if (h->d_barrier) cudaFree(h->d_barrier);
+    if (h->d_mirror) cudaFree(h->d_mirror);
     if (h->comm) ncclCommDestroy(h->comm);
     for (int t = 0; t < 2; ++t) {
         if (h->d_xstage[t]) cudaFree(h->d_xstage[t]);
@@ -423,7 +428,19 @@ extern "C" int ps_set_option(ps_handle h, int option, int64_t value) {
     case PS_OPT_VEC256: h->vec256 = value ? 1 : 0; break;
     case PS_OPT_TILE_TUNE: h->tile_tune = (int)value; break;
     case PS_OPT_LAYOUT:
-        if (value < 0 || value > 1) return fail(PS_EINVAL, "layout must be 0 or 1");
+        if (value < 0 || value > 2) return fail(PS_EINVAL, "layout must be 0, 1 or 2");
+        if (value == 2 && h->world > 1 && !h->d_mirror) {
+            cudaSetDevice(h->device);
+            cudaError_t e = cudaMalloc(&h->d_mirror, h->amp_bytes << h->nl);
+            if (e != cudaSuccess) {
+                h->d_mirror = nullptr;
+                return fail(PS_ENOMEM, std::string("mirror buffer: ") + cudaGetErrorString(e));
+            }
+        }
+        if (value == 2 && h->world > 1) {
+            int rc = restore_layout(h);
+            if (rc) return rc;
+        }
         h->layout = (int)value;
         break;
     case PS_OPT_TRANSPORT: h->transport = value ? 1 : 0; break;
@@ -719,23 +736,75 @@ static PlanConfig plan_config(const ps_state* h) {
     return cfg;
 }
 
+// the paper's step (i) + (ii): B <- conj(w_k) A_(k xor gx) via a full-partition exchange, butterfly
+static int mirror_begin(ps_state* h, const Pass& p) {
+    if (!h->d_mirror) return fail(PS_ESTATE, "mirror buffer missing (PS_OPT_LAYOUT=2)");
+    const int partner = h->rank ^ (int)p.gx;
+    const uint64_t N = local_amps(h);
+    const size_t bytes = h->amp_bytes * N;
+    {
+        Timed t(h, PS_K_EXCHANGE);
+        if (h->p2p && h->transport) {
+            int rc = barrier(h);
+            if (rc) return rc;
+            CUDA_TRY(h, launch_p2p_copy(h->dtype, h->d_mirror, h->peers[partner], N, h->stream));
+            rc = barrier(h);  // the partner may overwrite its A (butterfly) only after my read
+            if (rc) return rc;
+        } else {
+            for (size_t off = 0; off < bytes; off += h->chunk_bytes) {
+                const size_t len = std::min(h->chunk_bytes, bytes - off);
+                NCCL_TRY(h, ncclGroupStart());
+                NCCL_TRY(h, ncclSend((const char*)h->d_state + off, len, ncclChar, partner, h->comm, h->stream));
+                NCCL_TRY(h, ncclRecv((char*)h->d_mirror + off, len, ncclChar, partner, h->comm, h->stream));
+                NCCL_TRY(h, ncclGroupEnd());
+            }
+        }
+        h->stats.exchanges += 1;
+        h->stats.launches[PS_K_EXCHANGE] += 1;
+        h->stats.nvlink_bytes += (double)bytes;
+        h->stats.algo_bytes[PS_K_EXCHANGE] += (double)bytes * 2.0;
+    }
+    Timed t(h, PS_K_MIRROR);
+    CUDA_TRY(h, launch_butterfly(h->dtype, h->d_state, h->d_mirror, N, (int)p.wr, (int)p.wi, h->stream));
+    h->stats.launches[PS_K_MIRROR] += 1;
+    h->stats.algo_bytes[PS_K_MIRROR] += 4.0 * (double)bytes;
+    return PS_OK;
+}
+
 static int execute_plan(ps_state* h, const Plan& plan) {
     int rc = upload_plan(h, plan);
     if (rc) return rc;
     const double pass_bytes = 2.0 * (double)h->amp_bytes * (double)local_amps(h);
+    void* target = h->d_state;  // MIRROR_SWITCH redirects passes to the mirror buffer
     for (const Pass& p : plan.passes) {
         switch (p.kind) {
         case PASS_STREAM: {
             Timed t(h, PS_K_STREAM);
-            CUDA_TRY(h, launch_stream(h->dtype, h->d_state, h->nl, p, h->d_rots, h->vec256, h->stream));
+            CUDA_TRY(h, launch_stream(h->dtype, target, h->nl, p, h->d_rots, h->vec256, h->stream));
             break;
         }
         case PASS_TILE:
         case PASS_COSET: {
             Timed t(h, p.kind);
-            CUDA_TRY(h, launch_tile(h->dtype, h->d_state, h->nl, p, h->d_subs, h->d_trots, h->d_offs, h->tile_tma,
+            CUDA_TRY(h, launch_tile(h->dtype, target, h->nl, p, h->d_subs, h->d_trots, h->d_offs, h->tile_tma,
                                     h->tile_tune, h->stream));
             break;
+        }
+        case PASS_MIRROR_BEGIN:
+            rc = mirror_begin(h, p);
+            if (rc) return rc;
+            target = h->d_state;
+            continue;
+        case PASS_MIRROR_SWITCH:
+            target = h->d_mirror;
+            continue;
+        case PASS_MIRROR_END: {
+            Timed t(h, PS_K_MIRROR);
+            CUDA_TRY(h, launch_recombine(h->dtype, h->d_state, h->d_mirror, local_amps(h), h->stream));
+            h->stats.launches[PS_K_MIRROR] += 1;
+            h->stats.algo_bytes[PS_K_MIRROR] += 1.5 * pass_bytes;
+            target = h->d_state;
+            continue;
         }
         case PASS_PERMUTE: {
             Timed t(h, PS_K_PERMUTE);

@@ -1080,6 +1080,38 @@ __global__ void k_p2p_swap(T* __restrict__ local, T* __restrict__ peer, uint64_t
     }
 }
 
+// Eq. (core_state) helpers (PS_OPT_LAYOUT=2)
+// butterfly: b = w B (w = conj(w_k) in {+-1, +-i}); A <- (A + b)/sqrt2, B <- (A - b)/sqrt2
+template <typename T>
+__global__ void k_butterfly(T* __restrict__ A, T* __restrict__ B, uint64_t n, int wr, int wi) {
+    const T h = (T)0.70710678118654752440;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        const T ar = A[2 * i], ai = A[2 * i + 1], xr = B[2 * i], xi = B[2 * i + 1];
+        const T br = (T)wr * xr - (T)wi * xi, bi = (T)wr * xi + (T)wi * xr;  // exact: w in {+-1, +-i}
+        A[2 * i] = (ar + br) * h;
+        A[2 * i + 1] = (ai + bi) * h;
+        B[2 * i] = (ar - br) * h;
+        B[2 * i + 1] = (ai - bi) * h;
+    }
+}
+
+template <typename T>
+__global__ void k_recombine(T* __restrict__ A, const T* __restrict__ B, uint64_t n) {
+    const T h = (T)0.70710678118654752440;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < 2 * n; i += (uint64_t)gridDim.x * blockDim.x)
+        A[i] = (A[i] + B[i]) * h;
+}
+
+// dst <- peer's slice (NVLink reads through a CUDA-IPC pointer)
+template <typename T>
+__global__ void k_p2p_copy(T* __restrict__ dst, const T* __restrict__ src, uint64_t n) {
+    using V2 = typename SmemAmp<T>::V;
+    V2* d = reinterpret_cast<V2*>(dst);
+    const V2* r = reinterpret_cast<const V2*>(src);
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+        d[i] = __ldcv(&r[i]);
+}
+
 int g_num_sms = 0;
 int num_sms() {
     if (g_num_sms == 0) {
@@ -1327,6 +1359,33 @@ cudaError_t launch_p2p_swap(int dtype, void* local, void* peer, uint64_t rows, u
         k_p2p_swap<double><<<grid, 512, 0, s>>>((double*)local, (double*)peer, row_amps, my_off, peer_off, e0, e1);
     else
         k_p2p_swap<float><<<grid, 512, 0, s>>>((float*)local, (float*)peer, row_amps, my_off, peer_off, e0, e1);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_butterfly(int dtype, void* A, void* B, uint64_t n, int wr, int wi, cudaStream_t s) {
+    const unsigned grid = red_grid(n) * 2;
+    if (dtype == PS_C128)
+        k_butterfly<double><<<grid, kRedThreads, 0, s>>>((double*)A, (double*)B, n, wr, wi);
+    else
+        k_butterfly<float><<<grid, kRedThreads, 0, s>>>((float*)A, (float*)B, n, wr, wi);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_recombine(int dtype, void* A, const void* B, uint64_t n, cudaStream_t s) {
+    const unsigned grid = red_grid(n) * 2;
+    if (dtype == PS_C128)
+        k_recombine<double><<<grid, kRedThreads, 0, s>>>((double*)A, (const double*)B, n);
+    else
+        k_recombine<float><<<grid, kRedThreads, 0, s>>>((float*)A, (const float*)B, n);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_p2p_copy(int dtype, void* dst, const void* src, uint64_t n, cudaStream_t s) {
+    const unsigned grid = (unsigned)num_sms() * 4;
+    if (dtype == PS_C128)
+        k_p2p_copy<double><<<grid, 512, 0, s>>>((double*)dst, (const double*)src, n);
+    else
+        k_p2p_copy<float><<<grid, 512, 0, s>>>((float*)dst, (const float*)src, n);
     return cudaGetLastError();
 }
 

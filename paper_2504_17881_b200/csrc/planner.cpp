@@ -667,9 +667,88 @@ void make_plan(const PlanConfig& cfg, const uint64_t* x, const uint64_t* z, cons
     make_plan_core(cfg, xs.data(), zs.data(), as.data(), xs.size(), plan);
 }
 
+// the paper's grouped execution: groups of consecutive rotations sharing the
+// upper string Q = (gx, gz), gx != 0, run as MIRROR_BEGIN; passes of e^{+i phi P_l} on A;
+// MIRROR_SWITCH; passes of e^{-i phi P_l} on B; MIRROR_END.  P_l = the lower strings.
+static void plan_mirror(const PlanConfig& cfg, const uint64_t* x, const uint64_t* z, const double* angle,
+                        size_t count, Plan* plan) {
+    const int nl = cfg.n_local;
+    const uint64_t lmask = (1ull << nl) - 1;
+    const uint64_t rank = (uint64_t)cfg.rank;
+    std::vector<PhysRot> seg;
+    auto flush = [&]() {
+        form_passes(seg, cfg, plan);
+        seg.clear();
+    };
+    size_t i = 0;
+    while (i < count) {
+        const uint64_t gx = x[i] >> nl, gz = z[i] >> nl;
+        if (gx == 0) {
+            PhysRot pr;
+            pr.x = x[i] & lmask;
+            pr.z = z[i] & lmask;
+            pr.y = popc64(x[i] & z[i]) & 3;
+            pr.sign = parity64(gz & rank) ? -1 : 1;
+            pr.phi = angle[i];
+            pr.input = (int)i;
+            seg.push_back(pr);
+            push_debug_rot(cfg, plan, pr);
+            ++i;
+            continue;
+        }
+        size_t j = i;
+        while (j < count && (x[j] >> nl) == gx && (z[j] >> nl) == gz) ++j;
+        flush();
+        Pass b;
+        b.kind = PASS_MIRROR_BEGIN;
+        b.gx = gx;
+        b.gz = gz;
+        b.first_input = (int)i;
+        b.n_input = (int)(j - i);
+        // Q|k> = w_k |k xor gx>, w_k = i^popc(gx&gz) (-1)^popc(gz&k); B holds conj(w_k) A_(k xor gx)
+        const int e = ((popc64(gx & gz) & 3) + (parity64(gz & rank) ? 2 : 0)) & 3;
+        const double re[4] = {1, 0, -1, 0}, im[4] = {0, 1, 0, -1};
+        b.wr = re[e];
+        b.wi = -im[e];
+        plan->passes.push_back(b);
+        plan->exchanges += 1;
+        for (int half = 0; half < 2; ++half) {
+            if (half == 1) {
+                Pass sw;
+                sw.kind = PASS_MIRROR_SWITCH;
+                sw.first_input = (int)i;
+                plan->passes.push_back(sw);
+            }
+            for (size_t t = i; t < j; ++t) {
+                PhysRot pr;
+                pr.x = x[t] & lmask;
+                pr.z = z[t] & lmask;
+                pr.y = popc64(pr.x & pr.z) & 3;  // the lower string's own i^(#Y)
+                pr.sign = 1;
+                pr.phi = half ? -angle[t] : angle[t];
+                pr.input = (int)t;
+                seg.push_back(pr);
+                push_debug_rot(cfg, plan, pr);
+            }
+            flush();
+        }
+        Pass en;
+        en.kind = PASS_MIRROR_END;
+        en.first_input = (int)i;
+        plan->passes.push_back(en);
+        i = j;
+    }
+    flush();
+}
+
 static void make_plan_core(const PlanConfig& cfg, const uint64_t* x, const uint64_t* z, const double* angle,
                            size_t count, Plan* plan) {
     clear_plan(plan);
+    if (cfg.world > 1 && cfg.layout == 2) {
+        plan_mirror(cfg, x, z, angle, count, plan);
+        plan->perm_out.clear();
+        return;
+    }
     if (cfg.world > 1 && cfg.layout == 1) {
         plan_lazy(cfg, x, z, angle, count, plan);
         return;
@@ -997,11 +1076,14 @@ extern "C" int ps_plan_describe(int n_qubits, int world, int rank, int fusion, i
             ps_plan_op o{};
             o.kind = p.kind;
             o.first_rot = p.first_input;
-            o.n_rot = (p.kind == PASS_PERMUTE || (p.kind == PASS_EXCHANGE && !p.full)) ? 0 : p.n_input;
+            o.n_rot = (p.kind == PASS_PERMUTE || p.kind >= PASS_MIRROR_BEGIN || (p.kind == PASS_EXCHANGE && !p.full))
+                          ? 0
+                          : p.n_input;
             o.exch_bit = p.full ? -1 : p.ell;
             o.exch_gx = p.kind == PASS_PERMUTE ? (uint64_t)p.ell2 : p.gx;
             o.tile_bits = (uint32_t)p.kbits;
             o.n_sub = (uint32_t)p.sub_count;
+            if (p.kind == PASS_MIRROR_BEGIN) o.tile_bits = (uint32_t)p.gz;
             ops[t] = o;
         }
     }

@@ -95,6 +95,9 @@ enum PassKind : int {
     PASS_COSET = PS_K_COSET,
     PASS_EXCHANGE = PS_K_EXCHANGE,
     PASS_PERMUTE = PS_K_PERMUTE,  // local transposition of physical bits ell and ell2
+    PASS_MIRROR_BEGIN = PS_OP_MIRROR_BEGIN,
+    PASS_MIRROR_SWITCH = PS_OP_MIRROR_SWITCH,
+    PASS_MIRROR_END = PS_OP_MIRROR_END,
 };
 
 constexpr int kMaxTileHigh = 10;  // at most 2^10 gathered chunks per coset tile
@@ -122,6 +125,9 @@ struct Pass {
     int full = 0;         // 1: single-rotation full exchange (no free pivot); rot_begin/rot_count valid
     // PERMUTE
     int ell2 = 0;
+    // MIRROR_BEGIN: upper string (gx, gz) and this rank's conj(w_k)
+    uint64_t gz = 0;
+    double wr = 1.0, wi = 0.0;
 };
 
 struct Plan {

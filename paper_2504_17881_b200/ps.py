@@ -15,8 +15,9 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("PS_LIB_PATH") or os.path.join(_HERE, "libps.so")  # override for A/B builds
 
 C128, C64 = 0, 1
-K_STREAM, K_TILE, K_COSET, K_REDUCE, K_INIT, K_EXCHANGE, K_PERMUTE = range(7)
-KERNEL_NAMES = ["stream", "tile", "coset", "reduce", "init", "exchange", "permute"]
+K_STREAM, K_TILE, K_COSET, K_REDUCE, K_INIT, K_EXCHANGE, K_PERMUTE, K_MIRROR = range(8)
+KERNEL_NAMES = ["stream", "tile", "coset", "reduce", "init", "exchange", "permute", "mirror"]
+OP_MIRROR_BEGIN, OP_MIRROR_SWITCH, OP_MIRROR_END = 8, 9, 10
 OPT_PROFILE, OPT_FUSION, OPT_TILE_BITS, OPT_CHUNK_BYTES, OPT_MAX_PASS_ROTS, OPT_VEC256, OPT_TILE_TMA, OPT_CHUNK_BITS, OPT_TILE_TUNE, OPT_LAYOUT, OPT_TRANSPORT = range(11)
 
 
@@ -31,11 +32,11 @@ class Stats(ctypes.Structure):
         ("rotations", ctypes.c_uint64),
         ("passes", ctypes.c_uint64),
         ("exchanges", ctypes.c_uint64),
-        ("launches", ctypes.c_uint64 * 7),
-        ("rotations_by", ctypes.c_uint64 * 7),
-        ("algo_bytes", ctypes.c_double * 7),
+        ("launches", ctypes.c_uint64 * 8),
+        ("rotations_by", ctypes.c_uint64 * 8),
+        ("algo_bytes", ctypes.c_double * 8),
         ("nvlink_bytes", ctypes.c_double),
-        ("kernel_ms", ctypes.c_double * 7),
+        ("kernel_ms", ctypes.c_double * 8),
     ]
 
     def as_dict(self):

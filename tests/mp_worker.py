@@ -65,7 +65,8 @@ def main():
             x, z = P.pauli_encode_codes(codes)
             want = oracle.apply(n, oracle.random_state(SEED, n), codes, ang) if rank == 0 else None
             for fusion, chunk, layout, transport in ((0, 4096, 0, 0), (1, 1 << 28, 0, 1), (2, 4096, 0, 0),
-                                                     (2, 1 << 28, 1, 1), (0, 1 << 28, 1, 0), (2, 4096, 1, 1)):
+                                                     (2, 1 << 28, 1, 1), (0, 1 << 28, 1, 0), (2, 4096, 1, 1),
+                                                     (2, 1 << 28, 2, 1), (1, 4096, 2, 0)):
                 with P.State(n, "c128", world=world, rank=rank) as st:
                     st.set_option(ps.OPT_FUSION, fusion)
                     st.set_option(ps.OPT_TILE_BITS, 6)

@@ -180,9 +180,37 @@ def _run_model(n, world, x, z, ang, fusion=2, tile_bits=3, layout=1):
 
 def _execute(n, world, psi, plans, nl):
     local = [psi[r << nl:(r + 1) << nl].copy() for r in range(world)]
+    mirror = [None] * world
+    on_mirror = False
     cursors = [0] * world
     ops0 = plans[0][0]
     for t, op in enumerate(ops0):
+        if op["kind"] == ps.OP_MIRROR_BEGIN:
+            # paper step (i)+(ii): B_k = conj(w_k) A_(k xor gx), Q|k> = w_k|k xor gx>
+            gx, gz = op["exch_gx"], op["tile_bits"]
+            yq = bin(gx & gz).count("1") % 4
+            newA, newB = [], []
+            for r in range(world):
+                w = (1j ** yq) * (-1.0 if bin(gz & r).count("1") % 2 else 1.0)
+                b = np.conj(w) * local[r ^ gx]
+                newA.append((local[r] + b) / math.sqrt(2))
+                newB.append((local[r] - b) / math.sqrt(2))
+            local, mirror = newA, newB
+            on_mirror = False
+            continue
+        if op["kind"] == ps.OP_MIRROR_SWITCH:
+            on_mirror = True
+            continue
+        if op["kind"] == ps.OP_MIRROR_END:
+            local = [(a + b) / math.sqrt(2) for a, b in zip(local, mirror)]
+            on_mirror = False
+            continue
+        if op["kind"] in (ps.K_STREAM, ps.K_TILE, ps.K_COSET) and on_mirror:
+            for r in range(world):
+                for _ in range(op["n_rot"]):
+                    mirror[r] = _apply_phys(mirror[r], plans[r][1][cursors[r]])
+                    cursors[r] += 1
+            continue
         if op["kind"] == ps.K_PERMUTE:
             a, b = op["exch_bit"], op["exch_gx"]
             idx = np.arange(1 << nl)
@@ -224,7 +252,7 @@ def _execute(n, world, psi, plans, nl):
 
 @pytest.mark.parametrize("world", [1, 2, 4, 8])
 @pytest.mark.parametrize("kind", ["R4", "R10", "S8"])
-@pytest.mark.parametrize("layout", [0, 1])
+@pytest.mark.parametrize("layout", [0, 1, 2])
 def test_planner_model_matches_oracle(world, kind, layout):
     n = 7
     codes, ang = workloads.random_layer(n, 60, seed=world, kind=kind)
@@ -260,6 +288,26 @@ def test_planner_full_exchange_fallback(layout):
     psi = oracle.random_state(5, n)
     plans, nl = _run_model(n, world, x, z, ang, layout=layout)
     assert any(o["kind"] == ps.K_EXCHANGE and o["exch_bit"] < 0 for o in plans[0][0])
+    got = _execute(n, world, psi, plans, nl)
+    assert np.max(np.abs(got - oracle.apply(n, psi, codes, ang))) <= 1e-12
+
+
+def test_mirror_mode_one_exchange_per_group():
+    """PS_OPT_LAYOUT=2: a group sharing the upper string Q costs one exchange, and
+    grouped execution equals the sequential product (Eq. (core_state), checked by the model)."""
+    n, world = 8, 4
+    rng = np.random.default_rng(3)
+    L = 25
+    codes = np.zeros((L, n), np.uint8)
+    codes[:, :6] = rng.integers(0, 4, size=(L, 6))
+    codes[:, 6] = 2  # Y on global qubit 6
+    codes[:, 7] = 3  # Z on global qubit 7
+    x, z = P.pauli_encode_codes(codes)
+    ang = rng.uniform(-1, 1, L)
+    ops, _ = P.plan_describe(n, x, z, ang, world=world, rank=1, layout=2)
+    assert sum(o["kind"] == ps.OP_MIRROR_BEGIN for o in ops) == 1
+    plans, nl = _run_model(n, world, x, z, ang, layout=2)
+    psi = oracle.random_state(9, n)
     got = _execute(n, world, psi, plans, nl)
     assert np.max(np.abs(got - oracle.apply(n, psi, codes, ang))) <= 1e-12
 
