@@ -56,6 +56,7 @@ def parse():
     ap.add_argument("--tile-tune", type=int, default=-1)
     ap.add_argument("--layout", type=int, default=1, help="world > 1: 1 lazy qubit swaps, 0 runs + swap-back")
     ap.add_argument("--transport", type=int, default=1, help="world > 1: 1 NVLink P2P, 0 NCCL send/recv")
+    ap.add_argument("--overlap", type=int, default=1, help="world > 1: overlap swaps with the next pass")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     return ap.parse_args()
@@ -265,6 +266,7 @@ def run_ours(args):
         st.set_option(ps.OPT_TILE_TUNE, args.tile_tune)
     st.set_option(ps.OPT_LAYOUT, args.layout)
     st.set_option(ps.OPT_TRANSPORT, args.transport)
+    st.set_option(ps.OPT_OVERLAP, args.overlap)
     st.set_option(ps.OPT_PROFILE, 1)
     enc = layers(args, args.warmup + args.steps, world)
     rot_per_step = len(enc[0][2])
@@ -354,7 +356,7 @@ def run_ours(args):
             "data": "synthetic",
             "config": {"workload": workload_name(args), "n_qubits": args.n, "rotations_per_step": rot_per_step,
                        "fusion": args.fusion, "tile_mode": args.tile_mode, "tile_bits": args.tile_bits or 11,
-                       "layout": args.layout, "transport": args.transport,
+                       "layout": args.layout, "transport": args.transport, "overlap": args.overlap,
                        "parallelism": f"state sharded over {world} GPU(s) by top qubits",
                        "l2": "inputs larger than L2 (state %.1f GiB per GPU)" % (local_state / 2 ** 30)},
             "hbm_gbs": hbm_alg,

@@ -113,8 +113,10 @@ enum {
                                  per GPU (doubles memory), one full-partition exchange per group
                                  sharing the upper string, butterfly, U+ on A and U- on B,
                                  recombine -- kept for A/B */
-    PS_OPT_TRANSPORT = 10     /* world > 1: 1 = NVLink P2P swap kernel on CUDA-IPC peer pointers when
+    PS_OPT_TRANSPORT = 10,    /* world > 1: 1 = NVLink P2P swap kernel on CUDA-IPC peer pointers when
                                  available (default); 0 = NCCL send/recv with staging */
+    PS_OPT_OVERLAP = 11       /* world > 1, P2P: 1 = overlap each swap with the following tile pass
+                                 on a second stream (default); 0 = serialise */
 };
 
 /* ------------------------------------------------------------------------------------------ */

@@ -38,7 +38,7 @@ cudaError_t launch_butterfly(int dtype, void* A, void* B, uint64_t n, int wr, in
 cudaError_t launch_recombine(int dtype, void* A, const void* B, uint64_t n, cudaStream_t s);
 cudaError_t launch_p2p_copy(int dtype, void* dst, const void* src, uint64_t n, cudaStream_t s);
 cudaError_t launch_p2p_swap(int dtype, void* local, void* peer, uint64_t rows, uint64_t row_amps, uint64_t my_off,
-                            uint64_t peer_off, uint64_t e0, uint64_t e1, cudaStream_t s);
+                            uint64_t peer_off, uint64_t t0, uint64_t t1, int fb, uint64_t fv, cudaStream_t s);
 
 static thread_local std::string g_last_error;
 void set_last_error(const std::string& msg) { g_last_error = msg; }
@@ -92,6 +92,9 @@ struct ps_state {
     std::vector<void*> peer_bases;
     bool p2p = false;
     void* d_mirror = nullptr;  // PS_OPT_LAYOUT=2 mirror buffer B_k
+    cudaStream_t xstream = nullptr;  // second stream: swaps overlapped with the next pass
+    cudaEvent_t xev[2] = {nullptr, nullptr};
+    int overlap = 1;
     int layout = 1, transport = 1;
     // options
     int profile = 0, fusion = 2, tile_bits = 11, vec256 = 1, max_pass_rots = 1 << 30, tile_tma = 2, chunk_bits = 0, tile_tune = 512;
@@ -211,6 +214,9 @@ static void free_state(ps_state* h) {
         if (b) cudaIpcCloseMemHandle(b);
     if (h->d_barrier) cudaFree(h->d_barrier);
     if (h->d_mirror) cudaFree(h->d_mirror);
+    if (h->xstream) cudaStreamDestroy(h->xstream);
+    for (int t = 0; t < 2; ++t)
+        if (h->xev[t]) cudaEventDestroy(h->xev[t]);
     if (h->comm) ncclCommDestroy(h->comm);
     for (int t = 0; t < 2; ++t) {
         if (h->d_xstage[t]) cudaFree(h->d_xstage[t]);
@@ -299,6 +305,14 @@ static void setup_p2p(ps_state* h) {
         cudaStreamSynchronize(h->stream) == cudaSuccess)
         h->p2p = agree == 1;
     cudaMemsetAsync(d_flag, 0, sizeof(int), h->stream);
+    if (h->p2p) {
+        if (cudaStreamCreateWithFlags(&h->xstream, cudaStreamNonBlocking) != cudaSuccess ||
+            cudaEventCreateWithFlags(&h->xev[0], cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&h->xev[1], cudaEventDisableTiming) != cudaSuccess) {
+            cudaGetLastError();
+            h->overlap = 0;
+        }
+    }
 }
 
 extern "C" int ps_create_ex(int n_qubits, int dtype, void* dev_buf, size_t bytes, void* stream, int rank,
@@ -444,6 +458,7 @@ extern "C" int ps_set_option(ps_handle h, int option, int64_t value) {
         h->layout = (int)value;
         break;
     case PS_OPT_TRANSPORT: h->transport = value ? 1 : 0; break;
+    case PS_OPT_OVERLAP: h->overlap = (value && h->xstream) ? 1 : 0; break;
     case PS_OPT_CHUNK_BITS:
         if (value < 0 || value > 12) return fail(PS_EINVAL, "chunk bits must be 0..12 (0 = default)");
         h->chunk_bits = (int)value;
@@ -594,7 +609,8 @@ static int exchange_half(ps_state* h, const Pass& p) {
         int rc = barrier(h);
         if (rc) return rc;
         CUDA_TRY(h, launch_p2p_swap(h->dtype, h->d_state, h->peers[partner], rows, row_amps,
-                                    (uint64_t)(1 - p.keep) * row_amps, (uint64_t)p.keep * row_amps, e0, e1, h->stream));
+                                    (uint64_t)(1 - p.keep) * row_amps, (uint64_t)p.keep * row_amps, e0, e1, -1, 0,
+                                    h->stream));
         rc = barrier(h);
         if (rc) return rc;
         h->stats.nvlink_bytes += (double)(rows * row_bytes);
@@ -636,6 +652,81 @@ static int exchange_half(ps_state* h, const Pass& p) {
     }
     h->stats.exchanges += 1;
     h->stats.algo_bytes[PS_K_EXCHANGE] += (double)(rows * row_bytes) * 2.0;
+    return PS_OK;
+}
+
+static int barrier_on(ps_state* h, cudaStream_t st, int slot) {
+    NCCL_TRY(h, ncclAllReduce(h->d_barrier + slot, h->d_barrier + slot, 1, ncclInt32, ncclSum, h->comm, st));
+    return PS_OK;
+}
+
+static bool can_overlap(const ps_state* h, const Pass& ex, const Pass* np) {
+    return h->overlap && h->xstream && h->p2p && h->transport && !ex.full && ex.kind == PASS_EXCHANGE && np &&
+           (np->kind == PASS_TILE || np->kind == PASS_COSET) && h->tile_tma == 2 && np->free_mask != 0;
+}
+
+// swap E(gx, ell) overlapped with the following tile pass: the pass is split
+// by one of its free bits f; the half of its tiles that needs no (or only the already swapped)
+// data runs on the main stream while the second stream swaps the rest
+static int exchange_overlap(ps_state* h, const Pass& ex, const Pass& np) {
+    const int partner = h->rank ^ (int)ex.gx;
+    const uint64_t rows = 1ull << (h->nl - 1 - ex.ell);
+    const uint64_t row_amps = 1ull << ex.ell, total = rows * row_amps;
+    const uint64_t my_off = (uint64_t)(1 - ex.keep) * row_amps, peer_off = (uint64_t)ex.keep * row_amps;
+    const bool f_is_ell = (np.free_mask >> ex.ell) & 1;
+    const int f = f_is_ell ? ex.ell : highest_bit(np.free_mask);
+    Pass first = np, second = np;
+    first.free_mask = second.free_mask = np.free_mask & ~(1ull << f);
+    int rc = barrier(h);  // every rank's earlier passes are done
+    if (rc) return rc;
+    if (f_is_ell) {
+        // tiles on the kept side (bit ell == keep) touch no swapped slot
+        first.or_mask = np.or_mask | ((uint64_t)ex.keep << f);
+        second.or_mask = np.or_mask | ((uint64_t)(1 - ex.keep) << f);
+        CUDA_TRY(h, cudaEventRecord(h->xev[0], h->stream));
+        CUDA_TRY(h, cudaStreamWaitEvent(h->xstream, h->xev[0], 0));
+        const uint64_t e0 = ex.keep ? total / 2 : 0, e1 = ex.keep ? total : total / 2;
+        CUDA_TRY(h, launch_p2p_swap(h->dtype, h->d_state, h->peers[partner], rows, row_amps, my_off, peer_off, e0, e1,
+                                    -1, 0, h->xstream));
+    } else {
+        // element bit of f inside the region enumeration (local index = row 2^(ell+1) + half 2^ell + col)
+        const int fb = f < ex.ell ? f : f - 1;
+        const uint64_t half = total / 2;
+        const uint64_t t0 = ex.keep ? half / 2 : 0, t1 = ex.keep ? half : half / 2;
+        CUDA_TRY(h, launch_p2p_swap(h->dtype, h->d_state, h->peers[partner], rows, row_amps, my_off, peer_off, t0, t1,
+                                    fb, 0, h->stream));
+        rc = barrier(h);  // the f = 0 quarter is swapped on both ranks
+        if (rc) return rc;
+        first.or_mask = np.or_mask;
+        second.or_mask = np.or_mask | (1ull << f);
+        CUDA_TRY(h, cudaEventRecord(h->xev[0], h->stream));
+        CUDA_TRY(h, cudaStreamWaitEvent(h->xstream, h->xev[0], 0));
+        CUDA_TRY(h, launch_p2p_swap(h->dtype, h->d_state, h->peers[partner], rows, row_amps, my_off, peer_off, t0, t1,
+                                    fb, 1, h->xstream));
+    }
+    rc = barrier_on(h, h->xstream, 1);
+    if (rc) return rc;
+    CUDA_TRY(h, cudaEventRecord(h->xev[1], h->xstream));
+    {
+        Timed t(h, np.kind);
+        CUDA_TRY(h, launch_tile(h->dtype, h->d_state, h->nl, first, h->d_subs, h->d_trots, h->d_offs, h->tile_tma,
+                                h->tile_tune, h->stream));
+    }
+    CUDA_TRY(h, cudaStreamWaitEvent(h->stream, h->xev[1], 0));
+    {
+        Timed t(h, np.kind);
+        CUDA_TRY(h, launch_tile(h->dtype, h->d_state, h->nl, second, h->d_subs, h->d_trots, h->d_offs, h->tile_tma,
+                                h->tile_tune, h->stream));
+    }
+    const double region = (double)(rows * row_amps * h->amp_bytes);
+    h->stats.nvlink_bytes += region;
+    h->stats.exchanges += 1;
+    h->stats.launches[PS_K_EXCHANGE] += 1;
+    h->stats.algo_bytes[PS_K_EXCHANGE] += region * 2.0;
+    h->stats.launches[np.kind] += 2;
+    h->stats.rotations_by[np.kind] += (uint64_t)np.rot_count;
+    h->stats.algo_bytes[np.kind] += 2.0 * (double)h->amp_bytes * (double)local_amps(h);
+    h->stats.passes += 1;
     return PS_OK;
 }
 
@@ -776,7 +867,15 @@ static int execute_plan(ps_state* h, const Plan& plan) {
     if (rc) return rc;
     const double pass_bytes = 2.0 * (double)h->amp_bytes * (double)local_amps(h);
     void* target = h->d_state;  // MIRROR_SWITCH redirects passes to the mirror buffer
-    for (const Pass& p : plan.passes) {
+    for (size_t pi = 0; pi < plan.passes.size(); ++pi) {
+        const Pass& p = plan.passes[pi];
+        const Pass* next = pi + 1 < plan.passes.size() ? &plan.passes[pi + 1] : nullptr;
+        if (p.kind == PASS_EXCHANGE && can_overlap(h, p, next)) {
+            rc = exchange_overlap(h, p, *next);
+            if (rc) return rc;
+            ++pi;  // the next pass ran inside the overlap
+            continue;
+        }
         switch (p.kind) {
         case PASS_STREAM: {
             Timed t(h, PS_K_STREAM);

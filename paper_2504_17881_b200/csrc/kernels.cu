@@ -538,7 +538,7 @@ template <typename T, int MAXT, int MINB>
 __global__ void __launch_bounds__(MAXT, MINB)
     k_coset(T* __restrict__ a, int kbits, int cbits, const __grid_constant__ BitRuns runs, const uint64_t* __restrict__ offs,
             uint64_t ntiles, const DevSub* __restrict__ subs, int nsub, const DevTRot* __restrict__ trots,
-            int l2_prefetch) {
+            int l2_prefetch, uint64_t or_mask) {
     using V2 = typename SmemAmp<T>::V;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int hbits = kbits - cbits;
@@ -551,7 +551,7 @@ __global__ void __launch_bounds__(MAXT, MINB)
     V2* g = reinterpret_cast<V2*>(a);
     const uint32_t chunk_bytes = (uint32_t)(2 * sizeof(T)) << cbits;
     for (uint64_t tau = blockIdx.x; tau < ntiles; tau += gridDim.x) {
-        const uint64_t i0 = deposit(tau, runs);
+        const uint64_t i0 = deposit(tau, runs) | or_mask;
         T vr[kSubAmps], vi[kSubAmps];
         for (int s = 0; s < nsub; ++s) {
             const SubHdr h = load_sub(subs + s, tid, kbits - kSubDim);
@@ -586,7 +586,7 @@ __global__ void __launch_bounds__(MAXT, MINB)
             if (s == 0 && (l2_prefetch & 2) && tau + gridDim.x < ntiles && (tid & 7) == 0) {
                 // per-thread L2 prefetch of the lines of this thread's next-tile coset (one lane of
                 // 8 covers a 128-B line of 16-B amplitudes)
-                const uint64_t i1 = deposit(tau + gridDim.x, runs);
+                const uint64_t i1 = deposit(tau + gridDim.x, runs) | or_mask;
 #pragma unroll
                 for (int d = 0; d < kSubAmps; ++d) {
                     const uint32_t l = sub_local(h, d);
@@ -596,7 +596,7 @@ __global__ void __launch_bounds__(MAXT, MINB)
             if (s == 0 && (l2_prefetch & 1) && tau + gridDim.x < ntiles) {
                 // this tile's loads have landed (sub_apply consumes them): warm L2 with the CTA's next
                 // tile while the rest of this one is computed and stored
-                const uint64_t i1 = deposit(tau + gridDim.x, runs);
+                const uint64_t i1 = deposit(tau + gridDim.x, runs) | or_mask;
                 for (uint32_t u = tid; u < (1u << hbits); u += blockDim.x)
                     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a + 2 * (i1 ^ soff[u])),
                                  "r"(chunk_bytes)
@@ -1048,23 +1048,28 @@ __global__ void k_permute(T* __restrict__ a, uint64_t quarter, int b1, int b2) {
     }
 }
 
-// NVLink P2P half swap: local region element e (row, col) <-> the partner's matching element
+// NVLink P2P half swap: local region element e (row, col) <-> the partner's matching element.
+// Elements are enumerated as e = t (fb < 0) or e = t with bit fb of e forced to fv (one half of
+// the region, for the swap/compute overlap), t in [t0, t1).
 template <typename T>
 __global__ void k_p2p_swap(T* __restrict__ local, T* __restrict__ peer, uint64_t row_amps, uint64_t my_off,
-                           uint64_t peer_off, uint64_t e0, uint64_t e1) {
+                           uint64_t peer_off, uint64_t t0, uint64_t t1, int fb, uint64_t fv) {
     using V2 = typename SmemAmp<T>::V;
     V2* L = reinterpret_cast<V2*>(local);
     V2* R = reinterpret_cast<V2*>(peer);
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    for (uint64_t e = e0 + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < e1; e += 2 * stride) {
-        const uint64_t e2 = e + stride;
+    auto elem = [&](uint64_t t) { return fb < 0 ? t : (insert0(t, fb) | (fv << fb)); };
+    for (uint64_t t = t0 + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < t1; t += 2 * stride) {
+        const uint64_t t2 = t + stride;
+        const uint64_t e = elem(t);
         const uint64_t row = e / row_amps, col = e - row * row_amps;
         const uint64_t li = row * 2 * row_amps + my_off + col, ri = row * 2 * row_amps + peer_off + col;
         const V2 u = L[li], v = __ldcv(&R[ri]);
         V2 u2, v2;
         uint64_t li2 = 0, ri2 = 0;
-        const bool has2 = e2 < e1;
+        const bool has2 = t2 < t1;
         if (has2) {
+            const uint64_t e2 = elem(t2);
             const uint64_t r2 = e2 / row_amps, c2 = e2 - r2 * row_amps;
             li2 = r2 * 2 * row_amps + my_off + c2;
             ri2 = r2 * 2 * row_amps + peer_off + c2;
@@ -1169,7 +1174,7 @@ cudaError_t launch_coset_k(T* a, int nl, const Pass& p, const DevSub* d_subs, co
     const unsigned grid = (unsigned)(ntiles < cap ? ntiles : cap);
     k_coset<T, MAXT, MINB><<<grid, threads, smem, s>>>(a, p.kbits, p.cbits, make_runs(p.free_mask),
                                                         d_offs + p.off_begin, ntiles, d_subs + p.sub_begin,
-                                                        p.sub_count, d_trots, l2_prefetch);
+                                                        p.sub_count, d_trots, l2_prefetch, p.or_mask);
     return cudaGetLastError();
 }
 
@@ -1351,14 +1356,14 @@ cudaError_t launch_permute(int dtype, void* a, int nl, int b1, int b2, cudaStrea
 }
 
 cudaError_t launch_p2p_swap(int dtype, void* local, void* peer, uint64_t rows, uint64_t row_amps, uint64_t my_off,
-                            uint64_t peer_off, uint64_t e0, uint64_t e1, cudaStream_t s) {
+                            uint64_t peer_off, uint64_t t0, uint64_t t1, int fb, uint64_t fv, cudaStream_t s) {
     (void)rows;
-    if (e1 <= e0) return cudaSuccess;
+    if (t1 <= t0) return cudaSuccess;
     const unsigned grid = (unsigned)num_sms() * 4;
     if (dtype == PS_C128)
-        k_p2p_swap<double><<<grid, 512, 0, s>>>((double*)local, (double*)peer, row_amps, my_off, peer_off, e0, e1);
+        k_p2p_swap<double><<<grid, 512, 0, s>>>((double*)local, (double*)peer, row_amps, my_off, peer_off, t0, t1, fb, fv);
     else
-        k_p2p_swap<float><<<grid, 512, 0, s>>>((float*)local, (float*)peer, row_amps, my_off, peer_off, e0, e1);
+        k_p2p_swap<float><<<grid, 512, 0, s>>>((float*)local, (float*)peer, row_amps, my_off, peer_off, t0, t1, fb, fv);
     return cudaGetLastError();
 }
 

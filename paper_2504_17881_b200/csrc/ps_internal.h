@@ -115,6 +115,7 @@ struct Pass {
     int cbits = 0;        // log2 contiguous chunk amplitudes
     int hbits = 0;        // number of gathered high basis vectors
     uint64_t free_mask = 0;
+    uint64_t or_mask = 0;   // bits forced into every tile base (a pass split by one free bit)
     int off_begin = 0;    // first entry of this pass's 2^hbits chunk offsets in the call's table
     int sub_begin = 0;    // first DevSub of this pass
     int sub_count = 0;
