@@ -38,7 +38,8 @@ cudaError_t launch_butterfly(int dtype, void* A, void* B, uint64_t n, int wr, in
 cudaError_t launch_recombine(int dtype, void* A, const void* B, uint64_t n, cudaStream_t s);
 cudaError_t launch_p2p_copy(int dtype, void* dst, const void* src, uint64_t n, cudaStream_t s);
 cudaError_t launch_p2p_swap(int dtype, void* local, void* peer, uint64_t rows, uint64_t row_amps, uint64_t my_off,
-                            uint64_t peer_off, uint64_t t0, uint64_t t1, int fb, uint64_t fv, cudaStream_t s);
+                            uint64_t peer_off, uint64_t t0, uint64_t t1, int fb, uint64_t fv, cudaStream_t s,
+                            int ctas);
 
 static thread_local std::string g_last_error;
 void set_last_error(const std::string& msg) { g_last_error = msg; }
@@ -95,6 +96,7 @@ struct ps_state {
     cudaStream_t xstream = nullptr;  // second stream: swaps overlapped with the next pass
     cudaEvent_t xev[2] = {nullptr, nullptr};
     int overlap = 1;
+    int swap_ctas = 32;  // CTAs of an overlapped swap (NVLink-bound; leaves SMs to the pass)
     int layout = 1, transport = 1;
     // options
     int profile = 0, fusion = 2, tile_bits = 11, vec256 = 1, max_pass_rots = 1 << 30, tile_tma = 2, chunk_bits = 0, tile_tune = 512;
@@ -458,7 +460,11 @@ extern "C" int ps_set_option(ps_handle h, int option, int64_t value) {
         h->layout = (int)value;
         break;
     case PS_OPT_TRANSPORT: h->transport = value ? 1 : 0; break;
-    case PS_OPT_OVERLAP: h->overlap = (value && h->xstream) ? 1 : 0; break;
+    case PS_OPT_OVERLAP:
+        // 0: off; 1: on (32 swap CTAs); > 1: on with that many swap CTAs
+        h->overlap = (value && h->xstream) ? 1 : 0;
+        if (value > 1) h->swap_ctas = (int)value;
+        break;
     case PS_OPT_CHUNK_BITS:
         if (value < 0 || value > 12) return fail(PS_EINVAL, "chunk bits must be 0..12 (0 = default)");
         h->chunk_bits = (int)value;
@@ -610,7 +616,7 @@ static int exchange_half(ps_state* h, const Pass& p) {
         if (rc) return rc;
         CUDA_TRY(h, launch_p2p_swap(h->dtype, h->d_state, h->peers[partner], rows, row_amps,
                                     (uint64_t)(1 - p.keep) * row_amps, (uint64_t)p.keep * row_amps, e0, e1, -1, 0,
-                                    h->stream));
+                                    h->stream, 0));
         rc = barrier(h);
         if (rc) return rc;
         h->stats.nvlink_bytes += (double)(rows * row_bytes);
@@ -660,9 +666,13 @@ static int barrier_on(ps_state* h, cudaStream_t st, int slot) {
     return PS_OK;
 }
 
+// a bit that splits the next pass's tiles into two halves whose elements all have that bit
+// fixed: a free (tile-enumeration) bit in which no two elements of one tile differ
+static uint64_t split_bits(const Pass& np) { return np.free_mask & ~np.touch_mask; }
+
 static bool can_overlap(const ps_state* h, const Pass& ex, const Pass* np) {
     return h->overlap && h->xstream && h->p2p && h->transport && !ex.full && ex.kind == PASS_EXCHANGE && np &&
-           (np->kind == PASS_TILE || np->kind == PASS_COSET) && h->tile_tma == 2 && np->free_mask != 0;
+           (np->kind == PASS_TILE || np->kind == PASS_COSET) && h->tile_tma == 2 && split_bits(*np) != 0;
 }
 
 // swap E(gx, ell) overlapped with the following tile pass: the pass is split
@@ -673,8 +683,9 @@ static int exchange_overlap(ps_state* h, const Pass& ex, const Pass& np) {
     const uint64_t rows = 1ull << (h->nl - 1 - ex.ell);
     const uint64_t row_amps = 1ull << ex.ell, total = rows * row_amps;
     const uint64_t my_off = (uint64_t)(1 - ex.keep) * row_amps, peer_off = (uint64_t)ex.keep * row_amps;
-    const bool f_is_ell = (np.free_mask >> ex.ell) & 1;
-    const int f = f_is_ell ? ex.ell : highest_bit(np.free_mask);
+    const uint64_t sb = split_bits(np);
+    const bool f_is_ell = (sb >> ex.ell) & 1;
+    const int f = f_is_ell ? ex.ell : highest_bit(sb);
     Pass first = np, second = np;
     first.free_mask = second.free_mask = np.free_mask & ~(1ull << f);
     int rc = barrier(h);  // every rank's earlier passes are done
@@ -687,14 +698,14 @@ static int exchange_overlap(ps_state* h, const Pass& ex, const Pass& np) {
         CUDA_TRY(h, cudaStreamWaitEvent(h->xstream, h->xev[0], 0));
         const uint64_t e0 = ex.keep ? total / 2 : 0, e1 = ex.keep ? total : total / 2;
         CUDA_TRY(h, launch_p2p_swap(h->dtype, h->d_state, h->peers[partner], rows, row_amps, my_off, peer_off, e0, e1,
-                                    -1, 0, h->xstream));
+                                    -1, 0, h->xstream, h->swap_ctas));
     } else {
         // element bit of f inside the region enumeration (local index = row 2^(ell+1) + half 2^ell + col)
         const int fb = f < ex.ell ? f : f - 1;
         const uint64_t half = total / 2;
         const uint64_t t0 = ex.keep ? half / 2 : 0, t1 = ex.keep ? half : half / 2;
         CUDA_TRY(h, launch_p2p_swap(h->dtype, h->d_state, h->peers[partner], rows, row_amps, my_off, peer_off, t0, t1,
-                                    fb, 0, h->stream));
+                                    fb, 0, h->stream, 0));
         rc = barrier(h);  // the f = 0 quarter is swapped on both ranks
         if (rc) return rc;
         first.or_mask = np.or_mask;
@@ -702,7 +713,7 @@ static int exchange_overlap(ps_state* h, const Pass& ex, const Pass& np) {
         CUDA_TRY(h, cudaEventRecord(h->xev[0], h->stream));
         CUDA_TRY(h, cudaStreamWaitEvent(h->xstream, h->xev[0], 0));
         CUDA_TRY(h, launch_p2p_swap(h->dtype, h->d_state, h->peers[partner], rows, row_amps, my_off, peer_off, t0, t1,
-                                    fb, 1, h->xstream));
+                                    fb, 1, h->xstream, h->swap_ctas));
     }
     rc = barrier_on(h, h->xstream, 1);
     if (rc) return rc;

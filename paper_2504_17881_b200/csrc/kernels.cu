@@ -1169,7 +1169,7 @@ cudaError_t launch_coset_k(T* a, int nl, const Pass& p, const DevSub* d_subs, co
     int occ = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_coset<T, MAXT, MINB>, threads, smem);
     if (occ < 1) occ = 1;
-    const uint64_t ntiles = 1ull << (nl - p.kbits);
+    const uint64_t ntiles = 1ull << __builtin_popcountll(p.free_mask);  // == 2^(nl - kbits) unless split
     const uint64_t cap = (uint64_t)num_sms() * (uint64_t)occ * (uint64_t)(grid_mult > 0 ? grid_mult : 1);
     const unsigned grid = (unsigned)(ntiles < cap ? ntiles : cap);
     k_coset<T, MAXT, MINB><<<grid, threads, smem, s>>>(a, p.kbits, p.cbits, make_runs(p.free_mask),
@@ -1206,7 +1206,7 @@ cudaError_t launch_coset_pf_t(T* a, int nl, const Pass& p, const DevSub* d_subs,
     int occ = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_coset_pf<T, CPASYNC>, threads, smem);
     if (occ < 1) occ = 1;
-    const uint64_t ntiles = 1ull << (nl - p.kbits);
+    const uint64_t ntiles = 1ull << __builtin_popcountll(p.free_mask);  // == 2^(nl - kbits) unless split
     const uint64_t cap = (uint64_t)num_sms() * (uint64_t)occ;
     const unsigned grid = (unsigned)(ntiles < cap ? ntiles : cap);
     k_coset_pf<T, CPASYNC><<<grid, threads, smem, s>>>(a, p.kbits, p.cbits, p.free_mask, d_offs + p.off_begin, ntiles,
@@ -1229,7 +1229,7 @@ cudaError_t launch_tile_t(T* a, int nl, const Pass& p, const DevSub* d_subs, con
     int occ = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_tile<T>, threads, smem);
     if (occ < 1) occ = 1;
-    const uint64_t ntiles = 1ull << (nl - p.kbits);
+    const uint64_t ntiles = 1ull << __builtin_popcountll(p.free_mask);  // == 2^(nl - kbits) unless split
     const uint64_t cap = (uint64_t)num_sms() * (uint64_t)occ;
     const unsigned grid = (unsigned)(ntiles < cap ? ntiles : cap);
     k_tile<T><<<grid, threads, smem, s>>>(a, p.kbits, p.cbits, p.free_mask, d_offs + p.off_begin, ntiles,
@@ -1356,10 +1356,10 @@ cudaError_t launch_permute(int dtype, void* a, int nl, int b1, int b2, cudaStrea
 }
 
 cudaError_t launch_p2p_swap(int dtype, void* local, void* peer, uint64_t rows, uint64_t row_amps, uint64_t my_off,
-                            uint64_t peer_off, uint64_t t0, uint64_t t1, int fb, uint64_t fv, cudaStream_t s) {
+                            uint64_t peer_off, uint64_t t0, uint64_t t1, int fb, uint64_t fv, cudaStream_t s, int ctas) {
     (void)rows;
     if (t1 <= t0) return cudaSuccess;
-    const unsigned grid = (unsigned)num_sms() * 4;
+    const unsigned grid = ctas > 0 ? (unsigned)ctas : (unsigned)num_sms() * 4;
     if (dtype == PS_C128)
         k_p2p_swap<double><<<grid, 512, 0, s>>>((double*)local, (double*)peer, row_amps, my_off, peer_off, t0, t1, fb, fv);
     else

@@ -310,6 +310,7 @@ static void emit_tile(const std::vector<PhysRot>& seg, size_t b, size_t e, const
         p.free_mask = lmask & ~((1ull << k) - 1);
         p.off_begin = (int)plan->offsets.size();
         plan->offsets.push_back(0);
+        p.touch_mask = (1ull << k) - 1;
         const uint64_t kmask = (1ull << k) - 1;
         std::vector<LocalRot> lr;
         for (size_t t = b; t < e; ++t)
@@ -346,11 +347,13 @@ static void emit_tile(const std::vector<PhysRot>& seg, size_t b, size_t e, const
     std::vector<uint64_t> vs = vb.v;
     std::sort(vs.begin(), vs.end(), [](uint64_t a, uint64_t bb) { return highest_bit(a) < highest_bit(bb); });
     p.off_begin = (int)plan->offsets.size();
+    p.touch_mask = cmask;
     for (uint64_t u = 0; u < (1ull << p.hbits); ++u) {
         uint64_t o = 0;
         for (int t = 0; t < p.hbits; ++t)
             if ((u >> t) & 1) o ^= vs[t];
         plan->offsets.push_back(o);
+        p.touch_mask |= o;
     }
     std::vector<LocalRot> lr;
     for (size_t t = b; t < e; ++t) {

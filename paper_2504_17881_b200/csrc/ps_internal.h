@@ -116,6 +116,7 @@ struct Pass {
     int hbits = 0;        // number of gathered high basis vectors
     uint64_t free_mask = 0;
     uint64_t or_mask = 0;   // bits forced into every tile base (a pass split by one free bit)
+    uint64_t touch_mask = 0;  // bits in which elements of one tile can differ (chunk bits | offsets)
     int off_begin = 0;    // first entry of this pass's 2^hbits chunk offsets in the call's table
     int sub_begin = 0;    // first DevSub of this pass
     int sub_count = 0;
