@@ -313,7 +313,7 @@ def run_ours(args):
     peak, peak_src = peaks()
     rotations = stats["rotations"]
     passes = max(1, stats["passes"])
-    gpu_launches = sum(stats["launches"][k] for k in ("stream", "tile", "coset"))
+    gpu_launches = sum(stats["launches"].values())  # every libps kernel family (exchanges: swap kernels / NCCL)
 
     # e2e through the public API with host buffers (pinned): H2D of the initial state + rotation
     # arrays, the layer, D2H of the norm (the step's scalar result)
