@@ -1116,6 +1116,12 @@ __global__ void k_p2p_copy(T* __restrict__ dst, const T* __restrict__ src, uint6
         d[i] = __ldcv(&r[i]);
 }
 
+int current_device() {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    return dev & 63;
+}
+
 int g_num_sms = 0;
 int num_sms() {
     if (g_num_sms == 0) {
@@ -1158,10 +1164,11 @@ template <typename T, int MAXT, int MINB>
 cudaError_t launch_coset_k(T* a, int nl, const Pass& p, const DevSub* d_subs, const DevTRot* d_trots,
                            const uint64_t* d_offs, int l2_prefetch, int grid_mult, cudaStream_t s) {
     const size_t smem = coset_off_bytes(p.kbits - p.cbits) + ((size_t)(2 * sizeof(T)) << p.kbits);
-    static bool attr_done = false;
-    if (!attr_done) {
+    static uint64_t attr_devices = 0;  // function attributes are per device
+    const int dev = current_device();
+    if (!((attr_devices >> dev) & 1)) {
         cudaFuncSetAttribute(k_coset<T, MAXT, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        attr_done = true;
+        attr_devices |= 1ull << dev;
     }
     const int threads = 1 << (p.kbits - kSubDim);
     if (threads > MAXT) return cudaErrorInvalidValue;
@@ -1195,11 +1202,11 @@ template <typename T, int CPASYNC>
 cudaError_t launch_coset_pf_t(T* a, int nl, const Pass& p, const DevSub* d_subs, const DevTRot* d_trots,
                               const uint64_t* d_offs, cudaStream_t s) {
     const size_t smem = coset_off_bytes(p.kbits - p.cbits) + 2 * ((size_t)(2 * sizeof(T)) << p.kbits);
-    static bool attr_done[2] = {false, false};
-    const int which = sizeof(T) == 8 ? 0 : 1;
-    if (!attr_done[which]) {
+    static uint64_t attr_devices = 0;
+    const int dev = current_device();
+    if (!((attr_devices >> dev) & 1)) {
         cudaFuncSetAttribute(k_coset_pf<T, CPASYNC>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        attr_done[which] = true;
+        attr_devices |= 1ull << dev;
     }
     const int threads = 1 << (p.kbits - kSubDim);
     int occ = 1;
@@ -1218,11 +1225,11 @@ cudaError_t launch_tile_t(T* a, int nl, const Pass& p, const DevSub* d_subs, con
                           const uint64_t* d_offs, cudaStream_t s) {
     const size_t stage_bytes = (size_t)(2 * sizeof(T)) << p.kbits;
     const size_t smem = stage_bytes * kStages;
-    static bool attr_done[2] = {false, false};
-    const int which = sizeof(T) == 8 ? 0 : 1;
-    if (!attr_done[which]) {
+    static uint64_t attr_devices = 0;
+    const int dev = current_device();
+    if (!((attr_devices >> dev) & 1)) {
         cudaFuncSetAttribute(k_tile<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        attr_done[which] = true;
+        attr_devices |= 1ull << dev;
     }
     const int threads = 1 << (p.kbits - kSubDim);
     int occ = 1;
