@@ -100,8 +100,8 @@ enum {
                                  loads from HBM, last stores to HBM, smem between sub-groups;
                                  0 = cp.async-prefetched double buffer; 1 = 3-stage TMA ring;
                                  3 = TMA-bulk-prefetched double buffer (A/B) */
-    PS_OPT_CHUNK_BITS = 7,    /* min log2 contiguous amplitudes per gathered chunk (0 = default:
-                                 4 for C128, 5 for C64, i.e. 256 B) */
+    PS_OPT_CHUNK_BITS = 7,    /* min log2 contiguous amplitudes per gathered chunk (0 = default 4:
+                                 256 B for C128, 128 B for C64) */
     PS_OPT_TILE_TUNE = 8,     /* register-direct tile kernel tuning bits: 0 = TMA bulk L2 prefetch of
                                  the next tile, 1-3 = register cap for 5/6/8 CTAs per SM, 4-7 =
                                  persistent-grid multiplier, 8 = per-thread L2 prefetch, 9 = L2::256B

@@ -830,7 +830,7 @@ static PlanConfig plan_config(const ps_state* h) {
     cfg.rank = h->rank;
     cfg.fusion = h->fusion;
     cfg.tile_bits = h->tile_bits;
-    cfg.min_chunk_bits = h->chunk_bits ? h->chunk_bits : (h->dtype == PS_C128 ? 4 : 5);  // >= 256-B chunks
+    cfg.min_chunk_bits = h->chunk_bits ? h->chunk_bits : 4;  // >= 16 amplitudes (256 B fp64, 128 B fp32)
     cfg.phase_bits = h->dtype == PS_C128 ? 3 : 4;      // 16-B vs 8-B shared-memory accesses
     cfg.max_pass_rots = h->max_pass_rots;
     cfg.layout = h->layout;
