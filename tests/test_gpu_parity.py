@@ -318,3 +318,16 @@ def test_rpe_eigenstate_signal():
     for m in (0, 3, 6):
         got = rpe.signal(1, H, empty, 0.4, m, 0, seed=1, init=1)
         assert abs(got - np.exp(-1j * 0.4 * 0.7 * 2 ** m)) <= 1e-12
+
+
+def test_option_validation_and_restore():
+    with P.State(10, "c128") as st:
+        for opt, bad in ((ps.OPT_FUSION, 5), (ps.OPT_TILE_BITS, 13), (ps.OPT_TILE_BITS, 3), (ps.OPT_CHUNK_BYTES, 1000),
+                         (ps.OPT_MAX_PASS_ROTS, 0), (ps.OPT_TILE_TMA, 7), (ps.OPT_LAYOUT, 3), (99, 1)):
+            with pytest.raises(P.PsError) as ei:
+                st.set_option(opt, bad)
+            assert ei.value.code == -1
+        st.init_random(SEED)
+        a0 = st.get_amplitudes()
+        st.set_option(ps.OPT_TILE_BITS, 5)  # valid options leave the state alone
+        assert np.array_equal(st.get_amplitudes(), a0)
