@@ -57,6 +57,8 @@ def parse():
     ap.add_argument("--layout", type=int, default=1, help="world > 1: 1 lazy qubit swaps, 0 runs + swap-back")
     ap.add_argument("--transport", type=int, default=1, help="world > 1: 1 NVLink P2P, 0 NCCL send/recv")
     ap.add_argument("--overlap", type=int, default=1, help="world > 1: overlap swaps with the next pass")
+    ap.add_argument("--specialize", type=int, default=0,
+                    help="tile-kernel variant: 0 generic (default), 2 specialised, 1 planner's per-pass choice")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     return ap.parse_args()
@@ -267,6 +269,7 @@ def run_ours(args):
     st.set_option(ps.OPT_LAYOUT, args.layout)
     st.set_option(ps.OPT_TRANSPORT, args.transport)
     st.set_option(ps.OPT_OVERLAP, args.overlap)
+    st.set_option(ps.OPT_SPECIALIZE, args.specialize)
     st.set_option(ps.OPT_PROFILE, 1)
     enc = layers(args, args.warmup + args.steps, world)
     rot_per_step = len(enc[0][2])
@@ -356,7 +359,7 @@ def run_ours(args):
             "data": "synthetic",
             "config": {"workload": workload_name(args), "n_qubits": args.n, "rotations_per_step": rot_per_step,
                        "fusion": args.fusion, "tile_mode": args.tile_mode, "tile_bits": args.tile_bits or 11,
-                       "layout": args.layout, "transport": args.transport, "overlap": args.overlap,
+                       "layout": args.layout, "transport": args.transport, "overlap": args.overlap, "specialize": args.specialize,
                        "parallelism": f"state sharded over {world} GPU(s) by top qubits",
                        "l2": "inputs larger than L2 (state %.1f GiB per GPU)" % (local_state / 2 ** 30)},
             "hbm_gbs": hbm_alg,

@@ -115,8 +115,14 @@ enum {
                                  recombine -- kept for A/B */
     PS_OPT_TRANSPORT = 10,    /* world > 1: 1 = NVLink P2P swap kernel on CUDA-IPC peer pointers when
                                  available (default); 0 = NCCL send/recv with staging */
-    PS_OPT_OVERLAP = 11       /* world > 1, P2P: 1 = overlap each swap with the following tile pass
+    PS_OPT_OVERLAP = 11,      /* world > 1, P2P: 1 = overlap each swap with the following tile pass
                                  on a second stream (default); 0 = serialise */
+    PS_OPT_SPECIALIZE = 12    /* tile-kernel variant: 0 = generic (default; per-pair signs at run
+                                 time), 2 = specialised (a compile-time case per (real, dx, sign
+                                 pattern): no per-pair sign flips, but 256 cases cost i-cache
+                                 misses and register shuffles), 1 = planner's per-pass choice
+                                 (specialised for passes of >= 16 rotations using <= 32 cases).
+                                 Bitwise-identical results (same operations in the same order) */
 };
 
 /* ------------------------------------------------------------------------------------------ */

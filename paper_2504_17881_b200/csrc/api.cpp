@@ -98,6 +98,7 @@ struct ps_state {
     int overlap = 1;
     int swap_ctas = 32;  // CTAs of an overlapped swap (NVLink-bound; leaves SMs to the pass)
     int layout = 1, transport = 1;
+    int specialize = 0;
     // options
     int profile = 0, fusion = 2, tile_bits = 11, vec256 = 1, max_pass_rots = 1 << 30, tile_tma = 2, chunk_bits = 0, tile_tune = 512;
     ps_stats stats{};
@@ -469,6 +470,10 @@ extern "C" int ps_set_option(ps_handle h, int option, int64_t value) {
         if (value < 0 || value > 12) return fail(PS_EINVAL, "chunk bits must be 0..12 (0 = default)");
         h->chunk_bits = (int)value;
         break;
+    case PS_OPT_SPECIALIZE:
+        if (value < 0 || value > 2) return fail(PS_EINVAL, "specialize must be 0, 1 or 2");
+        h->specialize = (int)value;
+        break;
     case PS_OPT_TILE_TMA:
         if (value < 0 || value > 3) return fail(PS_EINVAL, "tile mode must be 0..3");
         h->tile_tma = (int)value;
@@ -834,6 +839,7 @@ static PlanConfig plan_config(const ps_state* h) {
     cfg.phase_bits = h->dtype == PS_C128 ? 3 : 4;      // 16-B vs 8-B shared-memory accesses
     cfg.max_pass_rots = h->max_pass_rots;
     cfg.layout = h->layout;
+    cfg.specialize = h->specialize;
     cfg.perm = h->perm;
     return cfg;
 }

@@ -380,34 +380,105 @@ __device__ __forceinline__ void sub_rotation(T (&vr)[kSubAmps], T (&vi)[kSubAmps
     }
 }
 
-// applies the rotations [rb, rb + nr) of a sub-group to the thread's 16 registers; the next
-// record is fetched while the current one is applied
+__host__ __device__ constexpr int par4(int v) { return (v ^ (v >> 1) ^ (v >> 2) ^ (v >> 3)) & 1; }
+
+// one CFORM rotation with a compile-time pair pattern (dx = DX) and sign pattern parity(DZ & d):
+// four fused multiply-adds per pair, the signs ride on the FMA operands
+template <int REAL, int DX, int DZ, typename T>
+__device__ __forceinline__ void cform_sub(T (&vr)[kSubAmps], T (&vi)[kSubAmps], T t) {
+    if constexpr (DX == 0) {
+#pragma unroll
+        for (int d = 0; d < kSubAmps; ++d) {
+            const T b = par4(DZ & d) ? -t : t;
+            const T nr = pfma(-b, vi[d], vr[d]), ni = pfma(b, vr[d], vi[d]);
+            vr[d] = nr;
+            vi[d] = ni;
+        }
+    } else if constexpr (DX < kSubAmps) {
+        constexpr int piv = hibit(DX);
+#pragma unroll
+        for (int d = 0; d < kSubAmps; ++d) {
+            if ((d >> piv) & 1) continue;
+            const int e = d ^ DX;
+            const T b = par4(DZ & d) ? -t : t;
+            if (REAL) {
+                const T nir = pfma(-b, vr[e], vr[d]), nii = pfma(-b, vi[e], vi[d]);
+                const T njr = pfma(b, vr[d], vr[e]), nji = pfma(b, vi[d], vi[e]);
+                vr[d] = nir; vi[d] = nii; vr[e] = njr; vi[e] = nji;
+            } else {
+                const T nir = pfma(-b, vi[e], vr[d]), nii = pfma(b, vr[e], vi[d]);
+                const T njr = pfma(-b, vi[d], vr[e]), nji = pfma(b, vr[d], vi[e]);
+                vr[d] = nir; vi[d] = nii; vr[e] = njr; vi[e] = nji;
+            }
+        }
+    }
+}
+
+// case lists: Dz values whose bit highest(dx) is clear (the planner clears it)
+#define PS_LC(R, X, Z) \
+    case tr_case(R, X, Z): cform_sub<R, X, Z, T>(vr, vi, t); break;
+#define PS_LZ_P0(R, X) PS_LC(R, X, 0) PS_LC(R, X, 2) PS_LC(R, X, 4) PS_LC(R, X, 6) \
+    PS_LC(R, X, 8) PS_LC(R, X, 10) PS_LC(R, X, 12) PS_LC(R, X, 14)
+#define PS_LZ_P1(R, X) PS_LC(R, X, 0) PS_LC(R, X, 1) PS_LC(R, X, 4) PS_LC(R, X, 5) \
+    PS_LC(R, X, 8) PS_LC(R, X, 9) PS_LC(R, X, 12) PS_LC(R, X, 13)
+#define PS_LZ_P2(R, X) PS_LC(R, X, 0) PS_LC(R, X, 1) PS_LC(R, X, 2) PS_LC(R, X, 3) \
+    PS_LC(R, X, 8) PS_LC(R, X, 9) PS_LC(R, X, 10) PS_LC(R, X, 11)
+#define PS_LZ_P3(R, X) PS_LC(R, X, 0) PS_LC(R, X, 1) PS_LC(R, X, 2) PS_LC(R, X, 3) \
+    PS_LC(R, X, 4) PS_LC(R, X, 5) PS_LC(R, X, 6) PS_LC(R, X, 7)
+#define PS_LZ_ALL(R, X) PS_LZ_P3(R, X) PS_LC(R, X, 8) PS_LC(R, X, 9) PS_LC(R, X, 10) PS_LC(R, X, 11) \
+    PS_LC(R, X, 12) PS_LC(R, X, 13) PS_LC(R, X, 14) PS_LC(R, X, 15)
+#define PS_LX_LOW(R) PS_LZ_P0(R, 1) PS_LZ_P1(R, 2) PS_LZ_P1(R, 3) PS_LZ_P2(R, 4) PS_LZ_P2(R, 5) \
+    PS_LZ_P2(R, 6) PS_LZ_P2(R, 7)
+#define PS_LX_HIGH(R) PS_LZ_P3(R, 8) PS_LZ_P3(R, 9) PS_LZ_P3(R, 10) PS_LZ_P3(R, 11) PS_LZ_P3(R, 12) \
+    PS_LZ_P3(R, 13) PS_LZ_P3(R, 14) PS_LZ_P3(R, 15)
+
 template <typename T>
+__device__ __forceinline__ void cform_dispatch(T (&vr)[kSubAmps], T (&vi)[kSubAmps], uint32_t code, T t) {
+    switch (code & 0xffu) {
+        PS_LZ_ALL(0, 0)
+        PS_LX_LOW(0)
+        PS_LX_LOW(1)
+#if PS_SUBDIM >= 4
+        PS_LX_HIGH(0)
+        PS_LX_HIGH(1)
+#endif
+    default: break;
+    }
+}
+
+// applies the rotations [rb, rb + nr) of a sub-group to the thread's 16 registers; the next
+// record is fetched while the current one is applied.  SPEC = 0: generic (one switch on dx, the
+// per-pair signs from M at run time); SPEC = 1: CFORM rotations through the specialised cases.
+template <typename T, int SPEC>
 __device__ __forceinline__ void sub_apply(T (&vr)[kSubAmps], T (&vi)[kSubAmps], const DevTRot* __restrict__ trots,
                                           int rb, int nr, uint32_t r, uint64_t i0) {
     if (nr <= 0) return;
     const DevTRot* tr = trots + rb;
     uint4 h = __ldg(reinterpret_cast<const uint4*>(tr));
-    uint64_t zt = __ldg(&tr->zt);
-    double t = __ldg(&tr->t);
+    double pn = __ldg(&tr->p);
     for (int q = 0; q < nr; ++q) {
-        const uint32_t dx = h.x, M = h.y, zr = h.z, mode = h.w;
-        const uint64_t zt_c = zt;
-        const T tq = (T)t;
+        const uint32_t code = h.x, zr = h.y;
+        const uint64_t zt_c = ((uint64_t)h.w << 32) | h.z;
+        const double pc = pn;
         if (q + 1 < nr) {
             const DevTRot* tn = trots + rb + q + 1;
             h = __ldg(reinterpret_cast<const uint4*>(tn));
-            zt = __ldg(&tn->zt);
-            t = __ldg(&tn->t);
+            pn = __ldg(&tn->p);
         }
         const int s0 = par32(zr & r) ^ par64(zt_c & i0);
-        uint32_t Ms = M ^ (s0 ? 0xffffu : 0u);
-        if (mode & 4u) Ms ^= 0xffffu;
-        switch (mode & 3u) {
-        case 0: sub_rotation<0, 0, T>(vr, vi, dx, Ms, tq); break;
-        case 1: sub_rotation<1, 0, T>(vr, vi, dx, Ms, tq); break;
-        case 2: sub_rotation<0, 1, T>(vr, vi, dx, Ms, tq); break;
-        default: sub_rotation<1, 1, T>(vr, vi, dx, Ms, tq); break;
+        if (SPEC && !(code & kTrSform)) {
+            // the thread-wide sign flips t once; the per-pair signs are static
+            cform_dispatch<T>(vr, vi, code, flip((T)pc, s0));
+        } else {
+            uint32_t Ms = (code >> 16) ^ (s0 ? 0xffffu : 0u);
+            if (code & kTrNeg) Ms ^= 0xffffu;
+            const uint32_t dx = (code >> 8) & 15u;
+            switch (((code & kTrReal) ? 1u : 0u) | ((code & kTrSform) ? 2u : 0u)) {
+            case 0: sub_rotation<0, 0, T>(vr, vi, dx, Ms, (T)pc); break;
+            case 1: sub_rotation<1, 0, T>(vr, vi, dx, Ms, (T)pc); break;
+            case 2: sub_rotation<0, 1, T>(vr, vi, dx, Ms, (T)pc); break;
+            default: sub_rotation<1, 1, T>(vr, vi, dx, Ms, (T)pc); break;
+            }
         }
     }
 }
@@ -534,7 +605,7 @@ __host__ __device__ inline size_t coset_off_bytes(int hbits) {
     return ((sizeof(uint64_t) << hbits) + 127) & ~(size_t)127;
 }
 
-template <typename T, int MAXT, int MINB>
+template <typename T, int MAXT, int MINB, int SPEC>
 __global__ void __launch_bounds__(MAXT, MINB)
     k_coset(T* __restrict__ a, int kbits, int cbits, const __grid_constant__ BitRuns runs, const uint64_t* __restrict__ offs,
             uint64_t ntiles, const DevSub* __restrict__ subs, int nsub, const DevTRot* __restrict__ trots,
@@ -602,7 +673,7 @@ __global__ void __launch_bounds__(MAXT, MINB)
                                  "r"(chunk_bytes)
                                  : "memory");
             }
-            sub_apply<T>(vr, vi, trots, h.rb, h.nr, h.r, i0);
+            sub_apply<T, SPEC>(vr, vi, trots, h.rb, h.nr, h.r, i0);
             if (h.F != 1.0) sub_scale<T>(vr, vi, (T)h.F);
             if (s == nsub - 1) {
 #pragma unroll
@@ -732,7 +803,7 @@ __global__ void __launch_bounds__(kCosetThreads, 2)
                 vr[d] = v.x;
                 vi[d] = v.y;
             }
-            sub_apply<T>(vr, vi, trots, h.rb, h.nr, h.r, i0);
+            sub_apply<T, 0>(vr, vi, trots, h.rb, h.nr, h.r, i0);
             if (h.F != 1.0) sub_scale<T>(vr, vi, (T)h.F);
             if (s == nsub - 1) {
 #pragma unroll
@@ -859,7 +930,7 @@ __global__ void __launch_bounds__(kTileMaxThreads, 1)
                 vr[d] = v.x;
                 vi[d] = v.y;
             }
-            sub_apply<T>(vr, vi, trots, h.rb, h.nr, h.r, i0);
+            sub_apply<T, 0>(vr, vi, trots, h.rb, h.nr, h.r, i0);
             if (h.F != 1.0) sub_scale<T>(vr, vi, (T)h.F);
 #pragma unroll
             for (int d = 0; d < kSubAmps; ++d) {
@@ -1160,27 +1231,27 @@ cudaError_t launch_stream_t(T* a, int nl, const Pass& p, const DevRot* d_rots, c
     return cudaGetLastError();
 }
 
-template <typename T, int MAXT, int MINB>
+template <typename T, int MAXT, int MINB, int SPEC>
 cudaError_t launch_coset_k(T* a, int nl, const Pass& p, const DevSub* d_subs, const DevTRot* d_trots,
                            const uint64_t* d_offs, int l2_prefetch, int grid_mult, cudaStream_t s) {
     const size_t smem = coset_off_bytes(p.kbits - p.cbits) + ((size_t)(2 * sizeof(T)) << p.kbits);
     static uint64_t attr_devices = 0;  // function attributes are per device
     const int dev = current_device();
     if (!((attr_devices >> dev) & 1)) {
-        cudaFuncSetAttribute(k_coset<T, MAXT, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        cudaFuncSetAttribute(k_coset<T, MAXT, MINB, SPEC>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         attr_devices |= 1ull << dev;
     }
     const int threads = 1 << (p.kbits - kSubDim);
     if (threads > MAXT) return cudaErrorInvalidValue;
     int occ = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_coset<T, MAXT, MINB>, threads, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_coset<T, MAXT, MINB, SPEC>, threads, smem);
     if (occ < 1) occ = 1;
     const uint64_t ntiles = 1ull << __builtin_popcountll(p.free_mask);  // == 2^(nl - kbits) unless split
     const uint64_t cap = (uint64_t)num_sms() * (uint64_t)occ * (uint64_t)(grid_mult > 0 ? grid_mult : 1);
     const unsigned grid = (unsigned)(ntiles < cap ? ntiles : cap);
-    k_coset<T, MAXT, MINB><<<grid, threads, smem, s>>>(a, p.kbits, p.cbits, make_runs(p.free_mask),
-                                                        d_offs + p.off_begin, ntiles, d_subs + p.sub_begin,
-                                                        p.sub_count, d_trots, l2_prefetch, p.or_mask);
+    k_coset<T, MAXT, MINB, SPEC><<<grid, threads, smem, s>>>(a, p.kbits, p.cbits, make_runs(p.free_mask),
+                                                              d_offs + p.off_begin, ntiles, d_subs + p.sub_begin,
+                                                              p.sub_count, d_trots, l2_prefetch, p.or_mask);
     return cudaGetLastError();
 }
 
@@ -1189,13 +1260,17 @@ template <typename T>
 cudaError_t launch_coset_t(T* a, int nl, const Pass& p, const DevSub* d_subs, const DevTRot* d_trots,
                            const uint64_t* d_offs, int l2_prefetch, int grid_mult, int occ_sel, cudaStream_t s) {
     const int threads = 1 << (p.kbits - kSubDim);
-    if (threads <= 128 && occ_sel == 1) return launch_coset_k<T, 128, 5>(a, nl, p, d_subs, d_trots, d_offs, l2_prefetch, grid_mult, s);
-    if (threads <= 128 && occ_sel == 2) return launch_coset_k<T, 128, 6>(a, nl, p, d_subs, d_trots, d_offs, l2_prefetch, grid_mult, s);
-    if (threads <= 128 && occ_sel == 3) return launch_coset_k<T, 128, 8>(a, nl, p, d_subs, d_trots, d_offs, l2_prefetch, grid_mult, s);
+#ifndef PS_ONLY_DEFAULT  // (development builds: the default kernel only, fast to compile)
+    if (threads <= 128 && occ_sel == 1) return launch_coset_k<T, 128, 5, 0>(a, nl, p, d_subs, d_trots, d_offs, l2_prefetch, grid_mult, s);
+    if (threads <= 128 && occ_sel == 2) return launch_coset_k<T, 128, 6, 0>(a, nl, p, d_subs, d_trots, d_offs, l2_prefetch, grid_mult, s);
+    if (threads <= 128 && occ_sel == 3) return launch_coset_k<T, 128, 8, 0>(a, nl, p, d_subs, d_trots, d_offs, l2_prefetch, grid_mult, s);
+#endif
 #ifndef PS_COSET_MINB
 #define PS_COSET_MINB 2
 #endif
-    return launch_coset_k<T, kCosetThreads, PS_COSET_MINB>(a, nl, p, d_subs, d_trots, d_offs, l2_prefetch, grid_mult, s);
+    if (p.spec)
+        return launch_coset_k<T, kCosetThreads, PS_COSET_MINB, 1>(a, nl, p, d_subs, d_trots, d_offs, l2_prefetch, grid_mult, s);
+    return launch_coset_k<T, kCosetThreads, PS_COSET_MINB, 0>(a, nl, p, d_subs, d_trots, d_offs, l2_prefetch, grid_mult, s);
 }
 
 template <typename T, int CPASYNC>
@@ -1274,13 +1349,16 @@ cudaError_t launch_tile(int dtype, void* a, int nl, const Pass& p, const DevSub*
     const int l2p = (tune & 1) | ((tune >> 7) & 2) | ((tune >> 7) & 4);
     const int occ_sel = (tune >> 1) & 7;
     const int gm = ((tune >> 4) & 15) ? ((tune >> 4) & 15) : 4;
-    if (use_tma == 1) {
-        if (dtype == PS_C128) return launch_tile_t<double>((double*)a, nl, p, d_subs, d_trots, d_offs, s);
-        return launch_tile_t<float>((float*)a, nl, p, d_subs, d_trots, d_offs, s);
-    }
     if (use_tma == 2) {
         if (dtype == PS_C128) return launch_coset_t<double>((double*)a, nl, p, d_subs, d_trots, d_offs, l2p, gm, occ_sel, s);
         return launch_coset_t<float>((float*)a, nl, p, d_subs, d_trots, d_offs, l2p, gm, occ_sel, s);
+    }
+#ifdef PS_ONLY_DEFAULT
+    return cudaErrorNotSupported;
+#else
+    if (use_tma == 1) {
+        if (dtype == PS_C128) return launch_tile_t<double>((double*)a, nl, p, d_subs, d_trots, d_offs, s);
+        return launch_tile_t<float>((float*)a, nl, p, d_subs, d_trots, d_offs, s);
     }
     if (use_tma == 3) {
         if (dtype == PS_C128) return launch_coset_pf_t<double, 0>((double*)a, nl, p, d_subs, d_trots, d_offs, s);
@@ -1288,6 +1366,7 @@ cudaError_t launch_tile(int dtype, void* a, int nl, const Pass& p, const DevSub*
     }
     if (dtype == PS_C128) return launch_coset_pf_t<double, 1>((double*)a, nl, p, d_subs, d_trots, d_offs, s);
     return launch_coset_pf_t<float, 1>((float*)a, nl, p, d_subs, d_trots, d_offs, s);
+#endif
 }
 
 cudaError_t launch_full_update(int dtype, void* a, const void* stage, uint64_t base, uint64_t count, uint64_t pbase,

@@ -251,19 +251,19 @@ static void make_subgroups(const std::vector<LocalRot>& lr, int k, int phase_bit
             const int real = (e4 & 1) ? 0 : 1;            // i^0, i^2 real; i^1, i^3 imaginary
             const double ph = (e4 == 0 || e4 == 1) ? 1.0 : -1.0;  // B = s0 * ph * (1 or i)
             DevTRot tr{};
-            tr.dx = dx;
-            tr.M = M;
             tr.zr = (uint32_t)L.z;
             tr.zt = L.zt;
-            // CFORM (one sign flip per pair) unless cos is tiny; |tan| <= 1024 keeps a + t b accurate
-            // and SFORM keeps phi = pi/2 exact (R8)
-            if (std::fabs(c) >= std::ldexp(std::fabs(s0), -10)) {
-                tr.mode = (uint32_t)real;
-                tr.t = ph * (s0 / c);
+            if (std::fabs(c) >= std::ldexp(std::fabs(s0), -10) && !(dx == 0 && real)) {
+                // CFORM: f = cos(phi), cross coefficient +-t, t = ph * s0 / c, |t| <= 1024
+                tr.code = (uint32_t)tr_case(real, (int)dx, (int)dz) | (dx << 8) | (real ? kTrReal : 0u) | (M << 16);
+                tr.p = ph * (s0 / c);
+                tr.s = 0.0;
                 F *= c;
             } else {
-                tr.mode = (uint32_t)real | 2u | (ph < 0 ? 4u : 0u);
-                tr.t = c / s0;
+                // SFORM: keeps phi = pi/2 exact (R8)
+                tr.code = (dx << 8) | (real ? kTrReal : 0u) | kTrSform | (ph < 0 ? kTrNeg : 0u) | (M << 16);
+                tr.p = c / s0;
+                tr.s = 0.0;
                 F *= s0;
             }
             plan->trots.push_back(tr);
@@ -287,6 +287,34 @@ static void make_subgroups(const std::vector<LocalRot>& lr, int k, int phase_bit
             plan->subs[t].F = 1.0;
         }
     }
+}
+
+// Tile-kernel variant of a pass.  The specialised kernel removes the per-pair sign flips (a
+// compile-time case per (real, dx, sign pattern)) but its 256 cases cost instruction-cache misses
+// and register shuffles; it wins on deep passes that reuse a few cases (Trotter steps, gate
+// layers) and loses on shallow memory-bound ones.
+static void choose_spec(const PlanConfig& cfg, const Plan& plan, Pass* p) {
+    if (cfg.specialize != 1) {
+        p->spec = cfg.specialize == 2;
+        return;
+    }
+    int nrot = 0;
+    uint64_t seen[4] = {0, 0, 0, 0};
+    int distinct = 0;
+    for (int t = p->sub_begin; t < p->sub_begin + p->sub_count; ++t) {
+        const DevSub& sb = plan.subs[t];
+        for (int q = sb.rot_begin; q < sb.rot_begin + sb.nrot; ++q) {
+            const uint32_t code = plan.trots[q].code;
+            ++nrot;
+            if (code & kTrSform) continue;
+            const uint32_t c = code & 0xffu;
+            if (!((seen[c >> 6] >> (c & 63)) & 1)) {
+                seen[c >> 6] |= 1ull << (c & 63);
+                ++distinct;
+            }
+        }
+    }
+    p->spec = nrot >= kSpecMinRots && distinct <= kSpecMaxCases;
 }
 
 static void emit_tile(const std::vector<PhysRot>& seg, size_t b, size_t e, const PlanConfig& cfg,
@@ -316,6 +344,7 @@ static void emit_tile(const std::vector<PhysRot>& seg, size_t b, size_t e, const
         for (size_t t = b; t < e; ++t)
             lr.push_back({seg[t].x, seg[t].z & kmask, seg[t].z & p.free_mask, seg[t].y, seg[t].sign, seg[t].phi});
         make_subgroups(lr, k, cfg.phase_bits, plan, &p);
+        choose_spec(cfg, *plan, &p);
         plan->passes.push_back(p);
         return;
     }
@@ -374,6 +403,7 @@ static void emit_tile(const std::vector<PhysRot>& seg, size_t b, size_t e, const
         lr.push_back({xl, zl, z & p.free_mask, seg[t].y, seg[t].sign, seg[t].phi});
     }
     make_subgroups(lr, p.kbits, cfg.phase_bits, plan, &p);
+    choose_spec(cfg, *plan, &p);
     plan->passes.push_back(p);
 }
 

@@ -47,7 +47,9 @@ static_assert(sizeof(DevRot) == 48, "DevRot layout");
 // cross_coef = +-t, t = sin/cos, |t| <= 1024) and f = sign*sin(phi) otherwise (SFORM: self_coef =
 // t = cos/(sign*sin), cross_coef = +-1 or +-i), i.e. one fused multiply-add per component; the
 // product F of the factors is applied when the amplitudes leave the registers (deferred across
-// sub-groups while it stays within [2^-40, 2^40]).
+// sub-groups while it stays within [2^-40, 2^40]).  CFORM's per-pair sign pattern parity(Dz & d)
+// is a compile-time case of the kernel's switch (code bits 0-8), so its pairs carry no sign
+// flips; only the thread-wide sign (the representative's parity) flips t once per rotation.
 #ifndef PS_SUBDIM
 #define PS_SUBDIM 4
 #endif
@@ -65,19 +67,36 @@ struct DevSub {
 static_assert(sizeof(DevSub) == 56, "DevSub layout");
 
 // one rotation of a sub-group: pair (d, d xor dx) of the thread's 16 registers ("i" member: bit
-// highest(dx) of d is 0), sigma = parity(zr & r) xor parity(zt & i0) xor bit d of M, with
-// M bit d = parity(Dz & d), Dz_b = parity(Z_loc & u_b).
-//   mode bit 0 (REAL): B real (y odd) or imaginary (y even), as in DevRot
-//   mode bit 1 (SFORM): factor f = sign*sin(phi) (self coefficient t = cos/f) instead of cos(phi)
-//                       (cross coefficient t = B/f up to the factor i)
-//   mode bit 2 (NEG):   SFORM only: B/f = -1 (REAL) or -i (imaginary) instead of +1 / +i
+// highest(dx) of d is 0), sigma = parity(zr & r) xor parity(zt & i0) xor parity(Dz & d),
+// Dz_b = parity(Z_loc & u_b).
+//   code bits 0-7   CFORM case = tr_case(real, dx, Dz) (specialised kernel: a compile-time case
+//                   per (real, dx, sign pattern); dense index)
+//   code bits 8-11  dx (0: diagonal, imaginary only)
+//   code bit  12    REAL: B real (y odd) or imaginary (y even), as in DevRot
+//   code bit  13    SFORM (else CFORM)
+//   code bit  14    NEG (SFORM only): B/f = -1 (REAL) or -i (imaginary) instead of +1 / +i
+//   code bits 16-31 M, bit d = parity(Dz & d) (generic kernel: per-pair sign at run time)
+constexpr uint32_t kTrReal = 1u << 12, kTrSform = 1u << 13, kTrNeg = 1u << 14;
+#ifdef __CUDACC__
+#define PS_HD __host__ __device__
+#else
+#define PS_HD
+#endif
+constexpr int kSpecMinRots = 16, kSpecMaxCases = 32;  // planner: choose_spec (auto)
+PS_HD constexpr int tr_hibit(int v) { return v >= 8 ? 3 : v >= 4 ? 2 : v >= 2 ? 1 : 0; }
+// CFORM case index: 0..15 diagonal (imaginary) by Dz; then 8 Dz patterns (bit highest(dx)
+// removed) per (real, dx), dx = 1..15
+PS_HD constexpr int tr_case(int real, int dx, int dz) {
+    return dx == 0 ? (dz & 15)
+                   : 16 + (real * 15 + dx - 1) * 8 +
+                         ((dz & ((1 << tr_hibit(dx)) - 1)) | ((dz >> (tr_hibit(dx) + 1)) << tr_hibit(dx)));
+}
 struct DevTRot {
-    uint32_t dx;   // 0: diagonal
-    uint32_t M;
+    uint32_t code;
     uint32_t zr;   // tile-local phase mask (parity with the coset representative r)
-    uint32_t mode;
     uint64_t zt;   // phase mask on the tile-enumeration bits (parity with the tile base i0)
-    double t;      // REAL: B/f = +-t (CFORM) ; imaginary: B/f = +-i t ; SFORM: t = cos/f, B/f = +-1/+-i
+    double p;      // CFORM: t (B/f = +-t or +-i t); SFORM: t = cos/f (B/f = +-1 or +-i)
+    double s;      // unused (keeps the record 32 B)
 };
 static_assert(sizeof(DevTRot) == 32, "DevTRot layout");
 
@@ -120,6 +139,7 @@ struct Pass {
     int off_begin = 0;    // first entry of this pass's 2^hbits chunk offsets in the call's table
     int sub_begin = 0;    // first DevSub of this pass
     int sub_count = 0;
+    int spec = 0;         // 1: the specialised tile kernel (compile-time sign patterns), see planner
     // EXCHANGE
     uint64_t gx = 0;      // partner = rank xor gx
     int ell = 0;          // local pivot bit
@@ -155,6 +175,7 @@ struct PlanConfig {
     int max_pass_rots = 1 << 30;
     bool want_debug = false;
     int layout = 1;             // world > 1: 1 lazy qubit swaps (Belady), 0 runs with swap-back
+    int specialize = 0;         // tile kernel variant: 0 generic (default), 1 per-pass choice, 2 specialised
     std::vector<int> perm;      // starting layout (physical bit -> logical qubit); empty = canonical
 };
 

@@ -18,7 +18,7 @@ C128, C64 = 0, 1
 K_STREAM, K_TILE, K_COSET, K_REDUCE, K_INIT, K_EXCHANGE, K_PERMUTE, K_MIRROR = range(8)
 KERNEL_NAMES = ["stream", "tile", "coset", "reduce", "init", "exchange", "permute", "mirror"]
 OP_MIRROR_BEGIN, OP_MIRROR_SWITCH, OP_MIRROR_END = 8, 9, 10
-OPT_PROFILE, OPT_FUSION, OPT_TILE_BITS, OPT_CHUNK_BYTES, OPT_MAX_PASS_ROTS, OPT_VEC256, OPT_TILE_TMA, OPT_CHUNK_BITS, OPT_TILE_TUNE, OPT_LAYOUT, OPT_TRANSPORT, OPT_OVERLAP = range(12)
+OPT_PROFILE, OPT_FUSION, OPT_TILE_BITS, OPT_CHUNK_BYTES, OPT_MAX_PASS_ROTS, OPT_VEC256, OPT_TILE_TMA, OPT_CHUNK_BITS, OPT_TILE_TUNE, OPT_LAYOUT, OPT_TRANSPORT, OPT_OVERLAP, OPT_SPECIALIZE = range(13)
 
 
 class PsError(RuntimeError):

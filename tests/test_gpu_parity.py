@@ -32,10 +32,12 @@ def _want(n, kind, count, seed):
     return _oracle_cache[key]
 
 
-def _run(n, dtype, codes, ang, fusion=2, tile_bits=None, init="random"):
+def _run(n, dtype, codes, ang, fusion=2, tile_bits=None, init="random", specialize=None):
     x, z = P.pauli_encode_codes(codes)
     with P.State(n, dtype) as st:
         st.set_option(ps.OPT_FUSION, fusion)
+        if specialize is not None:
+            st.set_option(ps.OPT_SPECIALIZE, specialize)
         if tile_bits:
             st.set_option(ps.OPT_TILE_BITS, tile_bits)
         if init == "random":
@@ -55,6 +57,24 @@ def test_config1(dtype, fusion):
     codes, ang, want = _want(10, "R10", 200, 1)
     got, _ = _run(10, dtype, codes, ang, fusion=fusion, tile_bits=6)
     assert np.max(np.abs(got - want)) <= TOL[dtype]
+
+
+@pytest.mark.parametrize("dtype", ["c128", "c64"])
+@pytest.mark.parametrize("kind,n,count,tb", [("R10", 12, 400, 8), ("S8", 13, 640, 9), ("LOW", 12, 300, 11),
+                                             ("D", 11, 200, 7), ("R4", 14, 500, 10)])
+def test_specialised_kernel_identical(dtype, kind, n, count, tb):
+    """The specialised tile kernel (compile-time sign-pattern cases, PS_OPT_SPECIALIZE=2) performs
+    the same operations as the generic one: bitwise-identical results, both at the oracle.  A
+    quarter of the angles sit at +-pi/2 or +-pi/4 so SFORM and CFORM records mix in one pass."""
+    codes, ang, _ = _want(n, kind, count, 7)
+    ang = ang.copy()
+    rng = np.random.default_rng(5)
+    pick = rng.random(count) < 0.25
+    ang[pick] = rng.choice([np.pi / 2, -np.pi / 2, np.pi / 4, -3 * np.pi / 4], size=int(pick.sum()))
+    want = oracle.apply(n, oracle.random_state(SEED, n), codes, ang)
+    outs = [_run(n, dtype, codes, ang, tile_bits=tb, specialize=sp)[0] for sp in (0, 1, 2)]
+    assert np.array_equal(outs[0], outs[2]) and np.array_equal(outs[0], outs[1])
+    assert np.max(np.abs(outs[2] - want)) <= TOL[dtype]
 
 
 @pytest.mark.parametrize("n", [1, 2, 3, 5, 8, 11, 14, 17])
@@ -323,7 +343,7 @@ def test_rpe_eigenstate_signal():
 def test_option_validation_and_restore():
     with P.State(10, "c128") as st:
         for opt, bad in ((ps.OPT_FUSION, 5), (ps.OPT_TILE_BITS, 13), (ps.OPT_TILE_BITS, 3), (ps.OPT_CHUNK_BYTES, 1000),
-                         (ps.OPT_MAX_PASS_ROTS, 0), (ps.OPT_TILE_TMA, 7), (ps.OPT_LAYOUT, 3), (99, 1)):
+                         (ps.OPT_MAX_PASS_ROTS, 0), (ps.OPT_TILE_TMA, 7), (ps.OPT_LAYOUT, 3), (ps.OPT_SPECIALIZE, 3), (99, 1)):
             with pytest.raises(P.PsError) as ei:
                 st.set_option(opt, bad)
             assert ei.value.code == -1
