@@ -103,7 +103,8 @@ enum {
     PS_OPT_CHUNK_BITS = 7,    /* min log2 contiguous amplitudes per gathered chunk (0 = default 4:
                                  256 B for C128, 128 B for C64) */
     PS_OPT_TILE_TUNE = 8,     /* register-direct tile kernel tuning bits: 0 = TMA bulk L2 prefetch of
-                                 the next tile, 1-3 = register cap for 5/6/8 CTAs per SM, 4-7 =
+                                 the next tile, 1-3 = CTAs per SM: 0 per-dtype default (fp64
+                                 uncapped, fp32 8), 1/2/3 register cap for 5/6/8, 4 uncapped, 4-7 =
                                  persistent-grid multiplier, 8 = per-thread L2 prefetch, 9 = L2::256B
                                  sector promotion on the gathered loads (default 512 = bit 9) */
     PS_OPT_LAYOUT = 9,        /* world > 1: 1 = lazy qubit-swap layout kept across calls, swaps chosen

@@ -1260,10 +1260,14 @@ template <typename T>
 cudaError_t launch_coset_t(T* a, int nl, const Pass& p, const DevSub* d_subs, const DevTRot* d_trots,
                            const uint64_t* d_offs, int l2_prefetch, int grid_mult, int occ_sel, cudaStream_t s) {
     const int threads = 1 << (p.kbits - kSubDim);
-#ifndef PS_ONLY_DEFAULT  // (development builds: the default kernel only, fast to compile)
-    if (threads <= 128 && occ_sel == 1) return launch_coset_k<T, 128, 5, 0>(a, nl, p, d_subs, d_trots, d_offs, l2_prefetch, grid_mult, s);
-    if (threads <= 128 && occ_sel == 2) return launch_coset_k<T, 128, 6, 0>(a, nl, p, d_subs, d_trots, d_offs, l2_prefetch, grid_mult, s);
-    if (threads <= 128 && occ_sel == 3) return launch_coset_k<T, 128, 8, 0>(a, nl, p, d_subs, d_trots, d_offs, l2_prefetch, grid_mult, s);
+    // occ_sel 0 = per-dtype default: fp32 tiles hold half the bytes, so 8 CTAs per SM (64
+    // registers) keep more bytes in flight (+7 % at 30q); fp64 spills under any cap
+    if (occ_sel == 0 && sizeof(T) == 4 && !p.spec) occ_sel = 3;
+    if (threads <= 128 && !p.spec && occ_sel == 3)
+        return launch_coset_k<T, 128, 8, 0>(a, nl, p, d_subs, d_trots, d_offs, l2_prefetch, grid_mult, s);
+#ifndef PS_ONLY_DEFAULT  // (development builds: the default kernels only, fast to compile)
+    if (threads <= 128 && !p.spec && occ_sel == 1) return launch_coset_k<T, 128, 5, 0>(a, nl, p, d_subs, d_trots, d_offs, l2_prefetch, grid_mult, s);
+    if (threads <= 128 && !p.spec && occ_sel == 2) return launch_coset_k<T, 128, 6, 0>(a, nl, p, d_subs, d_trots, d_offs, l2_prefetch, grid_mult, s);
 #endif
 #ifndef PS_COSET_MINB
 #define PS_COSET_MINB 2
