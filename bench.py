@@ -179,12 +179,17 @@ def peaks():
         return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def traffic_for(kernel: str):
-    """dram bytes per launch from the committed ncu --set full summary, if any."""
+def traffic_for(kernel: str, bytes_per_launch: float, dtype: str):
+    """dram bytes per launch from the committed ncu --set full summary, when that capture was of a
+    launch of the same size and dtype as this run's (else null: per-launch traffic of another
+    configuration says nothing about this one)."""
     path = os.path.join(ROOT, "profiles", "traffic.json")
     try:
         with open(path) as fh:
             d = json.load(fh)
+        alg = float(d[kernel + "_algorithmic"])
+        if d.get(kernel + "_dtype") != dtype or abs(bytes_per_launch - alg) > 0.01 * alg:
+            return None
         return d.get(kernel)
     except Exception:
         return None
@@ -374,7 +379,8 @@ def run_ours(args):
             "roofline": {"bound": "hbm", "kernel": fam, "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "peak_source": peak_src,
                          "algorithmic_bytes_per_launch": bytes_per_launch,
-                         "avg_launch_ms": kms / launches, "traffic": traffic_for(fam)},
+                         "avg_launch_ms": kms / launches,
+                         "traffic": traffic_for(fam, bytes_per_launch, args.dtype)},
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": gpu_launches,

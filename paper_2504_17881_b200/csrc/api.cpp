@@ -38,8 +38,8 @@ cudaError_t launch_butterfly(int dtype, void* A, void* B, uint64_t n, int wr, in
 cudaError_t launch_recombine(int dtype, void* A, const void* B, uint64_t n, cudaStream_t s);
 cudaError_t launch_p2p_copy(int dtype, void* dst, const void* src, uint64_t n, cudaStream_t s);
 cudaError_t launch_p2p_swap(int dtype, void* local, void* peer, uint64_t rows, uint64_t row_amps, uint64_t my_off,
-                            uint64_t peer_off, uint64_t t0, uint64_t t1, int fb, uint64_t fv, cudaStream_t s,
-                            int ctas);
+                            uint64_t peer_off, uint64_t t0, uint64_t t1, uint64_t fmask, uint64_t fval,
+                            cudaStream_t s, int ctas);
 
 static thread_local std::string g_last_error;
 void set_last_error(const std::string& msg) { g_last_error = msg; }
@@ -94,9 +94,11 @@ struct ps_state {
     bool p2p = false;
     void* d_mirror = nullptr;  // PS_OPT_LAYOUT=2 mirror buffer B_k
     cudaStream_t xstream = nullptr;  // second stream: swaps overlapped with the next pass
-    cudaEvent_t xev[2] = {nullptr, nullptr};
+    static constexpr int kXev = 9;
+    cudaEvent_t xev[kXev] = {};
     int overlap = 1;
-    int swap_ctas = 32;  // CTAs of an overlapped swap (NVLink-bound; leaves SMs to the pass)
+    int swap_ctas = 32;   // CTAs of an overlapped swap (NVLink-bound; leaves SMs to the pass)
+    int piece_bits = 2;   // an overlapped swap/pass pair runs in up to 2^piece_bits pieces
     int layout = 1, transport = 1;
     int specialize = 0;
     // options
@@ -218,7 +220,7 @@ static void free_state(ps_state* h) {
     if (h->d_barrier) cudaFree(h->d_barrier);
     if (h->d_mirror) cudaFree(h->d_mirror);
     if (h->xstream) cudaStreamDestroy(h->xstream);
-    for (int t = 0; t < 2; ++t)
+    for (int t = 0; t < ps_state::kXev; ++t)
         if (h->xev[t]) cudaEventDestroy(h->xev[t]);
     if (h->comm) ncclCommDestroy(h->comm);
     for (int t = 0; t < 2; ++t) {
@@ -309,9 +311,14 @@ static void setup_p2p(ps_state* h) {
         h->p2p = agree == 1;
     cudaMemsetAsync(d_flag, 0, sizeof(int), h->stream);
     if (h->p2p) {
-        if (cudaStreamCreateWithFlags(&h->xstream, cudaStreamNonBlocking) != cudaSuccess ||
-            cudaEventCreateWithFlags(&h->xev[0], cudaEventDisableTiming) != cudaSuccess ||
-            cudaEventCreateWithFlags(&h->xev[1], cudaEventDisableTiming) != cudaSuccess) {
+        // high priority: swap (and barrier) CTAs are dispatched ahead of the pending CTAs of the
+        // persistent tile grid they overlap with
+        int lo_prio = 0, hi_prio = 0;
+        cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio);
+        bool ok = cudaStreamCreateWithPriority(&h->xstream, cudaStreamNonBlocking, hi_prio) == cudaSuccess;
+        for (int t = 0; ok && t < ps_state::kXev; ++t)
+            ok = cudaEventCreateWithFlags(&h->xev[t], cudaEventDisableTiming) == cudaSuccess;
+        if (!ok) {
             cudaGetLastError();
             h->overlap = 0;
         }
@@ -463,8 +470,10 @@ extern "C" int ps_set_option(ps_handle h, int option, int64_t value) {
     case PS_OPT_TRANSPORT: h->transport = value ? 1 : 0; break;
     case PS_OPT_OVERLAP:
         // 0: off; 1: on (32 swap CTAs); > 1: on with that many swap CTAs
+        // 0: off; 1: on; > 1: on, bits 0-15 = swap CTAs (if > 1), bits 16-18 = piece bits + 1
         h->overlap = (value && h->xstream) ? 1 : 0;
-        if (value > 1) h->swap_ctas = (int)value;
+        if ((value & 0xffff) > 1) h->swap_ctas = (int)(value & 0xffff);
+        if ((value >> 16) & 7) h->piece_bits = (int)((value >> 16) & 7) - 1;
         break;
     case PS_OPT_CHUNK_BITS:
         if (value < 0 || value > 12) return fail(PS_EINVAL, "chunk bits must be 0..12 (0 = default)");
@@ -620,7 +629,7 @@ static int exchange_half(ps_state* h, const Pass& p) {
         int rc = barrier(h);
         if (rc) return rc;
         CUDA_TRY(h, launch_p2p_swap(h->dtype, h->d_state, h->peers[partner], rows, row_amps,
-                                    (uint64_t)(1 - p.keep) * row_amps, (uint64_t)p.keep * row_amps, e0, e1, -1, 0,
+                                    (uint64_t)(1 - p.keep) * row_amps, (uint64_t)p.keep * row_amps, e0, e1, 0, 0,
                                     h->stream, 0));
         rc = barrier(h);
         if (rc) return rc;
@@ -680,9 +689,12 @@ static bool can_overlap(const ps_state* h, const Pass& ex, const Pass* np) {
            (np->kind == PASS_TILE || np->kind == PASS_COSET) && h->tile_tma == 2 && split_bits(*np) != 0;
 }
 
-// swap E(gx, ell) overlapped with the following tile pass: the pass is split
-// by one of its free bits f; the half of its tiles that needs no (or only the already swapped)
-// data runs on the main stream while the second stream swaps the rest
+// swap E(gx, ell) overlapped with the following tile pass.  The pass is
+// split into P = 2^B pieces by B of its free bits outside its tile space (so every tile lies in one
+// piece); the region of the swap splits by the same bits.  The second stream swaps piece after
+// piece (each closed by a barrier: both ranks' halves have landed) while the main stream runs
+// each pass piece as soon as its data is in place.  If ell itself is such a bit, the tiles on the
+// kept side need no swapped data and run during the whole swap.
 static int exchange_overlap(ps_state* h, const Pass& ex, const Pass& np) {
     const int partner = h->rank ^ (int)ex.gx;
     const uint64_t rows = 1ull << (h->nl - 1 - ex.ell);
@@ -690,56 +702,84 @@ static int exchange_overlap(ps_state* h, const Pass& ex, const Pass& np) {
     const uint64_t my_off = (uint64_t)(1 - ex.keep) * row_amps, peer_off = (uint64_t)ex.keep * row_amps;
     const uint64_t sb = split_bits(np);
     const bool f_is_ell = (sb >> ex.ell) & 1;
-    const int f = f_is_ell ? ex.ell : highest_bit(sb);
-    Pass first = np, second = np;
-    first.free_mask = second.free_mask = np.free_mask & ~(1ull << f);
+    uint64_t pbits = 0;  // piece bits (local positions): the highest split bits other than ell
+    int B = 0;
+    for (int b = 63; b >= 0 && B < h->piece_bits; --b)
+        if (((sb >> b) & 1) && b != ex.ell) {
+            pbits |= 1ull << b;
+            ++B;
+        }
+    if (!f_is_ell && B == 0) return fail(PS_EUNSUPPORTED, "overlap without a split bit");  // can_overlap excludes it
+    const int P = 1 << B;
+    // local bit f -> bit of the region element index (bit ell removed)
+    auto elem_bits = [&](uint64_t m) {
+        uint64_t r = 0;
+        for (; m; m &= m - 1) {
+            const int f = __builtin_ctzll(m);
+            r |= 1ull << (f < ex.ell ? f : f - 1);
+        }
+        return r;
+    };
+    auto deposit = [](uint64_t v, uint64_t mask) {
+        uint64_t r = 0;
+        for (; mask; mask &= mask - 1, v >>= 1)
+            if (v & 1) r |= mask & (~mask + 1);
+        return r;
+    };
+    const uint64_t emask = elem_bits(pbits);
+    const uint64_t piece = total >> B;  // elements per piece; each rank swaps half of them
+    const uint64_t t0 = ex.keep ? piece / 2 : 0, t1 = ex.keep ? piece : piece / 2;
+    auto swap_piece = [&](int j, cudaStream_t st, int ctas) {
+        return launch_p2p_swap(h->dtype, h->d_state, h->peers[partner], rows, row_amps, my_off, peer_off, t0, t1,
+                               emask, deposit((uint64_t)j, emask), st, ctas);
+    };
+    auto run_pass = [&](uint64_t fixed_mask, uint64_t fixed_val) -> int {
+        Pass q = np;
+        q.free_mask = np.free_mask & ~fixed_mask;
+        q.or_mask = np.or_mask | fixed_val;
+        Timed t(h, np.kind);
+        CUDA_TRY(h, launch_tile(h->dtype, h->d_state, h->nl, q, h->d_subs, h->d_trots, h->d_offs, h->tile_tma,
+                                h->tile_tune, h->stream));
+        return PS_OK;
+    };
     int rc = barrier(h);  // every rank's earlier passes are done
     if (rc) return rc;
-    if (f_is_ell) {
-        // tiles on the kept side (bit ell == keep) touch no swapped slot
-        first.or_mask = np.or_mask | ((uint64_t)ex.keep << f);
-        second.or_mask = np.or_mask | ((uint64_t)(1 - ex.keep) << f);
-        CUDA_TRY(h, cudaEventRecord(h->xev[0], h->stream));
-        CUDA_TRY(h, cudaStreamWaitEvent(h->xstream, h->xev[0], 0));
-        const uint64_t e0 = ex.keep ? total / 2 : 0, e1 = ex.keep ? total : total / 2;
-        CUDA_TRY(h, launch_p2p_swap(h->dtype, h->d_state, h->peers[partner], rows, row_amps, my_off, peer_off, e0, e1,
-                                    -1, 0, h->xstream, h->swap_ctas));
-    } else {
-        // element bit of f inside the region enumeration (local index = row 2^(ell+1) + half 2^ell + col)
-        const int fb = f < ex.ell ? f : f - 1;
-        const uint64_t half = total / 2;
-        const uint64_t t0 = ex.keep ? half / 2 : 0, t1 = ex.keep ? half : half / 2;
-        CUDA_TRY(h, launch_p2p_swap(h->dtype, h->d_state, h->peers[partner], rows, row_amps, my_off, peer_off, t0, t1,
-                                    fb, 0, h->stream, 0));
-        rc = barrier(h);  // the f = 0 quarter is swapped on both ranks
+    int launches = 0;
+    const int first = f_is_ell ? 0 : 1;
+    if (!f_is_ell) {
+        // piece 0 is swapped with the whole GPU before anything can run
+        CUDA_TRY(h, swap_piece(0, h->stream, 0));
+        rc = barrier(h);
         if (rc) return rc;
-        first.or_mask = np.or_mask;
-        second.or_mask = np.or_mask | (1ull << f);
-        CUDA_TRY(h, cudaEventRecord(h->xev[0], h->stream));
-        CUDA_TRY(h, cudaStreamWaitEvent(h->xstream, h->xev[0], 0));
-        CUDA_TRY(h, launch_p2p_swap(h->dtype, h->d_state, h->peers[partner], rows, row_amps, my_off, peer_off, t0, t1,
-                                    fb, 1, h->xstream, h->swap_ctas));
     }
-    rc = barrier_on(h, h->xstream, 1);
-    if (rc) return rc;
-    CUDA_TRY(h, cudaEventRecord(h->xev[1], h->xstream));
-    {
-        Timed t(h, np.kind);
-        CUDA_TRY(h, launch_tile(h->dtype, h->d_state, h->nl, first, h->d_subs, h->d_trots, h->d_offs, h->tile_tma,
-                                h->tile_tune, h->stream));
+    CUDA_TRY(h, cudaEventRecord(h->xev[0], h->stream));
+    CUDA_TRY(h, cudaStreamWaitEvent(h->xstream, h->xev[0], 0));
+    for (int j = first; j < P; ++j) {
+        CUDA_TRY(h, swap_piece(j, h->xstream, h->swap_ctas));
+        rc = barrier_on(h, h->xstream, 1);
+        if (rc) return rc;
+        CUDA_TRY(h, cudaEventRecord(h->xev[1 + j], h->xstream));
     }
-    CUDA_TRY(h, cudaStreamWaitEvent(h->stream, h->xev[1], 0));
-    {
-        Timed t(h, np.kind);
-        CUDA_TRY(h, launch_tile(h->dtype, h->d_state, h->nl, second, h->d_subs, h->d_trots, h->d_offs, h->tile_tma,
-                                h->tile_tune, h->stream));
+    const uint64_t lbit = 1ull << ex.ell;
+    if (f_is_ell) {
+        rc = run_pass(lbit, (uint64_t)ex.keep << ex.ell);  // kept side: no swapped slot
+        if (rc) return rc;
+        ++launches;
+    }
+    for (int j = 0; j < P; ++j) {
+        if (j >= first) CUDA_TRY(h, cudaStreamWaitEvent(h->stream, h->xev[1 + j], 0));
+        const uint64_t fm = pbits | (f_is_ell ? lbit : 0);
+        const uint64_t fv = deposit((uint64_t)j, pbits) | (f_is_ell ? (uint64_t)(1 - ex.keep) << ex.ell : 0);
+        rc = run_pass(fm, fv);
+        if (rc) return rc;
+        ++launches;
     }
     const double region = (double)(rows * row_amps * h->amp_bytes);
     h->stats.nvlink_bytes += region;
     h->stats.exchanges += 1;
     h->stats.launches[PS_K_EXCHANGE] += 1;
     h->stats.algo_bytes[PS_K_EXCHANGE] += region * 2.0;
-    h->stats.launches[np.kind] += 2;
+    h->stats.launches[np.kind] += (uint64_t)launches;
     h->stats.rotations_by[np.kind] += (uint64_t)np.rot_count;
     h->stats.algo_bytes[np.kind] += 2.0 * (double)h->amp_bytes * (double)local_amps(h);
     h->stats.passes += 1;

@@ -1124,7 +1124,7 @@ __global__ void k_permute(T* __restrict__ a, uint64_t quarter, int b1, int b2) {
 // the region, for the swap/compute overlap), t in [t0, t1).
 template <typename T>
 __global__ void k_p2p_swap(T* __restrict__ local, T* __restrict__ peer, uint64_t row_amps, uint64_t my_off,
-                           uint64_t peer_off, uint64_t t0, uint64_t t1, int fb, uint64_t fv) {
+                           uint64_t peer_off, uint64_t t0, uint64_t t1, uint64_t fmask, uint64_t fval) {
     using V2 = typename SmemAmp<T>::V;
     constexpr int U = 8;  // elements in flight per thread (NVLink latency ~2 us)
     V2* L = reinterpret_cast<V2*>(local);
@@ -1136,7 +1136,12 @@ __global__ void k_p2p_swap(T* __restrict__ local, T* __restrict__ peer, uint64_t
 #pragma unroll
         for (int q = 0; q < U; ++q) {
             const uint64_t tq = t + (uint64_t)q * stride;
-            const uint64_t e = fb < 0 ? tq : (insert0(tq, fb) | (fv << fb));
+            // element index: tq with the filter bits (fmask, fval) inserted, lowest first
+            uint64_t e = tq;
+            for (uint64_t m = fmask; m; m &= m - 1) {
+                const int b = __ffsll((long long)m) - 1;
+                e = insert0(e, b) | (fval & (1ull << b));
+            }
             const uint64_t row = e / row_amps, col = e - row * row_amps;
             li[q] = row * 2 * row_amps + my_off + col;
             ri[q] = row * 2 * row_amps + peer_off + col;
@@ -1445,14 +1450,15 @@ cudaError_t launch_permute(int dtype, void* a, int nl, int b1, int b2, cudaStrea
 }
 
 cudaError_t launch_p2p_swap(int dtype, void* local, void* peer, uint64_t rows, uint64_t row_amps, uint64_t my_off,
-                            uint64_t peer_off, uint64_t t0, uint64_t t1, int fb, uint64_t fv, cudaStream_t s, int ctas) {
+                            uint64_t peer_off, uint64_t t0, uint64_t t1, uint64_t fmask, uint64_t fval, cudaStream_t s,
+                            int ctas) {
     (void)rows;
     if (t1 <= t0) return cudaSuccess;
     const unsigned grid = ctas > 0 ? (unsigned)ctas : (unsigned)num_sms();
     if (dtype == PS_C128)
-        k_p2p_swap<double><<<grid, 512, 0, s>>>((double*)local, (double*)peer, row_amps, my_off, peer_off, t0, t1, fb, fv);
+        k_p2p_swap<double><<<grid, 512, 0, s>>>((double*)local, (double*)peer, row_amps, my_off, peer_off, t0, t1, fmask, fval);
     else
-        k_p2p_swap<float><<<grid, 512, 0, s>>>((float*)local, (float*)peer, row_amps, my_off, peer_off, t0, t1, fb, fv);
+        k_p2p_swap<float><<<grid, 512, 0, s>>>((float*)local, (float*)peer, row_amps, my_off, peer_off, t0, t1, fmask, fval);
     return cudaGetLastError();
 }
 
