@@ -94,7 +94,7 @@ enum {
     PS_OPT_FUSION = 1,        /* 0: one rotation per pass (K1 only); 1: same-x runs; 2: + tiles (default 2) */
     PS_OPT_TILE_BITS = 2,     /* log2 amplitudes per fused tile, 4..12 (default 11) */
     PS_OPT_CHUNK_BYTES = 3,   /* exchange chunk size in bytes (default 256 MiB) */
-    PS_OPT_MAX_PASS_ROTS = 4, /* cap on rotations fused into one tile pass (default 64) */
+    PS_OPT_MAX_PASS_ROTS = 4, /* cap on rotations fused into one tile pass (default: no cap) */
     PS_OPT_VEC256 = 5,        /* 1: 256-bit LDG/STG in K1 (default 1); 0: 128-bit */
     PS_OPT_TILE_TMA = 6,      /* tile-pass kernel: 2 = register-direct (default): first sub-group
                                  loads from HBM, last stores to HBM, smem between sub-groups;
@@ -106,7 +106,9 @@ enum {
                                  the next tile, 1-3 = CTAs per SM: 0 per-dtype default (fp64
                                  uncapped, fp32 8), 1/2/3 register cap for 5/6/8, 4 uncapped, 4-7 =
                                  persistent-grid multiplier, 8 = per-thread L2 prefetch, 9 = L2::256B
-                                 sector promotion on the gathered loads (default 512 = bit 9) */
+                                 sector promotion on the gathered loads, 10 = the pass's records
+                                 in the launch's parameter block (uniform constant-bank loads;
+                                 passes of <= 64 rotations) (default 1536 = bits 9 + 10) */
     PS_OPT_LAYOUT = 9,        /* world > 1: 1 = lazy qubit-swap layout kept across calls, swaps chosen
                                  by furthest next use (default); 0 = one half-vector exchange per run
                                  sharing the upper X-part, swapped back at once (Eq. (1) economy);

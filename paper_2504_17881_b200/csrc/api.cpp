@@ -22,7 +22,8 @@ int kernel_max_red_blocks();
 cudaError_t launch_stream(int dtype, void* a, int nl, const Pass& p, const DevRot* d_rots, int vec256,
                           cudaStream_t s);
 cudaError_t launch_tile(int dtype, void* a, int nl, const Pass& p, const DevSub* d_subs, const DevTRot* d_trots,
-                        const uint64_t* d_offs, int use_tma, int tune, cudaStream_t s);
+                        const uint64_t* d_offs, int use_tma, int tune, cudaStream_t s, const DevSub* h_subs,
+                        const DevTRot* h_trots);
 cudaError_t launch_full_update(int dtype, void* a, const void* stage, uint64_t base, uint64_t count, uint64_t pbase,
                                const DevRot* rec, cudaStream_t s);
 cudaError_t launch_norm(int dtype, const void* a, uint64_t n, double* d_partial, double* d_out, cudaStream_t s);
@@ -99,10 +100,11 @@ struct ps_state {
     int overlap = 1;
     int swap_ctas = 32;   // CTAs of an overlapped swap (NVLink-bound; leaves SMs to the pass)
     int piece_bits = 2;   // an overlapped swap/pass pair runs in up to 2^piece_bits pieces
+    const Plan* cur_plan = nullptr;  // the plan being executed (host copies of its records)
     int layout = 1, transport = 1;
     int specialize = 0;
     // options
-    int profile = 0, fusion = 2, tile_bits = 11, vec256 = 1, max_pass_rots = 1 << 30, tile_tma = 2, chunk_bits = 0, tile_tune = 512;
+    int profile = 0, fusion = 2, tile_bits = 11, vec256 = 1, max_pass_rots = 1 << 30, tile_tma = 2, chunk_bits = 0, tile_tune = 1536;
     ps_stats stats{};
     std::vector<PendingTiming> pending;
     std::vector<cudaEvent_t> event_pool;
@@ -739,7 +741,7 @@ static int exchange_overlap(ps_state* h, const Pass& ex, const Pass& np) {
         q.or_mask = np.or_mask | fixed_val;
         Timed t(h, np.kind);
         CUDA_TRY(h, launch_tile(h->dtype, h->d_state, h->nl, q, h->d_subs, h->d_trots, h->d_offs, h->tile_tma,
-                                h->tile_tune, h->stream));
+                                h->tile_tune, h->stream, h->cur_plan->subs.data(), h->cur_plan->trots.data()));
         return PS_OK;
     };
     int rc = barrier(h);  // every rank's earlier passes are done
@@ -922,6 +924,7 @@ static int mirror_begin(ps_state* h, const Pass& p) {
 static int execute_plan(ps_state* h, const Plan& plan) {
     int rc = upload_plan(h, plan);
     if (rc) return rc;
+    h->cur_plan = &plan;
     const double pass_bytes = 2.0 * (double)h->amp_bytes * (double)local_amps(h);
     void* target = h->d_state;  // MIRROR_SWITCH redirects passes to the mirror buffer
     for (size_t pi = 0; pi < plan.passes.size(); ++pi) {
@@ -943,7 +946,7 @@ static int execute_plan(ps_state* h, const Plan& plan) {
         case PASS_COSET: {
             Timed t(h, p.kind);
             CUDA_TRY(h, launch_tile(h->dtype, target, h->nl, p, h->d_subs, h->d_trots, h->d_offs, h->tile_tma,
-                                    h->tile_tune, h->stream));
+                                    h->tile_tune, h->stream, plan.subs.data(), plan.trots.data()));
             break;
         }
         case PASS_MIRROR_BEGIN:

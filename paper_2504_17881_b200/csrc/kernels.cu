@@ -281,6 +281,14 @@ __global__ void __launch_bounds__(kStreamThreads) k_stream(T* __restrict__ a, ui
 // each component update is one fused multiply-add; F = product of the factors is applied when
 // the amplitudes leave the registers.
 
+// record loads: read-only global (__ldg) or the kernel's parameter block (PARAM = 1: uniform
+// constant-bank loads)
+template <int PARAM, typename U>
+__device__ __forceinline__ U ldr(const U* p) {
+    if constexpr (PARAM) return *p;
+    else return __ldg(p);
+}
+
 __host__ __device__ constexpr int hibit(int v) { return v >= 8 ? 3 : v >= 4 ? 2 : v >= 2 ? 1 : 0; }
 
 // SFORM = 0: a'_i = a_i + s*Ac a_j, a'_j = a_j + s*Bc a_i with Bc = t (REAL) or i t, Ac = -conj(Bc)
@@ -449,21 +457,21 @@ __device__ __forceinline__ void cform_dispatch(T (&vr)[kSubAmps], T (&vi)[kSubAm
 // applies the rotations [rb, rb + nr) of a sub-group to the thread's 16 registers; the next
 // record is fetched while the current one is applied.  SPEC = 0: generic (one switch on dx, the
 // per-pair signs from M at run time); SPEC = 1: CFORM rotations through the specialised cases.
-template <typename T, int SPEC>
+template <typename T, int SPEC, int PARAM = 0>
 __device__ __forceinline__ void sub_apply(T (&vr)[kSubAmps], T (&vi)[kSubAmps], const DevTRot* __restrict__ trots,
                                           int rb, int nr, uint32_t r, uint64_t i0) {
     if (nr <= 0) return;
     const DevTRot* tr = trots + rb;
-    uint4 h = __ldg(reinterpret_cast<const uint4*>(tr));
-    double pn = __ldg(&tr->p);
+    uint4 h = ldr<PARAM>(reinterpret_cast<const uint4*>(tr));
+    double pn = ldr<PARAM>(&tr->p);
     for (int q = 0; q < nr; ++q) {
         const uint32_t code = h.x, zr = h.y;
         const uint64_t zt_c = ((uint64_t)h.w << 32) | h.z;
         const double pc = pn;
         if (q + 1 < nr) {
             const DevTRot* tn = trots + rb + q + 1;
-            h = __ldg(reinterpret_cast<const uint4*>(tn));
-            pn = __ldg(&tn->p);
+            h = ldr<PARAM>(reinterpret_cast<const uint4*>(tn));
+            pn = ldr<PARAM>(&tn->p);
         }
         const int s0 = par32(zr & r) ^ par64(zt_c & i0);
         if (SPEC && !(code & kTrSform)) {
@@ -499,17 +507,18 @@ struct SubHdr {
     double F;
 };
 
+template <int PARAM = 0>
 __device__ __forceinline__ SubHdr load_sub(const DevSub* __restrict__ sp, uint32_t tid, int ncols) {
     SubHdr h;
 #pragma unroll
-    for (int b = 0; b < kSubDim; ++b) h.u[b] = __ldg(&sp->u[b]);
-    h.rb = __ldg(&sp->rot_begin);
-    h.nr = __ldg(&sp->nrot);
-    h.F = __ldg(&sp->F);
+    for (int b = 0; b < kSubDim; ++b) h.u[b] = ldr<PARAM>(&sp->u[b]);
+    h.rb = ldr<PARAM>(&sp->rot_begin);
+    h.nr = ldr<PARAM>(&sp->nrot);
+    h.F = ldr<PARAM>(&sp->F);
     uint32_t r = 0;
 #pragma unroll
     for (int b = 0; b < kMaxCols; ++b)
-        if (b < ncols && ((tid >> b) & 1u)) r ^= (uint32_t)__ldg(&sp->col[b]);
+        if (b < ncols && ((tid >> b) & 1u)) r ^= (uint32_t)ldr<PARAM>(&sp->col[b]);
     h.r = r;
     return h;
 }
@@ -605,11 +614,11 @@ __host__ __device__ inline size_t coset_off_bytes(int hbits) {
     return ((sizeof(uint64_t) << hbits) + 127) & ~(size_t)127;
 }
 
-template <typename T, int MAXT, int MINB, int SPEC>
-__global__ void __launch_bounds__(MAXT, MINB)
-    k_coset(T* __restrict__ a, int kbits, int cbits, const __grid_constant__ BitRuns runs, const uint64_t* __restrict__ offs,
-            uint64_t ntiles, const DevSub* __restrict__ subs, int nsub, const DevTRot* __restrict__ trots,
-            int l2_prefetch, uint64_t or_mask) {
+template <typename T, int SPEC, int PARAM>
+__device__ __forceinline__ void coset_body(T* __restrict__ a, int kbits, int cbits, const BitRuns& runs,
+                                           const uint64_t* __restrict__ offs, uint64_t ntiles,
+                                           const DevSub* __restrict__ subs, int nsub, const DevTRot* __restrict__ trots,
+                                           int l2_prefetch, uint64_t or_mask) {
     using V2 = typename SmemAmp<T>::V;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int hbits = kbits - cbits;
@@ -625,7 +634,7 @@ __global__ void __launch_bounds__(MAXT, MINB)
         const uint64_t i0 = deposit(tau, runs) | or_mask;
         T vr[kSubAmps], vi[kSubAmps];
         for (int s = 0; s < nsub; ++s) {
-            const SubHdr h = load_sub(subs + s, tid, kbits - kSubDim);
+            const SubHdr h = load_sub<PARAM>(subs + s, tid, kbits - kSubDim);
             if (s == 0) {
                 uint64_t gi[kSubAmps];
 #pragma unroll
@@ -673,7 +682,7 @@ __global__ void __launch_bounds__(MAXT, MINB)
                                  "r"(chunk_bytes)
                                  : "memory");
             }
-            sub_apply<T, SPEC>(vr, vi, trots, h.rb, h.nr, h.r, i0);
+            sub_apply<T, SPEC, PARAM>(vr, vi, trots, h.rb, h.nr, h.r, i0);
             if (h.F != 1.0) sub_scale<T>(vr, vi, (T)h.F);
             if (s == nsub - 1) {
 #pragma unroll
@@ -697,6 +706,30 @@ __global__ void __launch_bounds__(MAXT, MINB)
         }
         if (nsub > 1) __syncthreads();  // last sub-group's shared reads before the next tile's writes
     }
+}
+
+template <typename T, int MAXT, int MINB, int SPEC>
+__global__ void __launch_bounds__(MAXT, MINB)
+    k_coset(T* __restrict__ a, int kbits, int cbits, const __grid_constant__ BitRuns runs, const uint64_t* __restrict__ offs,
+            uint64_t ntiles, const DevSub* __restrict__ subs, int nsub, const DevTRot* __restrict__ trots,
+            int l2_prefetch, uint64_t or_mask) {
+    coset_body<T, SPEC, 0>(a, kbits, cbits, runs, offs, ntiles, subs, nsub, trots, l2_prefetch, or_mask);
+}
+
+// the pass's records in the parameter block (passes of <= kParamRots rotations): record reads
+// become uniform constant-bank loads instead of two LDGs per rotation and thread
+constexpr int kParamRots = 64;
+struct PassRecs {
+    DevSub subs[kParamRots];
+    DevTRot trots[kParamRots];
+};
+
+template <typename T, int MAXT, int MINB>
+__global__ void __launch_bounds__(MAXT, MINB)
+    k_coset_p(T* __restrict__ a, int kbits, int cbits, const __grid_constant__ BitRuns runs,
+              const uint64_t* __restrict__ offs, uint64_t ntiles, int nsub, int l2_prefetch, uint64_t or_mask,
+              const __grid_constant__ PassRecs recs) {
+    coset_body<T, 0, 1>(a, kbits, cbits, runs, offs, ntiles, recs.subs, nsub, recs.trots, l2_prefetch, or_mask);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -1282,6 +1315,51 @@ cudaError_t launch_coset_t(T* a, int nl, const Pass& p, const DevSub* d_subs, co
     return launch_coset_k<T, kCosetThreads, PS_COSET_MINB, 0>(a, nl, p, d_subs, d_trots, d_offs, l2_prefetch, grid_mult, s);
 }
 
+// the pass's records in the launch's parameter block (tune bit 10; passes of <= kParamRots
+// rotations); cudaErrorNotSupported when the pass does not fit
+template <typename T, int MAXT, int MINB>
+cudaError_t launch_coset_param_k(T* a, const Pass& p, const PassRecs& recs, const uint64_t* d_offs, int l2_prefetch,
+                                 int grid_mult, cudaStream_t s) {
+    const size_t smem = coset_off_bytes(p.kbits - p.cbits) + ((size_t)(2 * sizeof(T)) << p.kbits);
+    static uint64_t attr_devices = 0;
+    const int dev = current_device();
+    if (!((attr_devices >> dev) & 1)) {
+        cudaFuncSetAttribute(k_coset_p<T, MAXT, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        attr_devices |= 1ull << dev;
+    }
+    const int threads = 1 << (p.kbits - kSubDim);
+    if (threads > MAXT) return cudaErrorNotSupported;
+    int occ = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_coset_p<T, MAXT, MINB>, threads, smem);
+    if (occ < 1) occ = 1;
+    const uint64_t ntiles = 1ull << __builtin_popcountll(p.free_mask);
+    const uint64_t cap = (uint64_t)num_sms() * (uint64_t)occ * (uint64_t)(grid_mult > 0 ? grid_mult : 1);
+    const unsigned grid = (unsigned)(ntiles < cap ? ntiles : cap);
+    k_coset_p<T, MAXT, MINB><<<grid, threads, smem, s>>>(a, p.kbits, p.cbits, make_runs(p.free_mask), d_offs + p.off_begin,
+                                                          ntiles, p.sub_count, l2_prefetch, p.or_mask, recs);
+    return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t launch_coset_param(T* a, const Pass& p, const DevSub* h_subs, const DevTRot* h_trots,
+                               const uint64_t* d_offs, int l2_prefetch, int grid_mult, int occ_sel, cudaStream_t s) {
+    if (p.sub_count < 1 || p.sub_count > kParamRots) return cudaErrorNotSupported;
+    const int base = h_subs[p.sub_begin].rot_begin;
+    int nrot = 0;
+    for (int t = 0; t < p.sub_count; ++t) nrot += h_subs[p.sub_begin + t].nrot;
+    if (nrot > kParamRots) return cudaErrorNotSupported;
+    static thread_local PassRecs recs;
+    for (int t = 0; t < p.sub_count; ++t) {
+        recs.subs[t] = h_subs[p.sub_begin + t];
+        recs.subs[t].rot_begin -= base;
+    }
+    for (int q = 0; q < nrot; ++q) recs.trots[q] = h_trots[base + q];
+    const int threads = 1 << (p.kbits - kSubDim);
+    if (sizeof(T) == 4 && occ_sel == 0 && threads <= 128)
+        return launch_coset_param_k<T, 128, 8>(a, p, recs, d_offs, l2_prefetch, grid_mult, s);
+    return launch_coset_param_k<T, kCosetThreads, PS_COSET_MINB>(a, p, recs, d_offs, l2_prefetch, grid_mult, s);
+}
+
 template <typename T, int CPASYNC>
 cudaError_t launch_coset_pf_t(T* a, int nl, const Pass& p, const DevSub* d_subs, const DevTRot* d_trots,
                               const uint64_t* d_offs, cudaStream_t s) {
@@ -1352,12 +1430,19 @@ cudaError_t launch_stream(int dtype, void* a, int nl, const Pass& p, const DevRo
 }
 
 cudaError_t launch_tile(int dtype, void* a, int nl, const Pass& p, const DevSub* d_subs, const DevTRot* d_trots,
-                        const uint64_t* d_offs, int use_tma, int tune, cudaStream_t s) {
+                        const uint64_t* d_offs, int use_tma, int tune, cudaStream_t s, const DevSub* h_subs,
+                        const DevTRot* h_trots) {
     // tune: bit 0 = L2 prefetch of the next tile (register-direct kernel); bits 4.. = grid multiplier
     // bit 0: TMA bulk L2 prefetch; bit 8: per-thread L2 prefetch; bit 9: L2::256B load hint
     const int l2p = (tune & 1) | ((tune >> 7) & 2) | ((tune >> 7) & 4);
     const int occ_sel = (tune >> 1) & 7;
     const int gm = ((tune >> 4) & 15) ? ((tune >> 4) & 15) : 4;
+    if (use_tma == 2 && (tune & 1024) && h_subs && !p.spec) {
+        cudaError_t e = dtype == PS_C128
+                            ? launch_coset_param<double>((double*)a, p, h_subs, h_trots, d_offs, l2p, gm, occ_sel, s)
+                            : launch_coset_param<float>((float*)a, p, h_subs, h_trots, d_offs, l2p, gm, occ_sel, s);
+        if (e != cudaErrorNotSupported) return e;
+    }
     if (use_tma == 2) {
         if (dtype == PS_C128) return launch_coset_t<double>((double*)a, nl, p, d_subs, d_trots, d_offs, l2p, gm, occ_sel, s);
         return launch_coset_t<float>((float*)a, nl, p, d_subs, d_trots, d_offs, l2p, gm, occ_sel, s);

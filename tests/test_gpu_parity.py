@@ -77,6 +77,26 @@ def test_specialised_kernel_identical(dtype, kind, n, count, tb):
     assert np.max(np.abs(outs[2] - want)) <= TOL[dtype]
 
 
+@pytest.mark.parametrize("dtype", ["c128", "c64"])
+@pytest.mark.parametrize("kind,n,count,tb", [("R10", 12, 400, 8), ("S8", 13, 640, 9), ("R4", 14, 500, 10),
+                                             ("D", 11, 200, 7)])
+def test_param_block_records_identical(dtype, kind, n, count, tb):
+    """Records read from the launch's parameter block (PS_OPT_TILE_TUNE bit 10, the default) and
+    from global memory (bit 10 clear) drive the same arithmetic: bitwise-identical results."""
+    codes, ang, want = _want(n, kind, count, 11)
+    x, z = P.pauli_encode_codes(codes)
+    outs = []
+    for tune in (512, 1536):
+        with P.State(n, dtype) as st:
+            st.set_option(ps.OPT_TILE_BITS, tb)
+            st.set_option(ps.OPT_TILE_TUNE, tune)
+            st.init_random(SEED)
+            st.apply_rotations(x, z, ang)
+            outs.append(st.get_amplitudes())
+    assert np.array_equal(outs[0], outs[1])
+    assert np.max(np.abs(outs[1] - want)) <= TOL[dtype]
+
+
 @pytest.mark.parametrize("n", [1, 2, 3, 5, 8, 11, 14, 17])
 @pytest.mark.parametrize("kind", ["R4", "R10", "D", "S8", "LOW"])
 @pytest.mark.parametrize("dtype", ["c128", "c64"])
