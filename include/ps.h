@@ -108,7 +108,7 @@ enum {
                                  persistent-grid multiplier, 8 = per-thread L2 prefetch, 9 = L2::256B
                                  sector promotion on the gathered loads, 10 = the pass's records
                                  in the launch's parameter block (uniform constant-bank loads;
-                                 passes of <= 64 rotations) (default 1536 = bits 9 + 10) */
+                                 passes of <= 256 rotations) (default 1536 = bits 9 + 10) */
     PS_OPT_LAYOUT = 9,        /* world > 1: 1 = lazy qubit-swap layout kept across calls, swaps chosen
                                  by furthest next use (default); 0 = one half-vector exchange per run
                                  sharing the upper X-part, swapped back at once (Eq. (1) economy);

@@ -716,11 +716,12 @@ __global__ void __launch_bounds__(MAXT, MINB)
     coset_body<T, SPEC, 0>(a, kbits, cbits, runs, offs, ntiles, subs, nsub, trots, l2_prefetch, or_mask);
 }
 
-// the pass's records in the parameter block (passes of <= kParamRots rotations): record reads
-// become uniform constant-bank loads instead of two LDGs per rotation and thread
-constexpr int kParamRots = 64;
+// the pass's records in the parameter block (passes of <= kParamRots rotations in <= kParamSubs
+// sub-groups; 15.4 KB of the 32 KB parameter space): record reads become uniform constant-bank
+// loads instead of two LDGs per rotation and thread
+constexpr int kParamRots = 256, kParamSubs = 128;
 struct PassRecs {
-    DevSub subs[kParamRots];
+    DevSub subs[kParamSubs];
     DevTRot trots[kParamRots];
 };
 
@@ -1343,7 +1344,7 @@ cudaError_t launch_coset_param_k(T* a, const Pass& p, const PassRecs& recs, cons
 template <typename T>
 cudaError_t launch_coset_param(T* a, const Pass& p, const DevSub* h_subs, const DevTRot* h_trots,
                                const uint64_t* d_offs, int l2_prefetch, int grid_mult, int occ_sel, cudaStream_t s) {
-    if (p.sub_count < 1 || p.sub_count > kParamRots) return cudaErrorNotSupported;
+    if (p.sub_count < 1 || p.sub_count > kParamSubs) return cudaErrorNotSupported;
     const int base = h_subs[p.sub_begin].rot_begin;
     int nrot = 0;
     for (int t = 0; t < p.sub_count; ++t) nrot += h_subs[p.sub_begin + t].nrot;
