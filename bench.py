@@ -202,6 +202,15 @@ def cpu_oracle_sample(args, budget_s=15.0, n_sample=26):
     low n_sample qubits, same weights/letters otherwise) at n_sample qubits until the time budget
     is spent; rot/s is scaled by 2^(n_sample - n) to the n-qubit state (cost is linear in 2^n)."""
     import oracle
+    cores = os.cpu_count() or 1
+    try:
+        # the host's cores, even under torchrun (which exports OMP_NUM_THREADS=1): the oracle's
+        # OpenMP runtime is the system libgomp, whose thread count is set here process-wide
+        import ctypes
+        oracle.lib()
+        ctypes.CDLL("libgomp.so.1").omp_set_num_threads(cores)
+    except OSError:
+        cores = int(os.environ.get("OMP_NUM_THREADS", cores))
     n_s = min(n_sample, args.n)
     codes, ang = workloads.random_layer(n_s, args.layer, seed=1000, kind=args.kind)
     psi = oracle.random_state(workloads.BASE_SEED, n_s)
@@ -213,7 +222,6 @@ def cpu_oracle_sample(args, budget_s=15.0, n_sample=26):
             break
     el = time.perf_counter() - t0
     rate = done / el * 2.0 ** (n_s - args.n)
-    cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
     return {"value": rate, "unit": UNIT, "cores": cores, "kind": "oracle",
             "sample": f"{done} rotations of a {args.kind} layer on a {n_s}-qubit fp64 state in {el:.1f} s, "
                       f"scaled by 2^({n_s}-{args.n}) to the {args.n}-qubit state"}
