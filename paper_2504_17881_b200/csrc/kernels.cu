@@ -531,6 +531,21 @@ __device__ __forceinline__ uint32_t sub_local(const SubHdr& h, int d) {
     return l;
 }
 
+// global indices of the thread's 16 elements l_d = r xor U(d): the map l -> i0 xor off[l >> c] xor
+// (l & cmask) is GF(2)-linear in l (off[] enumerates a span, chunk bits and free bits are
+// disjoint), so gi[d] = gi[d without its lowest bit] xor Lin(u_lowest): one 64-bit xor each
+__host__ __device__ constexpr int lowbit_index(int d) { return (d & 1) ? 0 : (d & 2) ? 1 : (d & 4) ? 2 : 3; }
+
+__device__ __forceinline__ void elem_index(uint64_t (&gi)[kSubAmps], const SubHdr& h, uint64_t i0,
+                                           const uint64_t* soff, int cbits, uint32_t cmask) {
+    uint64_t E[kSubDim];
+#pragma unroll
+    for (int b = 0; b < kSubDim; ++b) E[b] = soff[h.u[b] >> cbits] ^ (uint64_t)(h.u[b] & cmask);
+    gi[0] = i0 ^ soff[h.r >> cbits] ^ (uint64_t)(h.r & cmask);
+#pragma unroll
+    for (int d = 1; d < kSubAmps; ++d) gi[d] = gi[d & (d - 1)] ^ E[lowbit_index(d)];
+}
+
 __device__ __forceinline__ double2 ld_l2_256(const double2* p) {
     double2 v;
     asm volatile("ld.global.L1::no_allocate.L2::256B.v2.f64 {%0,%1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
@@ -637,11 +652,7 @@ __device__ __forceinline__ void coset_body(T* __restrict__ a, int kbits, int cbi
             const SubHdr h = load_sub<PARAM>(subs + s, tid, kbits - kSubDim);
             if (s == 0) {
                 uint64_t gi[kSubAmps];
-#pragma unroll
-                for (int d = 0; d < kSubAmps; ++d) {
-                    const uint32_t l = sub_local(h, d);
-                    gi[d] = (i0 ^ soff[l >> cbits]) | (l & cmask);
-                }
+                elem_index(gi, h, i0, soff, cbits, cmask);
                 V2 v[kSubAmps];
                 if (l2_prefetch & 4) {
 #pragma unroll
@@ -685,13 +696,14 @@ __device__ __forceinline__ void coset_body(T* __restrict__ a, int kbits, int cbi
             sub_apply<T, SPEC, PARAM>(vr, vi, trots, h.rb, h.nr, h.r, i0);
             if (h.F != 1.0) sub_scale<T>(vr, vi, (T)h.F);
             if (s == nsub - 1) {
+                uint64_t gi[kSubAmps];
+                elem_index(gi, h, i0, soff, cbits, cmask);
 #pragma unroll
                 for (int d = 0; d < kSubAmps; ++d) {
-                    const uint32_t l = sub_local(h, d);
                     V2 v;
                     v.x = vr[d];
                     v.y = vi[d];
-                    __stcs(&g[(i0 ^ soff[l >> cbits]) | (l & cmask)], v);
+                    __stcs(&g[gi[d]], v);
                 }
             } else {
 #pragma unroll
