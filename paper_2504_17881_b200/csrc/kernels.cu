@@ -507,19 +507,32 @@ struct SubHdr {
     double F;
 };
 
+// the thread's coset representative r = xor of col[b] over the set bits b of its thread index
 template <int PARAM = 0>
-__device__ __forceinline__ SubHdr load_sub(const DevSub* __restrict__ sp, uint32_t tid, int ncols) {
+__device__ __forceinline__ uint32_t sub_rep(const DevSub* __restrict__ sp, uint32_t tid, int ncols) {
+    uint32_t r = 0;
+#pragma unroll
+    for (int b = 0; b < kMaxCols; ++b)
+        if (b < ncols && ((tid >> b) & 1u)) r ^= (uint32_t)ldr<PARAM>(&sp->col[b]);
+    return r;
+}
+
+template <int PARAM = 0>
+__device__ __forceinline__ SubHdr load_sub_hdr(const DevSub* __restrict__ sp) {
     SubHdr h;
 #pragma unroll
     for (int b = 0; b < kSubDim; ++b) h.u[b] = ldr<PARAM>(&sp->u[b]);
     h.rb = ldr<PARAM>(&sp->rot_begin);
     h.nr = ldr<PARAM>(&sp->nrot);
     h.F = ldr<PARAM>(&sp->F);
-    uint32_t r = 0;
-#pragma unroll
-    for (int b = 0; b < kMaxCols; ++b)
-        if (b < ncols && ((tid >> b) & 1u)) r ^= (uint32_t)ldr<PARAM>(&sp->col[b]);
-    h.r = r;
+    h.r = 0;
+    return h;
+}
+
+template <int PARAM = 0>
+__device__ __forceinline__ SubHdr load_sub(const DevSub* __restrict__ sp, uint32_t tid, int ncols) {
+    SubHdr h = load_sub_hdr<PARAM>(sp);
+    h.r = sub_rep<PARAM>(sp, tid, ncols);
     return h;
 }
 
@@ -629,27 +642,47 @@ __host__ __device__ inline size_t coset_off_bytes(int hbits) {
     return ((sizeof(uint64_t) << hbits) + 127) & ~(size_t)127;
 }
 
+// per-thread coset representatives of the first rep_tab sub-groups, computed once per CTA (fp64
+// only: at 8 CTAs per SM the fp32 kernel loses more to the extra shared memory than it saves)
+__host__ __device__ constexpr int rep_tab(size_t amp_bytes) { return amp_bytes == 16 ? 16 : 0; }
+
+// dynamic shared memory of the register-direct tile kernels: offsets | tile | representatives
+__host__ __device__ inline size_t coset_smem_bytes(int kbits, int cbits, size_t amp_bytes) {
+    const size_t threads = (size_t)1 << (kbits - kSubDim);
+    return coset_off_bytes(kbits - cbits) + (amp_bytes << kbits) + rep_tab(amp_bytes) * threads * sizeof(uint32_t);
+}
+
 template <typename T, int SPEC, int PARAM>
 __device__ __forceinline__ void coset_body(T* __restrict__ a, int kbits, int cbits, const BitRuns& runs,
                                            const uint64_t* __restrict__ offs, uint64_t ntiles,
                                            const DevSub* __restrict__ subs, int nsub, const DevTRot* __restrict__ trots,
-                                           int l2_prefetch, uint64_t or_mask) {
+                                           int l2_prefetch, uint64_t or_mask, uint64_t free_mask) {
     using V2 = typename SmemAmp<T>::V;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int hbits = kbits - cbits;
     uint64_t* soff = reinterpret_cast<uint64_t*>(smem_raw);
     V2* tile = reinterpret_cast<V2*>(smem_raw + coset_off_bytes(hbits));
+    uint32_t* rtab = reinterpret_cast<uint32_t*>(smem_raw + coset_off_bytes(hbits) + (sizeof(V2) << kbits));
     const uint32_t tid = threadIdx.x;
     const uint32_t cmask = (1u << cbits) - 1u;
+    const int ncols = kbits - kSubDim;
     for (uint32_t u = tid; u < (1u << hbits); u += blockDim.x) soff[u] = __ldg(&offs[u]);
+    // representatives depend on (sub-group, thread) only: once per CTA (each thread reads its own)
+    constexpr int kRepTab = rep_tab(sizeof(V2));
+    for (int s = 0; s < nsub && s < kRepTab; ++s) rtab[s * blockDim.x + tid] = sub_rep<PARAM>(subs + s, tid, ncols);
     __syncthreads();
     V2* g = reinterpret_cast<V2*>(a);
     const uint32_t chunk_bytes = (uint32_t)(2 * sizeof(T)) << cbits;
-    for (uint64_t tau = blockIdx.x; tau < ntiles; tau += gridDim.x) {
-        const uint64_t i0 = deposit(tau, runs) | or_mask;
+    // tile bases advance in the deposited domain: pdep(tau + G) = ((pdep(tau) | ~M) + pdep(G)) & M
+    const uint64_t dstep = deposit((uint64_t)gridDim.x, runs);
+    uint64_t dtau = deposit((uint64_t)blockIdx.x, runs);
+    for (uint64_t tau = blockIdx.x; tau < ntiles;
+         tau += gridDim.x, dtau = ((dtau | ~free_mask) + dstep) & free_mask) {
+        const uint64_t i0 = dtau | or_mask;
         T vr[kSubAmps], vi[kSubAmps];
         for (int s = 0; s < nsub; ++s) {
-            const SubHdr h = load_sub<PARAM>(subs + s, tid, kbits - kSubDim);
+            SubHdr h = load_sub_hdr<PARAM>(subs + s);
+            h.r = s < kRepTab ? rtab[s * blockDim.x + tid] : sub_rep<PARAM>(subs + s, tid, ncols);
             if (s == 0) {
                 uint64_t gi[kSubAmps];
                 elem_index(gi, h, i0, soff, cbits, cmask);
@@ -724,8 +757,8 @@ template <typename T, int MAXT, int MINB, int SPEC>
 __global__ void __launch_bounds__(MAXT, MINB)
     k_coset(T* __restrict__ a, int kbits, int cbits, const __grid_constant__ BitRuns runs, const uint64_t* __restrict__ offs,
             uint64_t ntiles, const DevSub* __restrict__ subs, int nsub, const DevTRot* __restrict__ trots,
-            int l2_prefetch, uint64_t or_mask) {
-    coset_body<T, SPEC, 0>(a, kbits, cbits, runs, offs, ntiles, subs, nsub, trots, l2_prefetch, or_mask);
+            int l2_prefetch, uint64_t or_mask, uint64_t free_mask) {
+    coset_body<T, SPEC, 0>(a, kbits, cbits, runs, offs, ntiles, subs, nsub, trots, l2_prefetch, or_mask, free_mask);
 }
 
 // the pass's records in the parameter block (passes of <= kParamRots rotations in <= kParamSubs
@@ -741,8 +774,9 @@ template <typename T, int MAXT, int MINB>
 __global__ void __launch_bounds__(MAXT, MINB)
     k_coset_p(T* __restrict__ a, int kbits, int cbits, const __grid_constant__ BitRuns runs,
               const uint64_t* __restrict__ offs, uint64_t ntiles, int nsub, int l2_prefetch, uint64_t or_mask,
-              const __grid_constant__ PassRecs recs) {
-    coset_body<T, 0, 1>(a, kbits, cbits, runs, offs, ntiles, recs.subs, nsub, recs.trots, l2_prefetch, or_mask);
+              uint64_t free_mask, const __grid_constant__ PassRecs recs) {
+    coset_body<T, 0, 1>(a, kbits, cbits, runs, offs, ntiles, recs.subs, nsub, recs.trots, l2_prefetch, or_mask,
+                        free_mask);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -1285,7 +1319,7 @@ cudaError_t launch_stream_t(T* a, int nl, const Pass& p, const DevRot* d_rots, c
 template <typename T, int MAXT, int MINB, int SPEC>
 cudaError_t launch_coset_k(T* a, int nl, const Pass& p, const DevSub* d_subs, const DevTRot* d_trots,
                            const uint64_t* d_offs, int l2_prefetch, int grid_mult, cudaStream_t s) {
-    const size_t smem = coset_off_bytes(p.kbits - p.cbits) + ((size_t)(2 * sizeof(T)) << p.kbits);
+    const size_t smem = coset_smem_bytes(p.kbits, p.cbits, 2 * sizeof(T));
     static uint64_t attr_devices = 0;  // function attributes are per device
     const int dev = current_device();
     if (!((attr_devices >> dev) & 1)) {
@@ -1302,7 +1336,7 @@ cudaError_t launch_coset_k(T* a, int nl, const Pass& p, const DevSub* d_subs, co
     const unsigned grid = (unsigned)(ntiles < cap ? ntiles : cap);
     k_coset<T, MAXT, MINB, SPEC><<<grid, threads, smem, s>>>(a, p.kbits, p.cbits, make_runs(p.free_mask),
                                                               d_offs + p.off_begin, ntiles, d_subs + p.sub_begin,
-                                                              p.sub_count, d_trots, l2_prefetch, p.or_mask);
+                                                              p.sub_count, d_trots, l2_prefetch, p.or_mask, p.free_mask);
     return cudaGetLastError();
 }
 
@@ -1333,7 +1367,7 @@ cudaError_t launch_coset_t(T* a, int nl, const Pass& p, const DevSub* d_subs, co
 template <typename T, int MAXT, int MINB>
 cudaError_t launch_coset_param_k(T* a, const Pass& p, const PassRecs& recs, const uint64_t* d_offs, int l2_prefetch,
                                  int grid_mult, cudaStream_t s) {
-    const size_t smem = coset_off_bytes(p.kbits - p.cbits) + ((size_t)(2 * sizeof(T)) << p.kbits);
+    const size_t smem = coset_smem_bytes(p.kbits, p.cbits, 2 * sizeof(T));
     static uint64_t attr_devices = 0;
     const int dev = current_device();
     if (!((attr_devices >> dev) & 1)) {
@@ -1349,7 +1383,8 @@ cudaError_t launch_coset_param_k(T* a, const Pass& p, const PassRecs& recs, cons
     const uint64_t cap = (uint64_t)num_sms() * (uint64_t)occ * (uint64_t)(grid_mult > 0 ? grid_mult : 1);
     const unsigned grid = (unsigned)(ntiles < cap ? ntiles : cap);
     k_coset_p<T, MAXT, MINB><<<grid, threads, smem, s>>>(a, p.kbits, p.cbits, make_runs(p.free_mask), d_offs + p.off_begin,
-                                                          ntiles, p.sub_count, l2_prefetch, p.or_mask, recs);
+                                                          ntiles, p.sub_count, l2_prefetch, p.or_mask, p.free_mask,
+                                                          recs);
     return cudaGetLastError();
 }
 
