@@ -570,6 +570,18 @@ __device__ __forceinline__ float2 ld_l2_256(const float2* p) {
     return v;
 }
 
+// one amplitude HBM -> shared memory without a register round trip (LDGSTS), L2 256-B sector hint
+__device__ __forceinline__ void cp_async_amp(double2* dst, const double2* src) {
+    asm volatile("cp.async.cg.shared.global.L2::256B [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
+                 "l"(src)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_amp(float2* dst, const float2* src) {
+    asm volatile("cp.async.ca.shared.global.L2::256B [%0], [%1], 8;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
+                 "l"(src)
+                 : "memory");
+}
+
 template <typename T>
 struct SmemAmp;
 template <>
@@ -676,6 +688,22 @@ __device__ __forceinline__ void coset_body(T* __restrict__ a, int kbits, int cbi
     // tile bases advance in the deposited domain: pdep(tau + G) = ((pdep(tau) | ~M) + pdep(G)) & M
     const uint64_t dstep = deposit((uint64_t)gridDim.x, runs);
     uint64_t dtau = deposit((uint64_t)blockIdx.x, runs);
+    // tune bit 11 (l2_prefetch & 8): sub-group 0 of the CTA's next tile is copied HBM -> shared
+    // memory (LDGSTS, one slot per thread and element) as soon as this tile's last sub-group has
+    // its inputs in registers, so the next tile's reads are in flight while this one is computed
+    // and stored; sub-group 0 then reads its own slots instead of HBM
+    const bool pf = (l2_prefetch & 8) != 0;
+    const uint32_t nthr = blockDim.x;
+    auto prefetch_tile = [&](uint64_t i1) {
+        SubHdr h0 = load_sub_hdr<PARAM>(subs);
+        h0.r = kRepTab > 0 ? rtab[tid] : sub_rep<PARAM>(subs, tid, ncols);
+        uint64_t gi[kSubAmps];
+        elem_index(gi, h0, i1, soff, cbits, cmask);
+#pragma unroll
+        for (int d = 0; d < kSubAmps; ++d) cp_async_amp(&tile[d * nthr + tid], &g[gi[d]]);
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    if (pf && blockIdx.x < ntiles) prefetch_tile(dtau | or_mask);
     for (uint64_t tau = blockIdx.x; tau < ntiles;
          tau += gridDim.x, dtau = ((dtau | ~free_mask) + dstep) & free_mask) {
         const uint64_t i0 = dtau | or_mask;
@@ -683,7 +711,15 @@ __device__ __forceinline__ void coset_body(T* __restrict__ a, int kbits, int cbi
         for (int s = 0; s < nsub; ++s) {
             SubHdr h = load_sub_hdr<PARAM>(subs + s);
             h.r = s < kRepTab ? rtab[s * blockDim.x + tid] : sub_rep<PARAM>(subs + s, tid, ncols);
-            if (s == 0) {
+            if (s == 0 && pf) {
+                asm volatile("cp.async.wait_group 0;" ::: "memory");
+#pragma unroll
+                for (int d = 0; d < kSubAmps; ++d) {
+                    const V2 v = tile[d * nthr + tid];
+                    vr[d] = v.x;
+                    vi[d] = v.y;
+                }
+            } else if (s == 0) {
                 uint64_t gi[kSubAmps];
                 elem_index(gi, h, i0, soff, cbits, cmask);
                 V2 v[kSubAmps];
@@ -726,6 +762,13 @@ __device__ __forceinline__ void coset_body(T* __restrict__ a, int kbits, int cbi
                                  "r"(chunk_bytes)
                                  : "memory");
             }
+            if (pf && (s == 0 || s == nsub - 1)) {
+                // every thread's shared-memory reads of this sub-group are done before the slots
+                // (s == 0) or the tile (last sub-group) are overwritten
+                __syncthreads();
+                if (s == nsub - 1 && tau + gridDim.x < ntiles)
+                    prefetch_tile((((dtau | ~free_mask) + dstep) & free_mask) | or_mask);
+            }
             sub_apply<T, SPEC, PARAM>(vr, vi, trots, h.rb, h.nr, h.r, i0);
             if (h.F != 1.0) sub_scale<T>(vr, vi, (T)h.F);
             if (s == nsub - 1) {
@@ -749,7 +792,7 @@ __device__ __forceinline__ void coset_body(T* __restrict__ a, int kbits, int cbi
                 __syncthreads();
             }
         }
-        if (nsub > 1) __syncthreads();  // last sub-group's shared reads before the next tile's writes
+        if (nsub > 1 && !pf) __syncthreads();  // last sub-group's shared reads before the next tile's writes
     }
 }
 
@@ -1482,7 +1525,8 @@ cudaError_t launch_tile(int dtype, void* a, int nl, const Pass& p, const DevSub*
                         const DevTRot* h_trots) {
     // tune: bit 0 = L2 prefetch of the next tile (register-direct kernel); bits 4.. = grid multiplier
     // bit 0: TMA bulk L2 prefetch; bit 8: per-thread L2 prefetch; bit 9: L2::256B load hint
-    const int l2p = (tune & 1) | ((tune >> 7) & 2) | ((tune >> 7) & 4);
+    // bit 11: LDGSTS prefetch of the next tile's first sub-group into shared memory
+    const int l2p = (tune & 1) | ((tune >> 7) & 2) | ((tune >> 7) & 4) | ((tune >> 8) & 8);
     const int occ_sel = (tune >> 1) & 7;
     const int gm = ((tune >> 4) & 15) ? ((tune >> 4) & 15) : 4;
     if (use_tma == 2 && (tune & 1024) && h_subs && !p.spec) {

@@ -82,18 +82,20 @@ def test_specialised_kernel_identical(dtype, kind, n, count, tb):
                                              ("D", 11, 200, 7)])
 def test_param_block_records_identical(dtype, kind, n, count, tb):
     """Records read from the launch's parameter block (PS_OPT_TILE_TUNE bit 10, the default) and
-    from global memory (bit 10 clear) drive the same arithmetic: bitwise-identical results."""
+    from global memory (bit 10 clear), with or without the shared-memory prefetch of the next
+    tile (bit 11), drive the same arithmetic: bitwise-identical results."""
     codes, ang, want = _want(n, kind, count, 11)
     x, z = P.pauli_encode_codes(codes)
     outs = []
-    for tune in (512, 1536):
+    for tune in (512, 1536, 512 | 2048, 1536 | 2048):
         with P.State(n, dtype) as st:
             st.set_option(ps.OPT_TILE_BITS, tb)
             st.set_option(ps.OPT_TILE_TUNE, tune)
             st.init_random(SEED)
             st.apply_rotations(x, z, ang)
             outs.append(st.get_amplitudes())
-    assert np.array_equal(outs[0], outs[1])
+    for o in outs[1:]:
+        assert np.array_equal(outs[0], o)
     assert np.max(np.abs(outs[1] - want)) <= TOL[dtype]
 
 
