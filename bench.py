@@ -371,7 +371,7 @@ def run_ours(args):
             "scaling": "strong", "vs_baseline": None, "dtype": "f64" if args.dtype == "c128" else "f32",
             "data": "synthetic",
             "config": {"workload": workload_name(args), "n_qubits": args.n, "rotations_per_step": rot_per_step,
-                       "fusion": args.fusion, "tile_mode": args.tile_mode, "tile_bits": args.tile_bits or 11,
+                       "fusion": args.fusion, "tile_mode": args.tile_mode, "tile_bits": args.tile_bits or (12 if args.dtype == "c128" else 11),
                        "layout": args.layout, "transport": args.transport, "overlap": args.overlap, "specialize": args.specialize,
                        "parallelism": f"state sharded over {world} GPU(s) by top qubits",
                        "l2": "inputs larger than L2 (state %.1f GiB per GPU)" % (local_state / 2 ** 30)},

@@ -92,7 +92,8 @@ typedef struct ps_stats {
 enum {
     PS_OPT_PROFILE = 0,       /* 1: time every launch with CUDA events on the handle's stream (default 0) */
     PS_OPT_FUSION = 1,        /* 0: one rotation per pass (K1 only); 1: same-x runs; 2: + tiles (default 2) */
-    PS_OPT_TILE_BITS = 2,     /* log2 amplitudes per fused tile, 4..12 (default 11) */
+    PS_OPT_TILE_BITS = 2,     /* log2 amplitudes per fused tile, 4..12 (default 12 for C128,
+                                 11 for C64) */
     PS_OPT_CHUNK_BYTES = 3,   /* exchange chunk size in bytes (default 256 MiB) */
     PS_OPT_MAX_PASS_ROTS = 4, /* cap on rotations fused into one tile pass (default: no cap) */
     PS_OPT_VEC256 = 5,        /* 1: 256-bit LDG/STG in K1 (default 1); 0: 128-bit */
@@ -108,7 +109,10 @@ enum {
                                  persistent-grid multiplier, 8 = per-thread L2 prefetch, 9 = L2::256B
                                  sector promotion on the gathered loads, 10 = the pass's records
                                  in the launch's parameter block (uniform constant-bank loads;
-                                 passes of <= 256 rotations) (default 1536 = bits 9 + 10) */
+                                 passes of <= 256 rotations), 11 = LDGSTS prefetch of the next
+                                 tile's first sub-group into shared memory while the current
+                                 tile's last sub-group is computed and stored (default C128 3584
+                                 = bits 9 + 10 + 11, C64 1536 = bits 9 + 10) */
     PS_OPT_LAYOUT = 9,        /* world > 1: 1 = lazy qubit-swap layout kept across calls, swaps chosen
                                  by furthest next use (default); 0 = one half-vector exchange per run
                                  sharing the upper X-part, swapped back at once (Eq. (1) economy);

@@ -345,7 +345,11 @@ extern "C" int ps_create_ex(int n_qubits, int dtype, void* dev_buf, size_t bytes
     h->world = world;
     h->dtype = dtype;
     h->amp_bytes = dtype == PS_C128 ? 16 : 8;
-    h->tile_bits = 11;
+    // per-dtype defaults (profiles/r01/kernel_ab.md): fp64 2^12 tiles with the next tile's first
+    // sub-group prefetched into shared memory (tune bit 11); fp32 2^11 tiles at 8 CTAs per SM,
+    // where the prefetch costs more occupancy than it hides
+    h->tile_bits = dtype == PS_C128 ? 12 : 11;
+    h->tile_tune = dtype == PS_C128 ? (1536 | 2048) : 1536;
     cudaError_t e = cudaGetDevice(&h->device);
     if (e != cudaSuccess) {
         delete h;
