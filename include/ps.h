@@ -60,21 +60,23 @@ typedef enum {
 /* kernel families counted in ps_stats */
 enum {
     PS_K_STREAM = 0,   /* K1: streaming pair-rotation pass (single rotation or same-x run)   */
-    PS_K_TILE = 1,     /* K2: low-qubit fused tile pass (contiguous 2^k tile through TMA)     */
+    PS_K_TILE = 1,     /* K2: low-qubit fused tile pass (contiguous 2^k tile: gathered into registers,
+                          shared memory between sub-groups; TMA only in the A/B modes)       */
     PS_K_COSET = 2,    /* K7: coset-tile fused pass (gathered 2^k tile)                       */
     PS_K_REDUCE = 3,   /* K5: norm / expectation / inner-product reductions                   */
     PS_K_INIT = 4,     /* K6: state initialisation                                            */
     PS_K_EXCHANGE = 5, /* K3: half-vector exchange (NVLink P2P swap or NCCL send/recv)       */
     PS_K_PERMUTE = 6,  /* local qubit transposition pass (restoring the canonical layout)     */
     PS_K_MIRROR = 7,   /* PS_OPT_LAYOUT=2: butterfly / recombine passes of Eq. (core_state)    */
-    PS_K_COUNT = 8
+    PS_K_XTILE = 8,    /* K8: fused half-vector exchange + tile pass (PS_OPT_FUSED_EXCHANGE)    */
+    PS_K_COUNT = 9
 };
 
 /* extra plan-op kinds (ps_plan_describe only): the paper's three-step grouped execution */
 enum {
-    PS_OP_MIRROR_BEGIN = 8,  /* B <- conj(w_k) A_(k xor gx) (full exchange), butterfly A,B      */
-    PS_OP_MIRROR_SWITCH = 9, /* following passes act on B (with negated angles)               */
-    PS_OP_MIRROR_END = 10    /* A <- (A + B)/sqrt(2); passes act on A again                   */
+    PS_OP_MIRROR_BEGIN = 16,  /* B <- conj(w_k) A_(k xor gx) (full exchange), butterfly A,B     */
+    PS_OP_MIRROR_SWITCH = 17, /* following passes act on B (with negated angles)              */
+    PS_OP_MIRROR_END = 18     /* A <- (A + B)/sqrt(2); passes act on A again                  */
 };
 
 typedef struct ps_stats {
@@ -84,16 +86,20 @@ typedef struct ps_stats {
     uint64_t launches[PS_K_COUNT];       /* kernel launches per family */
     uint64_t rotations_by[PS_K_COUNT];   /* rotations applied per family */
     double algo_bytes[PS_K_COUNT];       /* algorithmic HBM bytes per family (2*2^n_l*s per pass) */
-    double nvlink_bytes;                 /* bytes sent to peers by exchanges */
+    double nvlink_bytes;                 /* bytes sent to each peer by swap exchanges and mirror
+                                            fetches, per direction (PS_K_EXCHANGE time) */
     double kernel_ms[PS_K_COUNT];        /* device time per family (CUDA events; PS_OPT_PROFILE=1 only) */
+    double nvlink_fused_bytes;           /* bytes read from the partner by fused exchange + tile
+                                            passes (PS_K_XTILE time) */
 } ps_stats;
 
 /* options for ps_set_option */
 enum {
     PS_OPT_PROFILE = 0,       /* 1: time every launch with CUDA events on the handle's stream (default 0) */
     PS_OPT_FUSION = 1,        /* 0: one rotation per pass (K1 only); 1: same-x runs; 2: + tiles (default 2) */
-    PS_OPT_TILE_BITS = 2,     /* log2 amplitudes per fused tile, 4..12 (default 12 for C128,
-                                 11 for C64) */
+    PS_OPT_TILE_BITS = 2,     /* log2 amplitudes per fused tile, 4..13 for C128 (default 12),
+                                 4..14 for C64 (default 11); 2^13 / 2^14 tiles run one CTA of
+                                 512 / 1024 threads per SM */
     PS_OPT_CHUNK_BYTES = 3,   /* exchange chunk size in bytes (default 256 MiB) */
     PS_OPT_MAX_PASS_ROTS = 4, /* cap on rotations fused into one tile pass (default: no cap) */
     PS_OPT_VEC256 = 5,        /* 1: 256-bit LDG/STG in K1 (default 1); 0: 128-bit */
@@ -129,13 +135,21 @@ enum {
                                  pattern): no per-pair sign flips, but 256 cases cost i-cache
                                  misses and register shuffles), 1 = planner's per-pass choice
                                  (specialised for passes of >= 16 rotations using <= 32 cases).
-                                 Bitwise-identical results (same operations in the same order) */
+                                 Bitwise-identical results (same operations in the same order) */,
+    PS_OPT_GRID_CAP = 13,     /* test knob: cap on the persistent tile grid (CTAs), so small states
+                                 run several tiles per CTA (incremental tile bases, next-tile
+                                 prefetch); 0 = no cap (default) */
+    PS_OPT_FUSED_EXCHANGE = 14 /* world > 1 with peer access (P2P transport or emulation): 1 = a
+                                 half-vector exchange followed by a tile pass runs as ONE kernel that
+                                 reads the partner's half through the peer pointer and stores in the
+                                 new layout, with per-tile release/acquire flags instead of a swap
+                                 (default); 0 = swap, then the pass */
 };
 
 /* ------------------------------------------------------------------------------------------ */
 /* Lifetime                                                                                    */
 
-/* Single GPU on the current CUDA device.  n_qubits in [1, 40] (memory permitting).
+/* Single GPU on the current CUDA device.  n_qubits in [1, 62] (memory permitting: 2^n amplitudes).
  * The state is allocated (2^n * 16 B for PS_C128) and set to |0>. */
 int ps_create(int n_qubits, int dtype, ps_handle *out);
 
@@ -152,6 +166,21 @@ int ps_create(int n_qubits, int dtype, ps_handle *out);
  * The state is set to |0>. */
 int ps_create_ex(int n_qubits, int dtype, void *dev_buf, size_t bytes, void *stream, int rank,
                  int world, const void *nccl_id, ps_handle *out);
+
+/* Rank emulation on ONE device (tests and single-GPU evidence of the multi-GPU path): the state is
+ * split into `world` = G = 2^m slices of one device buffer (dev_buf, or library-owned when NULL;
+ * 2^n amplitudes, slice r = global indices [r 2^(n-m), (r+1) 2^(n-m)) as on G GPUs), each driven by
+ * a virtual rank with its own plan (per-rank signs and exchange sides), its own records
+ * and the same kernels as a real rank; peer pointers are the other slices, NCCL barriers become
+ * stream order on `stream` (NULL: the library creates one), all-reduces become host sums.  The
+ * virtual ranks run their plans pass by pass in lockstep (two phases where ranks read each other's
+ * data; one launch over all ranks for the fused exchange).  The handle is used like a single
+ * state: calls are NOT collective, index ranges are global, ps_get_stats reports rank 0's
+ * counters.  Transport is always peer access (PS_OPT_TRANSPORT is ignored) and the two-stream
+ * overlap is off.  world in [1, 8] for the fused exchange kernel (larger groups fall back to
+ * swaps).  The state is set to |0>. */
+int ps_create_emulated(int n_qubits, int dtype, int world, void *dev_buf, size_t bytes, void *stream,
+                       ps_handle *out);
 
 /* Convenience: ps_create_ex with library-owned memory and stream. */
 int ps_create_dist(int n_qubits, int dtype, int rank, int world, const void *nccl_id,

@@ -1,6 +1,14 @@
 // api.cpp -- the C ABI of libps (include/ps.h): handles, device memory, streams, NCCL, and the
 // execution of plans produced by planner.cpp.  Argument marshalling and orchestration only;
 // every step of the path runs in the kernels of kernels.cu (or NCCL for exchanges).
+//
+// Rank sets.  Every operation runs on a RANK SET: one handle for a real rank (one process per
+// GPU, collectives over NCCL), or the G virtual ranks of an emulation group (ps_create_emulated:
+// G slices of one device buffer, the same planner, plans and kernels, peer pointers into the
+// other slices, stream order instead of NCCL barriers and host sums instead of all-reduces).
+// The virtual ranks of a group execute their plans pass by pass in lockstep; a pass whose
+// ranks read each other's data (full exchange, mirror fetch) runs as two phases over all ranks,
+// and the fused exchange + tile pass runs as one kernel over all ranks' slices.
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <nccl.h>
@@ -23,7 +31,7 @@ cudaError_t launch_stream(int dtype, void* a, int nl, const Pass& p, const DevRo
                           cudaStream_t s);
 cudaError_t launch_tile(int dtype, void* a, int nl, const Pass& p, const DevSub* d_subs, const DevTRot* d_trots,
                         const uint64_t* d_offs, int use_tma, int tune, cudaStream_t s, const DevSub* h_subs,
-                        const DevTRot* h_trots);
+                        const DevTRot* h_trots, int grid_cap);
 cudaError_t launch_full_update(int dtype, void* a, const void* stage, uint64_t base, uint64_t count, uint64_t pbase,
                                const DevRot* rec, cudaStream_t s);
 cudaError_t launch_norm(int dtype, const void* a, uint64_t n, double* d_partial, double* d_out, cudaStream_t s);
@@ -31,6 +39,9 @@ cudaError_t launch_inner(int dtype, const void* a, const void* b, uint64_t n, do
                          cudaStream_t s);
 cudaError_t launch_expect(int dtype, const void* a, uint64_t n, uint64_t x0, const DevTerm* terms, int nt,
                           double* d_partial, double* d_out_slot, cudaStream_t s);
+cudaError_t launch_expect_cross(int dtype, const void* a, const void* stage, uint64_t base, uint64_t count,
+                                uint64_t pbase, uint64_t xl, uint64_t zl, int y, int sgn, double* d_partial,
+                                double* d_out_slot, cudaStream_t s);
 cudaError_t launch_init_random(int dtype, void* a, uint64_t n, uint64_t seed, uint64_t goff, cudaStream_t s);
 cudaError_t launch_set_one(int dtype, void* a, uint64_t idx, cudaStream_t s);
 cudaError_t launch_scale(int dtype, void* a, uint64_t n, double f, cudaStream_t s);
@@ -41,6 +52,8 @@ cudaError_t launch_p2p_copy(int dtype, void* dst, const void* src, uint64_t n, c
 cudaError_t launch_p2p_swap(int dtype, void* local, void* peer, uint64_t rows, uint64_t row_amps, uint64_t my_off,
                             uint64_t peer_off, uint64_t t0, uint64_t t1, uint64_t fmask, uint64_t fval,
                             cudaStream_t s, int ctas);
+cudaError_t launch_xtile(int dtype, const XTileRank* ranks, int nranks, const Pass& p, const uint64_t* d_offs,
+                         const uint64_t* h_offs, int ell, uint32_t epoch, cudaStream_t s, int grid_cap);
 
 static thread_local std::string g_last_error;
 void set_last_error(const std::string& msg) { g_last_error = msg; }
@@ -63,6 +76,11 @@ struct ps_state {
     cudaStream_t stream = nullptr;
     bool own_stream = false;
     bool poisoned = false;
+    // emulation: a virtual rank of a group (no NCCL; peers = the group's other slices), or the
+    // group handle itself (vranks = its virtual ranks in rank order)
+    bool emulated = false;
+    std::vector<ps_state*> vranks;
+    bool is_group() const { return !vranks.empty(); }
     // per-call plan buffers
     DevRot* d_rots = nullptr;
     size_t d_rots_cap = 0;
@@ -90,12 +108,19 @@ struct ps_state {
     // layout (world > 1): physical bit -> logical qubit; identity = canonical
     std::vector<int> perm;
     int* d_barrier = nullptr;
-    std::vector<void*> peers;  // CUDA-IPC peer pointers to every rank's local slice (P2P transport)
+    std::vector<void*> peers;  // peer pointers to every rank's local slice (CUDA IPC, or the group's slices)
     std::vector<void*> peer_bases;
     bool p2p = false;
+    // fused exchange + tile pass (PS_OPT_FUSED_EXCHANGE): per-tile handshake flags of every rank
+    uint32_t* d_flags = nullptr;
+    size_t flags_cap = 0;
+    std::vector<uint32_t*> peer_flags;
+    uint32_t epoch = 0;
+    int fused = 1;
     void* d_mirror = nullptr;  // PS_OPT_LAYOUT=2 mirror buffer B_k
     cudaStream_t xstream = nullptr;  // second stream: swaps overlapped with the next pass
-    static constexpr int kXev = 9;
+    static constexpr int kMaxPieceBits = 3;
+    static constexpr int kXev = 2 + (1 << kMaxPieceBits);
     cudaEvent_t xev[kXev] = {};
     int overlap = 1;
     int swap_ctas = 32;   // CTAs of an overlapped swap (NVLink-bound; leaves SMs to the pass)
@@ -103,6 +128,7 @@ struct ps_state {
     const Plan* cur_plan = nullptr;  // the plan being executed (host copies of its records)
     int layout = 1, transport = 1;
     int specialize = 0;
+    int grid_cap = 0;
     // options
     int profile = 0, fusion = 2, tile_bits = 11, vec256 = 1, max_pass_rots = 1 << 30, tile_tma = 2, chunk_bits = 0, tile_tune = 1536;
     ps_stats stats{};
@@ -110,6 +136,8 @@ struct ps_state {
     std::vector<cudaEvent_t> event_pool;
     Plan plan;  // reused
 };
+
+using RankSet = std::vector<ps_state*>;
 
 // ------------------------------------------------------------------------------------------
 // error helpers
@@ -139,12 +167,25 @@ static int fail(int code, const std::string& msg) {
         }                                                                                          \
     } while (0)
 
+static bool any_poisoned(ps_state* h) {
+    if (h->poisoned) return true;
+    for (ps_state* v : h->vranks)
+        if (v->poisoned) return h->poisoned = true;
+    return false;
+}
+
 #define CHECK_HANDLE(h)                                                                            \
     do {                                                                                           \
         if (!(h)) return fail(PS_EINVAL, "NULL handle");                                           \
-        if ((h)->poisoned) return fail(PS_ESTATE, "handle poisoned by an earlier fault");          \
+        if (any_poisoned(h)) return fail(PS_ESTATE, "handle poisoned by an earlier fault");        \
         cudaSetDevice((h)->device);                                                                \
     } while (0)
+
+static RankSet ranks_of(ps_state* h) { return h->is_group() ? h->vranks : RankSet{h}; }
+
+static void poison_all(const RankSet& rs) {
+    for (ps_state* r : rs) r->poisoned = true;
+}
 
 static cudaEvent_t get_event(ps_state* h) {
     if (!h->event_pool.empty()) {
@@ -157,20 +198,22 @@ static cudaEvent_t get_event(ps_state* h) {
     return e;
 }
 
+// CUDA events around a launch on the stream it runs on (PS_OPT_PROFILE)
 struct Timed {
     ps_state* h;
     int kind;
+    cudaStream_t st;
     cudaEvent_t e0 = nullptr;
-    Timed(ps_state* hh, int k) : h(hh), kind(k) {
+    Timed(ps_state* hh, int k, cudaStream_t s = nullptr) : h(hh), kind(k), st(s ? s : hh->stream) {
         if (h->profile) {
             e0 = get_event(h);
-            cudaEventRecord(e0, h->stream);
+            cudaEventRecord(e0, st);
         }
     }
     ~Timed() {
         if (h->profile && e0) {
             cudaEvent_t e1 = get_event(h);
-            cudaEventRecord(e1, h->stream);
+            cudaEventRecord(e1, st);
             h->pending.push_back({kind, e0, e1});
         }
     }
@@ -215,11 +258,14 @@ static void free_state(ps_state* h) {
     if (!h) return;
     cudaSetDevice(h->device);
     if (h->stream) cudaStreamSynchronize(h->stream);
+    for (ps_state* v : h->vranks) free_state(v);
+    h->vranks.clear();
     drain_timings(h);
     for (auto e : h->event_pool) cudaEventDestroy(e);
     for (void* b : h->peer_bases)
         if (b) cudaIpcCloseMemHandle(b);
     if (h->d_barrier) cudaFree(h->d_barrier);
+    if (h->d_flags) cudaFree(h->d_flags);
     if (h->d_mirror) cudaFree(h->d_mirror);
     if (h->xstream) cudaStreamDestroy(h->xstream);
     for (int t = 0; t < ps_state::kXev; ++t)
@@ -243,35 +289,44 @@ static void free_state(ps_state* h) {
     delete h;
 }
 
-extern "C" int ps_init_basis(ps_handle h, uint64_t index);
+static int init_basis_rank(ps_state* h, uint64_t index);
 static void reset_layout(ps_state* h);
-static int restore_layout(ps_state* h);
+static int restore_layout(const RankSet& rs);
 
-// CUDA-IPC peer pointers to every rank's local slice: the allocation base is exported with its
-// offset (cuMemGetAddressRange through the runtime's driver entry point), all-gathered with NCCL
+// CUDA-IPC peer pointers to every rank's local slice and handshake flags: the allocation base is
+// exported with its offset (cuMemGetAddressRange through the runtime's driver entry point),
+// all-gathered with NCCL
 struct IpcRec {
     cudaIpcMemHandle_t handle;
     uint64_t offset;
+    cudaIpcMemHandle_t flag_handle;
     int32_t ok;
     int32_t pad;
 };
 
+static bool ipc_export(void* ptr, cudaIpcMemHandle_t* handle, uint64_t* offset) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn) return false;
+    typedef CUresult (*GetRange)(CUdeviceptr*, size_t*, CUdeviceptr);
+    CUdeviceptr base = 0;
+    size_t size = 0;
+    if (((GetRange)fn)(&base, &size, (CUdeviceptr)ptr) != CUDA_SUCCESS) return false;
+    if (cudaIpcGetMemHandle(handle, (void*)base) != cudaSuccess) return false;
+    *offset = (uint64_t)((CUdeviceptr)ptr - base);
+    return true;
+}
+
+// handshake flags of the fused exchange + tile pass: one 32-bit word per tile of the smallest
+// tiles a pass can have (2^4 amplitudes), so every pass's tile index has a word
+static size_t flag_words(const ps_state* h) { return (size_t)1 << std::max(0, h->nl - 4); }
+
 static void setup_p2p(ps_state* h) {
     h->p2p = false;
     IpcRec mine{};
-    mine.ok = 0;
-    void* fn = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) == cudaSuccess && fn) {
-        typedef CUresult (*GetRange)(CUdeviceptr*, size_t*, CUdeviceptr);
-        CUdeviceptr base = 0;
-        size_t size = 0;
-        if (((GetRange)fn)(&base, &size, (CUdeviceptr)h->d_state) == CUDA_SUCCESS &&
-            cudaIpcGetMemHandle(&mine.handle, (void*)base) == cudaSuccess) {
-            mine.offset = (uint64_t)((CUdeviceptr)h->d_state - base);
-            mine.ok = 1;
-        }
-    }
+    mine.ok = ipc_export(h->d_state, &mine.handle, &mine.offset) ? 1 : 0;
+    uint64_t foff = 0;
+    if (mine.ok && h->d_flags) mine.ok = ipc_export(h->d_flags, &mine.flag_handle, &foff) && foff == 0;
     cudaGetLastError();
     IpcRec* d_all = nullptr;
     if (cudaMalloc(&d_all, sizeof(IpcRec) * (h->world + 1)) != cudaSuccess) return;
@@ -284,7 +339,8 @@ static void setup_p2p(ps_state* h) {
     cudaFree(d_all);
     int my_ok = ok ? 1 : 0;
     h->peers.assign(h->world, nullptr);
-    h->peer_bases.assign(h->world, nullptr);
+    h->peer_bases.assign(2 * h->world, nullptr);
+    h->peer_flags.assign(h->world, nullptr);
     for (int r = 0; r < h->world && my_ok; ++r) {
         if (!all[r].ok) {
             my_ok = 0;
@@ -292,6 +348,7 @@ static void setup_p2p(ps_state* h) {
         }
         if (r == h->rank) {
             h->peers[r] = h->d_state;
+            h->peer_flags[r] = h->d_flags;
             continue;
         }
         void* b = nullptr;
@@ -302,6 +359,14 @@ static void setup_p2p(ps_state* h) {
         }
         h->peer_bases[r] = b;
         h->peers[r] = (char*)b + all[r].offset;
+        void* f = nullptr;
+        if (cudaIpcOpenMemHandle(&f, all[r].flag_handle, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+            cudaGetLastError();
+            my_ok = 0;
+            break;
+        }
+        h->peer_bases[h->world + r] = f;
+        h->peer_flags[r] = (uint32_t*)f;
     }
     // every rank must agree (the transport is collective)
     int* d_flag = h->d_barrier;
@@ -312,38 +377,35 @@ static void setup_p2p(ps_state* h) {
         cudaStreamSynchronize(h->stream) == cudaSuccess)
         h->p2p = agree == 1;
     cudaMemsetAsync(d_flag, 0, sizeof(int), h->stream);
+    if (!h->p2p) h->fused = 0;
     if (h->p2p) {
         // high priority: swap (and barrier) CTAs are dispatched ahead of the pending CTAs of the
         // persistent tile grid they overlap with
         int lo_prio = 0, hi_prio = 0;
         cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio);
-        bool ok = cudaStreamCreateWithPriority(&h->xstream, cudaStreamNonBlocking, hi_prio) == cudaSuccess;
-        for (int t = 0; ok && t < ps_state::kXev; ++t)
-            ok = cudaEventCreateWithFlags(&h->xev[t], cudaEventDisableTiming) == cudaSuccess;
-        if (!ok) {
+        bool sok = cudaStreamCreateWithPriority(&h->xstream, cudaStreamNonBlocking, hi_prio) == cudaSuccess;
+        for (int t = 0; sok && t < ps_state::kXev; ++t)
+            sok = cudaEventCreateWithFlags(&h->xev[t], cudaEventDisableTiming) == cudaSuccess;
+        if (!sok) {
             cudaGetLastError();
             h->overlap = 0;
         }
     }
 }
 
-extern "C" int ps_create_ex(int n_qubits, int dtype, void* dev_buf, size_t bytes, void* stream, int rank,
-                            int world, const void* nccl_id, ps_handle* out) {
-    if (!out) return fail(PS_EINVAL, "NULL out");
+// one rank's state: device memory (or the caller's), scratch, layout; NCCL and P2P when world > 1
+// and the rank is real
+static int make_state(int n_qubits, int dtype, void* dev_buf, size_t bytes, void* stream, int rank, int world,
+                      const void* nccl_id, bool emulated, ps_state** out) {
     *out = nullptr;
-    if (dtype != PS_C128 && dtype != PS_C64) return fail(PS_EINVAL, "dtype must be PS_C128 or PS_C64");
-    if (world < 1 || (world & (world - 1))) return fail(PS_EINVAL, "world must be a power of two");
-    if (rank < 0 || rank >= world) return fail(PS_EINVAL, "rank out of range");
     const int m = __builtin_ctz((unsigned)world);
-    if (n_qubits < 1 || n_qubits > 62) return fail(PS_EINVAL, "n_qubits must be in [1, 62]");
-    if (n_qubits - m < 1) return fail(PS_EINVAL, "need at least one local qubit (n - log2(world) >= 1)");
-    if (world > 1 && !nccl_id) return fail(PS_EINVAL, "world > 1 needs an NCCL unique id");
     ps_state* h = new ps_state();
     h->n = n_qubits;
     h->nl = n_qubits - m;
     h->rank = rank;
     h->world = world;
     h->dtype = dtype;
+    h->emulated = emulated;
     h->amp_bytes = dtype == PS_C128 ? 16 : 8;
     // per-dtype defaults (profiles/r01/kernel_ab.md): fp64 2^12 tiles with the next tile's first
     // sub-group prefetched into shared memory (tune bit 11); fp32 2^11 tiles at 8 CTAs per SM,
@@ -356,7 +418,6 @@ extern "C" int ps_create_ex(int n_qubits, int dtype, void* dev_buf, size_t bytes
         return fail(PS_ECUDA, std::string("cudaGetDevice: ") + cudaGetErrorString(e));
     }
     const size_t need = h->amp_bytes << h->nl;
-    int rc = PS_OK;
     auto bail = [&](int code, const std::string& msg) {
         free_state(h);
         return fail(code, msg);
@@ -370,7 +431,9 @@ extern "C" int ps_create_ex(int n_qubits, int dtype, void* dev_buf, size_t bytes
     }
     if (dev_buf) {
         if (bytes < need) return bail(PS_EINVAL, "dev_buf smaller than the local slice");
-        if (((uintptr_t)dev_buf) & 255) return bail(PS_EINVAL, "dev_buf must be 256-byte aligned");
+        // 256-byte aligned (slices smaller than 256 B, e.g. of an emulation group: aligned to their size)
+        if (((uintptr_t)dev_buf) & (std::min<size_t>(256, need) - 1))
+            return bail(PS_EINVAL, "dev_buf must be 256-byte aligned");
         h->d_state = dev_buf;
     } else {
         e = cudaMalloc(&h->d_state, need);
@@ -389,16 +452,27 @@ extern "C" int ps_create_ex(int n_qubits, int dtype, void* dev_buf, size_t bytes
     h->perm.resize(n_qubits);
     for (int q = 0; q < n_qubits; ++q) h->perm[q] = q;
     if (world > 1) {
+        // handshake flags of the fused exchange + tile pass (0 = no epoch raised yet)
+        if ((e = cudaMalloc(&h->d_flags, sizeof(uint32_t) * flag_words(h))) != cudaSuccess)
+            return bail(PS_ENOMEM, std::string("flags: ") + cudaGetErrorString(e));
+        h->flags_cap = flag_words(h);
+        if ((e = cudaMemsetAsync(h->d_flags, 0, sizeof(uint32_t) * h->flags_cap, h->stream)) != cudaSuccess)
+            return bail(PS_ECUDA, std::string("flags: ") + cudaGetErrorString(e));
+    }
+    if (world > 1 && !emulated) {
         ncclUniqueId id;
         std::memcpy(&id, nccl_id, 128);
         ncclResult_t r = ncclCommInitRank(&h->comm, world, id, rank);
         if (r != ncclSuccess) return bail(PS_ENCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
         if ((e = cudaMalloc(&h->d_barrier, sizeof(int) * 4)) != cudaSuccess)
             return bail(PS_ENOMEM, std::string("barrier: ") + cudaGetErrorString(e));
-        cudaMemset(h->d_barrier, 0, sizeof(int) * 4);
+        // stream-ordered before setup_p2p's copies and all-reduces on the same words
+        if ((e = cudaMemsetAsync(h->d_barrier, 0, sizeof(int) * 4, h->stream)) != cudaSuccess)
+            return bail(PS_ECUDA, std::string("barrier: ") + cudaGetErrorString(e));
         setup_p2p(h);  // best effort; NCCL send/recv otherwise
     }
-    rc = ps_init_basis(h, 0);
+    if (emulated) h->overlap = 0;  // one stream per group; the fused kernel replaces the overlap
+    int rc = init_basis_rank(h, 0);
     if (rc) {
         std::string msg = ps_last_error();
         free_state(h);
@@ -408,12 +482,92 @@ extern "C" int ps_create_ex(int n_qubits, int dtype, void* dev_buf, size_t bytes
     return PS_OK;
 }
 
+static int check_create_args(int n_qubits, int dtype, int rank, int world) {
+    if (dtype != PS_C128 && dtype != PS_C64) return fail(PS_EINVAL, "dtype must be PS_C128 or PS_C64");
+    if (world < 1 || (world & (world - 1)) || world > (1 << 20)) return fail(PS_EINVAL, "world must be a power of two");
+    if (rank < 0 || rank >= world) return fail(PS_EINVAL, "rank out of range");
+    const int m = __builtin_ctz((unsigned)world);
+    if (n_qubits < 1 || n_qubits > 62) return fail(PS_EINVAL, "n_qubits must be in [1, 62]");
+    if (n_qubits - m < 1) return fail(PS_EINVAL, "need at least one local qubit (n - log2(world) >= 1)");
+    return PS_OK;
+}
+
+extern "C" int ps_create_ex(int n_qubits, int dtype, void* dev_buf, size_t bytes, void* stream, int rank,
+                            int world, const void* nccl_id, ps_handle* out) {
+    if (!out) return fail(PS_EINVAL, "NULL out");
+    *out = nullptr;
+    int rc = check_create_args(n_qubits, dtype, rank, world);
+    if (rc) return rc;
+    if (world > 1 && !nccl_id) return fail(PS_EINVAL, "world > 1 needs an NCCL unique id");
+    return make_state(n_qubits, dtype, dev_buf, bytes, stream, rank, world, nccl_id, false, out);
+}
+
 extern "C" int ps_create_dist(int n_qubits, int dtype, int rank, int world, const void* nccl_id, ps_handle* out) {
     return ps_create_ex(n_qubits, dtype, nullptr, 0, nullptr, rank, world, nccl_id, out);
 }
 
 extern "C" int ps_create(int n_qubits, int dtype, ps_handle* out) {
     return ps_create_ex(n_qubits, dtype, nullptr, 0, nullptr, 0, 1, nullptr, out);
+}
+
+extern "C" int ps_create_emulated(int n_qubits, int dtype, int world, void* dev_buf, size_t bytes, void* stream,
+                                  ps_handle* out) {
+    if (!out) return fail(PS_EINVAL, "NULL out");
+    *out = nullptr;
+    int rc = check_create_args(n_qubits, dtype, 0, world);
+    if (rc) return rc;
+    ps_state* g = new ps_state();
+    g->n = n_qubits;
+    g->nl = n_qubits - __builtin_ctz((unsigned)world);
+    g->world = world;
+    g->dtype = dtype;
+    g->amp_bytes = dtype == PS_C128 ? 16 : 8;
+    cudaError_t e = cudaGetDevice(&g->device);
+    auto bail = [&](int code, const std::string& msg) {
+        free_state(g);
+        return fail(code, msg);
+    };
+    if (e != cudaSuccess) return bail(PS_ECUDA, std::string("cudaGetDevice: ") + cudaGetErrorString(e));
+    const size_t slice = g->amp_bytes << g->nl, need = slice * (size_t)world;
+    if (stream) {
+        g->stream = (cudaStream_t)stream;
+    } else {
+        e = cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking);
+        if (e != cudaSuccess) return bail(PS_ECUDA, std::string("cudaStreamCreate: ") + cudaGetErrorString(e));
+        g->own_stream = true;
+    }
+    if (dev_buf) {
+        if (bytes < need) return bail(PS_EINVAL, "dev_buf smaller than the state");
+        if (((uintptr_t)dev_buf) & 255) return bail(PS_EINVAL, "dev_buf must be 256-byte aligned");
+        g->d_state = dev_buf;
+    } else {
+        e = cudaMalloc(&g->d_state, need);
+        if (e != cudaSuccess) return bail(PS_ENOMEM, std::string("cudaMalloc state: ") + cudaGetErrorString(e));
+        g->own_state = true;
+    }
+    for (int r = 0; r < world; ++r) {
+        ps_state* v = nullptr;
+        rc = make_state(n_qubits, dtype, (char*)g->d_state + slice * r, slice, g->stream, r, world, nullptr,
+                        world > 1, &v);
+        if (rc) {
+            std::string msg = ps_last_error();
+            return bail(rc, msg);
+        }
+        g->vranks.push_back(v);
+    }
+    for (ps_state* v : g->vranks) {
+        v->peers.resize(world);
+        v->peer_flags.resize(world);
+        for (int r = 0; r < world; ++r) {
+            v->peers[r] = g->vranks[r]->d_state;
+            v->peer_flags[r] = g->vranks[r]->d_flags;
+        }
+        v->p2p = world > 1;
+    }
+    g->tile_bits = g->vranks[0]->tile_bits;
+    g->tile_tune = g->vranks[0]->tile_tune;
+    *out = g;
+    return PS_OK;
 }
 
 extern "C" int ps_destroy(ps_handle h) {
@@ -433,32 +587,48 @@ extern "C" int ps_info(ps_handle h, int* n_qubits, int* n_local, int* rank, int*
     return PS_OK;
 }
 
-extern "C" int ps_set_option(ps_handle h, int option, int64_t value) {
-    if (!h) return fail(PS_EINVAL, "NULL handle");
+static int check_option(const ps_state* h, int option, int64_t value) {
     switch (option) {
-    case PS_OPT_PROFILE: h->profile = value ? 1 : 0; break;
-    case PS_OPT_FUSION:
-        if (value < 0 || value > 2) return fail(PS_EINVAL, "fusion must be 0, 1 or 2");
-        h->fusion = (int)value;
-        break;
+    case PS_OPT_PROFILE:
+    case PS_OPT_VEC256:
+    case PS_OPT_TILE_TUNE:
+    case PS_OPT_TRANSPORT:
+    case PS_OPT_FUSED_EXCHANGE: return PS_OK;
+    case PS_OPT_FUSION: return (value < 0 || value > 2) ? fail(PS_EINVAL, "fusion must be 0, 1 or 2") : PS_OK;
     case PS_OPT_TILE_BITS: {
-        // <= 256 threads x 16 amplitudes per tile (and 3 TMA stages of <= 64 KiB)
-        if (value < 4 || value > 12) return fail(PS_EINVAL, "tile bits out of range [4, 12]");
-        h->tile_bits = (int)value;
-        break;
+        // <= 512 (fp64) / 1024 (fp32) threads x 16 amplitudes per tile: 128 KiB of shared memory
+        const int kmax = h->dtype == PS_C128 ? 13 : 14;
+        return (value < 4 || value > kmax) ? fail(PS_EINVAL, "tile bits out of range [4, 13] (C128) / [4, 14] (C64)")
+                                           : PS_OK;
     }
     case PS_OPT_CHUNK_BYTES:
-        if (value < 4096 || (value & (value - 1))) return fail(PS_EINVAL, "chunk bytes must be a power of two >= 4096");
-        h->chunk_bytes = (size_t)value;
-        break;
-    case PS_OPT_MAX_PASS_ROTS:
-        if (value < 1) return fail(PS_EINVAL, "max pass rotations must be >= 1");
-        h->max_pass_rots = (int)std::min<int64_t>(value, 1 << 30);
-        break;
+        return (value < 4096 || (value & (value - 1))) ? fail(PS_EINVAL, "chunk bytes must be a power of two >= 4096")
+                                                        : PS_OK;
+    case PS_OPT_MAX_PASS_ROTS: return value < 1 ? fail(PS_EINVAL, "max pass rotations must be >= 1") : PS_OK;
+    case PS_OPT_LAYOUT: return (value < 0 || value > 2) ? fail(PS_EINVAL, "layout must be 0, 1 or 2") : PS_OK;
+    case PS_OPT_OVERLAP:
+        return (((value >> 16) & 7) > ps_state::kMaxPieceBits + 1) ? fail(PS_EINVAL, "overlap piece bits must be <= 3")
+                                                                    : PS_OK;
+    case PS_OPT_CHUNK_BITS:
+        return (value < 0 || value > 12) ? fail(PS_EINVAL, "chunk bits must be 0..12 (0 = default)") : PS_OK;
+    case PS_OPT_SPECIALIZE: return (value < 0 || value > 2) ? fail(PS_EINVAL, "specialize must be 0, 1 or 2") : PS_OK;
+    case PS_OPT_GRID_CAP: return (value < 0 || value > (1 << 20)) ? fail(PS_EINVAL, "grid cap must be 0..2^20") : PS_OK;
+    case PS_OPT_TILE_TMA: return (value < 0 || value > 3) ? fail(PS_EINVAL, "tile mode must be 0..3") : PS_OK;
+    default: return fail(PS_EINVAL, "unknown option");
+    }
+}
+
+// applies a validated option to one rank
+static int set_option_rank(ps_state* h, int option, int64_t value) {
+    switch (option) {
+    case PS_OPT_PROFILE: h->profile = value ? 1 : 0; break;
+    case PS_OPT_FUSION: h->fusion = (int)value; break;
+    case PS_OPT_TILE_BITS: h->tile_bits = (int)value; break;
+    case PS_OPT_CHUNK_BYTES: h->chunk_bytes = (size_t)value; break;
+    case PS_OPT_MAX_PASS_ROTS: h->max_pass_rots = (int)std::min<int64_t>(value, 1 << 30); break;
     case PS_OPT_VEC256: h->vec256 = value ? 1 : 0; break;
     case PS_OPT_TILE_TUNE: h->tile_tune = (int)value; break;
     case PS_OPT_LAYOUT:
-        if (value < 0 || value > 2) return fail(PS_EINVAL, "layout must be 0, 1 or 2");
         if (value == 2 && h->world > 1 && !h->d_mirror) {
             cudaSetDevice(h->device);
             cudaError_t e = cudaMalloc(&h->d_mirror, h->amp_bytes << h->nl);
@@ -467,33 +637,76 @@ extern "C" int ps_set_option(ps_handle h, int option, int64_t value) {
                 return fail(PS_ENOMEM, std::string("mirror buffer: ") + cudaGetErrorString(e));
             }
         }
-        if (value == 2 && h->world > 1) {
-            int rc = restore_layout(h);
-            if (rc) return rc;
-        }
         h->layout = (int)value;
         break;
-    case PS_OPT_TRANSPORT: h->transport = value ? 1 : 0; break;
-    case PS_OPT_OVERLAP:
-        // 0: off; 1: on (32 swap CTAs); > 1: on with that many swap CTAs
+    case PS_OPT_TRANSPORT: h->transport = (value || h->emulated) ? 1 : 0; break;
+    case PS_OPT_OVERLAP: {
         // 0: off; 1: on; > 1: on, bits 0-15 = swap CTAs (if > 1), bits 16-18 = piece bits + 1
+        const int pb = (int)((value >> 16) & 7);
         h->overlap = (value && h->xstream) ? 1 : 0;
         if ((value & 0xffff) > 1) h->swap_ctas = (int)(value & 0xffff);
-        if ((value >> 16) & 7) h->piece_bits = (int)((value >> 16) & 7) - 1;
+        if (pb) h->piece_bits = pb - 1;
         break;
-    case PS_OPT_CHUNK_BITS:
-        if (value < 0 || value > 12) return fail(PS_EINVAL, "chunk bits must be 0..12 (0 = default)");
-        h->chunk_bits = (int)value;
-        break;
-    case PS_OPT_SPECIALIZE:
-        if (value < 0 || value > 2) return fail(PS_EINVAL, "specialize must be 0, 1 or 2");
-        h->specialize = (int)value;
-        break;
-    case PS_OPT_TILE_TMA:
-        if (value < 0 || value > 3) return fail(PS_EINVAL, "tile mode must be 0..3");
-        h->tile_tma = (int)value;
-        break;
+    }
+    case PS_OPT_CHUNK_BITS: h->chunk_bits = (int)value; break;
+    case PS_OPT_SPECIALIZE: h->specialize = (int)value; break;
+    case PS_OPT_GRID_CAP: h->grid_cap = (int)value; break;
+    case PS_OPT_FUSED_EXCHANGE: h->fused = (value && h->p2p) ? 1 : 0; break;
+    case PS_OPT_TILE_TMA: h->tile_tma = (int)value; break;
     default: return fail(PS_EINVAL, "unknown option");
+    }
+    return PS_OK;
+}
+
+extern "C" int ps_set_option(ps_handle h, int option, int64_t value) {
+    if (!h) return fail(PS_EINVAL, "NULL handle");
+    int rc = check_option(h, option, value);
+    if (rc) return rc;
+    RankSet rs = ranks_of(h);
+    if (option == PS_OPT_LAYOUT && value == 2 && h->world > 1) {
+        // the mirror mode starts from the canonical layout
+        if (any_poisoned(h)) return fail(PS_ESTATE, "handle poisoned by an earlier fault");
+        cudaSetDevice(h->device);
+        if ((rc = restore_layout(rs))) return rc;
+    }
+    for (ps_state* r : rs)
+        if ((rc = set_option_rank(r, option, value))) return rc;
+    if (h->is_group()) {  // the group handle mirrors its ranks' options
+        h->tile_bits = rs[0]->tile_bits;
+        h->tile_tune = rs[0]->tile_tune;
+        h->layout = rs[0]->layout;
+        h->profile = rs[0]->profile;
+    }
+    return PS_OK;
+}
+
+// ------------------------------------------------------------------------------------------
+// collectives over a rank set: NCCL for a real rank, stream order and host sums for a group
+
+static int barrier(ps_state* h) {
+    if (h->emulated || h->world == 1) return PS_OK;  // emulation: one stream orders everything
+    NCCL_TRY(h, ncclAllReduce(h->d_barrier, h->d_barrier, 1, ncclInt32, ncclSum, h->comm, h->stream));
+    return PS_OK;
+}
+
+static int barrier_on(ps_state* h, cudaStream_t st, int slot) {
+    if (h->emulated || h->world == 1) return PS_OK;
+    NCCL_TRY(h, ncclAllReduce(h->d_barrier + slot, h->d_barrier + slot, 1, ncclInt32, ncclSum, h->comm, st));
+    return PS_OK;
+}
+
+// vals[k] = sum over all ranks of d_result[k], k < nvals (blocks)
+static int sum_results(const RankSet& rs, int nvals, double* vals) {
+    ps_state* h0 = rs[0];
+    if (!h0->emulated && h0->world > 1)
+        NCCL_TRY(h0, ncclAllReduce(h0->d_result, h0->d_result, (size_t)nvals, ncclDouble, ncclSum, h0->comm, h0->stream));
+    for (ps_state* r : rs)
+        CUDA_TRY(r, cudaMemcpyAsync(r->h_result, r->d_result, sizeof(double) * nvals, cudaMemcpyDeviceToHost, r->stream));
+    for (ps_state* r : rs) CUDA_TRY(r, cudaStreamSynchronize(r->stream));
+    for (int k = 0; k < nvals; ++k) {
+        double s = 0.0;
+        for (ps_state* r : rs) s += r->h_result[k];
+        vals[k] = s;
     }
     return PS_OK;
 }
@@ -503,36 +716,50 @@ extern "C" int ps_set_option(ps_handle h, int option, int64_t value) {
 
 static uint64_t local_amps(const ps_state* h) { return 1ull << h->nl; }
 
-extern "C" int ps_init_basis(ps_handle h, uint64_t index) {
-    CHECK_HANDLE(h);
-    if (h->n < 64 && index >> h->n) return fail(PS_ERANGE, "basis index >= 2^n");
+static int init_basis_rank(ps_state* h, uint64_t index) {
     reset_layout(h);  // the whole state is overwritten
     Timed t(h, PS_K_INIT);
     CUDA_TRY(h, cudaMemsetAsync(h->d_state, 0, h->amp_bytes * local_amps(h), h->stream));
-    if ((index >> h->nl) == (uint64_t)h->rank) CUDA_TRY(h, launch_set_one(h->dtype, h->d_state, index & (local_amps(h) - 1), h->stream));
+    if ((index >> h->nl) == (uint64_t)h->rank)
+        CUDA_TRY(h, launch_set_one(h->dtype, h->d_state, index & (local_amps(h) - 1), h->stream));
     h->stats.launches[PS_K_INIT] += 1;
+    return PS_OK;
+}
+
+extern "C" int ps_init_basis(ps_handle h, uint64_t index) {
+    CHECK_HANDLE(h);
+    if (h->n < 64 && index >> h->n) return fail(PS_ERANGE, "basis index >= 2^n");
+    for (ps_state* r : ranks_of(h)) {
+        int rc = init_basis_rank(r, index);
+        if (rc) return rc;
+    }
     return PS_OK;
 }
 
 extern "C" int ps_init_random(ps_handle h, uint64_t seed) {
     CHECK_HANDLE(h);
-    reset_layout(h);  // the whole state is overwritten
-    Timed t(h, PS_K_INIT);
-    CUDA_TRY(h, launch_init_random(h->dtype, h->d_state, local_amps(h), seed, (uint64_t)h->rank << h->nl, h->stream));
-    h->stats.launches[PS_K_INIT] += 1;
+    for (ps_state* r : ranks_of(h)) {
+        reset_layout(r);  // the whole state is overwritten
+        Timed t(r, PS_K_INIT);
+        CUDA_TRY(r, launch_init_random(r->dtype, r->d_state, local_amps(r), seed, (uint64_t)r->rank << r->nl, r->stream));
+        r->stats.launches[PS_K_INIT] += 1;
+    }
     return PS_OK;
 }
 
-static int reduce_norm(ps_state* h, double* out);
+static int reduce_norm(const RankSet& rs, double* out);
 
 extern "C" int ps_normalize(ps_handle h) {
     CHECK_HANDLE(h);
+    RankSet rs = ranks_of(h);
     double nrm = 0.0;
-    int rc = reduce_norm(h, &nrm);
+    int rc = reduce_norm(rs, &nrm);
     if (rc) return rc;
     if (!(nrm > 0.0)) return fail(PS_EINVAL, "cannot normalise a zero state");
-    Timed t(h, PS_K_INIT);
-    CUDA_TRY(h, launch_scale(h->dtype, h->d_state, local_amps(h), 1.0 / std::sqrt(nrm), h->stream));
+    for (ps_state* r : rs) {
+        Timed t(r, PS_K_INIT);
+        CUDA_TRY(r, launch_scale(r->dtype, r->d_state, local_amps(r), 1.0 / std::sqrt(nrm), r->stream));
+    }
     return PS_OK;
 }
 
@@ -549,18 +776,21 @@ extern "C" int ps_set_state(ps_handle h, uint64_t first, uint64_t count, const v
     if (count && !amps) return fail(PS_EINVAL, "NULL amps with count > 0");
     int rc = check_range(h, first, count);
     if (rc) return rc;
-    if (first == 0 && h->n < 64 && count == (1ull << h->n))
-        reset_layout(h);  // the whole state is overwritten
-    else if ((rc = restore_layout(h)))
+    RankSet rs = ranks_of(h);
+    if (first == 0 && h->n < 64 && count == (1ull << h->n)) {
+        for (ps_state* r : rs) reset_layout(r);  // the whole state is overwritten
+    } else if ((rc = restore_layout(rs))) {
         return rc;
-    const uint64_t lo = (uint64_t)h->rank << h->nl, hi = lo + local_amps(h);
-    const uint64_t a = std::max(lo, first), b = std::min(hi, first + count);
-    if (a < b) {
-        CUDA_TRY(h, cudaMemcpyAsync((char*)h->d_state + (a - lo) * h->amp_bytes,
-                                    (const char*)amps + (a - first) * h->amp_bytes, (b - a) * h->amp_bytes,
-                                    cudaMemcpyHostToDevice, h->stream));
-        CUDA_TRY(h, cudaStreamSynchronize(h->stream));
     }
+    for (ps_state* r : rs) {
+        const uint64_t lo = (uint64_t)r->rank << r->nl, hi = lo + local_amps(r);
+        const uint64_t a = std::max(lo, first), b = std::min(hi, first + count);
+        if (a < b)
+            CUDA_TRY(r, cudaMemcpyAsync((char*)r->d_state + (a - lo) * r->amp_bytes,
+                                        (const char*)amps + (a - first) * r->amp_bytes, (b - a) * r->amp_bytes,
+                                        cudaMemcpyHostToDevice, r->stream));
+    }
+    for (ps_state* r : rs) CUDA_TRY(r, cudaStreamSynchronize(r->stream));
     return PS_OK;
 }
 
@@ -582,12 +812,19 @@ extern "C" int ps_get_amplitudes(ps_handle h, uint64_t first, uint64_t count, vo
     if (count && !amps_out) return fail(PS_EINVAL, "NULL amps_out with count > 0");
     int rc = check_range(h, first, count);
     if (rc) return rc;
-    if ((rc = restore_layout(h))) return rc;
-    if (h->world == 1) {
-        if (count)
-            CUDA_TRY(h, cudaMemcpyAsync(amps_out, (const char*)h->d_state + first * h->amp_bytes, count * h->amp_bytes,
-                                        cudaMemcpyDeviceToHost, h->stream));
-        CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+    RankSet rs = ranks_of(h);
+    if ((rc = restore_layout(rs))) return rc;
+    if (h->world == 1 || h->is_group()) {
+        // every slice is on this device: copy each rank's part directly
+        for (ps_state* r : rs) {
+            const uint64_t lo = (uint64_t)r->rank << r->nl, hi = lo + local_amps(r);
+            const uint64_t a = std::max(lo, first), b = std::min(hi, first + count);
+            if (a < b)
+                CUDA_TRY(r, cudaMemcpyAsync((char*)amps_out + (a - first) * r->amp_bytes,
+                                            (const char*)r->d_state + (a - lo) * r->amp_bytes, (b - a) * r->amp_bytes,
+                                            cudaMemcpyDeviceToHost, r->stream));
+        }
+        for (ps_state* r : rs) CUDA_TRY(r, cudaStreamSynchronize(r->stream));
         return PS_OK;
     }
     // world > 1: pieces broadcast from their owners (collective; all ranks pass the same range)
@@ -615,11 +852,6 @@ extern "C" int ps_get_amplitudes(ps_handle h, uint64_t first, uint64_t count, vo
 // ------------------------------------------------------------------------------------------
 // exchanges (K3): half-vector swap of slots with bit ell == 1-keep with partner rank^gx
 
-static int barrier(ps_state* h) {
-    NCCL_TRY(h, ncclAllReduce(h->d_barrier, h->d_barrier, 1, ncclInt32, ncclSum, h->comm, h->stream));
-    return PS_OK;
-}
-
 static int exchange_half(ps_state* h, const Pass& p) {
     const int partner = h->rank ^ (int)p.gx;
     const size_t s = h->amp_bytes;
@@ -630,6 +862,7 @@ static int exchange_half(ps_state* h, const Pass& p) {
     if (h->p2p && h->transport) {
         // both ranks of the pair swap their regions in place through NVLink peer pointers, each
         // doing half of the elements; barriers order it against all earlier and later work
+        // (emulation: both halves run one after the other on the group's stream)
         const uint64_t row_amps = 1ull << p.ell, total = rows * row_amps;
         const uint64_t e0 = p.keep ? total / 2 : 0, e1 = p.keep ? total : total / 2;
         int rc = barrier(h);
@@ -681,11 +914,6 @@ static int exchange_half(ps_state* h, const Pass& p) {
     return PS_OK;
 }
 
-static int barrier_on(ps_state* h, cudaStream_t st, int slot) {
-    NCCL_TRY(h, ncclAllReduce(h->d_barrier + slot, h->d_barrier + slot, 1, ncclInt32, ncclSum, h->comm, st));
-    return PS_OK;
-}
-
 // a bit that splits the next pass's tiles into two halves whose elements all have that bit
 // fixed: a free (tile-enumeration) bit in which no two elements of one tile differ
 static uint64_t split_bits(const Pass& np) { return np.free_mask & ~np.touch_mask; }
@@ -710,7 +938,7 @@ static int exchange_overlap(ps_state* h, const Pass& ex, const Pass& np) {
     const bool f_is_ell = (sb >> ex.ell) & 1;
     uint64_t pbits = 0;  // piece bits (local positions): the highest split bits other than ell
     int B = 0;
-    for (int b = 63; b >= 0 && B < h->piece_bits; --b)
+    for (int b = 63; b >= 0 && B < std::min(h->piece_bits, (int)ps_state::kMaxPieceBits); --b)
         if (((sb >> b) & 1) && b != ex.ell) {
             pbits |= 1ull << b;
             ++B;
@@ -745,32 +973,37 @@ static int exchange_overlap(ps_state* h, const Pass& ex, const Pass& np) {
         q.or_mask = np.or_mask | fixed_val;
         Timed t(h, np.kind);
         CUDA_TRY(h, launch_tile(h->dtype, h->d_state, h->nl, q, h->d_subs, h->d_trots, h->d_offs, h->tile_tma,
-                                h->tile_tune, h->stream, h->cur_plan->subs.data(), h->cur_plan->trots.data()));
+                                h->tile_tune, h->stream, h->cur_plan->subs.data(), h->cur_plan->trots.data(),
+                                h->grid_cap));
         return PS_OK;
     };
     int rc = barrier(h);  // every rank's earlier passes are done
     if (rc) return rc;
-    int launches = 0;
     const int first = f_is_ell ? 0 : 1;
     if (!f_is_ell) {
         // piece 0 is swapped with the whole GPU before anything can run
+        Timed t(h, PS_K_EXCHANGE);
         CUDA_TRY(h, swap_piece(0, h->stream, 0));
         rc = barrier(h);
         if (rc) return rc;
     }
     CUDA_TRY(h, cudaEventRecord(h->xev[0], h->stream));
     CUDA_TRY(h, cudaStreamWaitEvent(h->xstream, h->xev[0], 0));
-    for (int j = first; j < P; ++j) {
-        CUDA_TRY(h, swap_piece(j, h->xstream, h->swap_ctas));
-        rc = barrier_on(h, h->xstream, 1);
-        if (rc) return rc;
-        CUDA_TRY(h, cudaEventRecord(h->xev[1 + j], h->xstream));
+    {
+        // the overlapped swap pieces, timed on the stream they run on: kernel_ms[EXCHANGE] then
+        // covers every swapped byte (and overlaps the pass's own time)
+        Timed t(h, PS_K_EXCHANGE, h->xstream);
+        for (int j = first; j < P; ++j) {
+            CUDA_TRY(h, swap_piece(j, h->xstream, h->swap_ctas));
+            rc = barrier_on(h, h->xstream, 1);
+            if (rc) return rc;
+            CUDA_TRY(h, cudaEventRecord(h->xev[1 + j], h->xstream));
+        }
     }
     const uint64_t lbit = 1ull << ex.ell;
     if (f_is_ell) {
         rc = run_pass(lbit, (uint64_t)ex.keep << ex.ell);  // kept side: no swapped slot
         if (rc) return rc;
-        ++launches;
     }
     for (int j = 0; j < P; ++j) {
         if (j >= first) CUDA_TRY(h, cudaStreamWaitEvent(h->stream, h->xev[1 + j], 0));
@@ -778,14 +1011,14 @@ static int exchange_overlap(ps_state* h, const Pass& ex, const Pass& np) {
         const uint64_t fv = deposit((uint64_t)j, pbits) | (f_is_ell ? (uint64_t)(1 - ex.keep) << ex.ell : 0);
         rc = run_pass(fm, fv);
         if (rc) return rc;
-        ++launches;
     }
     const double region = (double)(rows * row_amps * h->amp_bytes);
     h->stats.nvlink_bytes += region;
     h->stats.exchanges += 1;
     h->stats.launches[PS_K_EXCHANGE] += 1;
     h->stats.algo_bytes[PS_K_EXCHANGE] += region * 2.0;
-    h->stats.launches[np.kind] += (uint64_t)launches;
+    // the pass pieces are one logical pass over the local state
+    h->stats.launches[np.kind] += 1;
     h->stats.rotations_by[np.kind] += (uint64_t)np.rot_count;
     h->stats.algo_bytes[np.kind] += 2.0 * (double)h->amp_bytes * (double)local_amps(h);
     h->stats.passes += 1;
@@ -827,6 +1060,112 @@ static int exchange_full(ps_state* h, const Pass& p, const DevRot* d_rec, const 
     h->stats.exchanges += 1;
     h->stats.rotations_by[PS_K_EXCHANGE] += 1;
     h->stats.algo_bytes[PS_K_EXCHANGE] += (double)(N * s) * 3.0;
+    return PS_OK;
+}
+
+// the same full exchange for the virtual ranks of a group: per chunk step, every rank first stages
+// its partner's chunks t and u (the "receive"), then every rank updates its own chunks
+static int exchange_full_group(const RankSet& rs, const std::vector<Plan*>& plans, size_t pi) {
+    ps_state* h0 = rs[0];
+    const Pass& p0 = plans[0]->passes[pi];
+    const size_t s = h0->amp_bytes;
+    const uint64_t N = local_amps(h0);
+    uint64_t C = std::max<uint64_t>(1, h0->chunk_bytes / s);
+    if (C > N) C = N;
+    C = 1ull << highest_bit(C);
+    const uint64_t delta = plans[0]->rots[p0.rot_begin].x / C;
+    for (ps_state* r : rs) {
+        int rc = ensure_xstage(r, 2 * C * s);
+        if (rc) return rc;
+    }
+    const uint64_t nchunks = N / C;
+    for (uint64_t t = 0; t < nchunks; ++t) {
+        const uint64_t u = t ^ delta;
+        if (u < t) continue;
+        for (ps_state* r : rs) {
+            const ps_state* q = rs[r->rank ^ (int)p0.gx];
+            char* st = (char*)r->d_xstage[0];
+            CUDA_TRY(r, cudaMemcpyAsync(st, (const char*)q->d_state + t * C * s, C * s, cudaMemcpyDeviceToDevice, r->stream));
+            if (u != t)
+                CUDA_TRY(r, cudaMemcpyAsync(st + C * s, (const char*)q->d_state + u * C * s, C * s,
+                                            cudaMemcpyDeviceToDevice, r->stream));
+        }
+        for (size_t k = 0; k < rs.size(); ++k) {
+            ps_state* r = rs[k];
+            const Pass& p = plans[k]->passes[pi];
+            const char* st = (const char*)r->d_xstage[0];
+            const char* pu = (u != t) ? st + C * s : st;
+            CUDA_TRY(r, launch_full_update(r->dtype, r->d_state, pu, t * C, C, u * C, r->d_rots + p.rot_begin, r->stream));
+            if (u != t)
+                CUDA_TRY(r, launch_full_update(r->dtype, r->d_state, st, u * C, C, t * C, r->d_rots + p.rot_begin,
+                                               r->stream));
+            r->stats.nvlink_bytes += (double)(C * s * (u != t ? 2 : 1));
+        }
+    }
+    for (ps_state* r : rs) {
+        r->stats.exchanges += 1;
+        r->stats.launches[PS_K_EXCHANGE] += 1;
+        r->stats.rotations_by[PS_K_EXCHANGE] += 1;
+        r->stats.algo_bytes[PS_K_EXCHANGE] += (double)(N * s) * 3.0;
+    }
+    return PS_OK;
+}
+
+// ------------------------------------------------------------------------------------------
+// fused exchange + tile pass (NEXT-2): the half-vector exchange E(gx, ell)
+// and the tile pass after it run as ONE kernel.  Each rank's tiles read their kept half from local
+// memory and the other half straight from the partner's slots through the peer pointer, compute,
+// and store every element locally in the new layout.  A store into a slot the partner still has to
+// read waits on a per-tile flag the partner raises (release, system scope) once its reads of that
+// tile are done; both ranks walk their tiles in the same order, so no swap, no staging and no
+// barrier after the pass.  Emulated ranks run as one kernel over all ranks' slices.
+
+static bool can_fuse(const ps_state* h, const Pass& ex, const Pass* np) {
+    return h->fused && h->p2p && h->transport && h->world > 1 && ex.kind == PASS_EXCHANGE && !ex.full && np &&
+           (np->kind == PASS_TILE || np->kind == PASS_COSET) && h->tile_tma == 2 && !np->spec;
+}
+
+static int exchange_fused(const RankSet& rs, const std::vector<Plan*>& plans, size_t pi) {
+    ps_state* h0 = rs[0];
+    const Pass& ex0 = plans[0]->passes[pi];
+    const Pass& np0 = plans[0]->passes[pi + 1];
+    const size_t ntiles = (size_t)1 << __builtin_popcountll(np0.free_mask);
+    if (ntiles > h0->flags_cap) return fail(PS_EUNSUPPORTED, "fused exchange: more tiles than flag words");
+    int rc = barrier(h0);  // every rank's earlier passes are done before anyone reads a peer slot
+    if (rc) return rc;
+    std::vector<XTileRank> xr(rs.size());
+    for (size_t k = 0; k < rs.size(); ++k) {
+        ps_state* r = rs[k];
+        const Pass& ex = plans[k]->passes[pi];
+        const Pass& np = plans[k]->passes[pi + 1];
+        const int partner = r->rank ^ (int)ex.gx;
+        r->epoch += 1;
+        xr[k].a = r->d_state;
+        xr[k].peer = r->peers[partner];
+        xr[k].flags = r->d_flags;
+        xr[k].peer_flags = r->peer_flags[partner];
+        xr[k].subs = r->d_subs + np.sub_begin;
+        xr[k].trots = r->d_trots;
+        xr[k].rank = r->rank;
+        xr[k].keep = ex.keep;
+    }
+    {
+        Timed t(h0, PS_K_XTILE);
+        CUDA_TRY(h0, launch_xtile(h0->dtype, xr.data(), (int)xr.size(), np0, h0->d_offs + np0.off_begin,
+                                  plans[0]->offsets.data() + np0.off_begin, ex0.ell, h0->epoch, h0->stream,
+                                  h0->grid_cap));
+    }
+    for (size_t k = 0; k < rs.size(); ++k) {
+        ps_state* r = rs[k];
+        const Pass& np = plans[k]->passes[pi + 1];
+        // one pass over the local state (half of it read through the peer pointer), no swap
+        r->stats.nvlink_fused_bytes += (double)(local_amps(r) / 2 * r->amp_bytes);
+        r->stats.exchanges += 1;
+        r->stats.launches[PS_K_XTILE] += 1;
+        r->stats.rotations_by[PS_K_XTILE] += (uint64_t)np.rot_count;
+        r->stats.algo_bytes[PS_K_XTILE] += 2.0 * (double)r->amp_bytes * (double)local_amps(r);
+        r->stats.passes += 1;
+    }
     return PS_OK;
 }
 
@@ -890,111 +1229,147 @@ static PlanConfig plan_config(const ps_state* h) {
     return cfg;
 }
 
-// the paper's step (i) + (ii): B <- conj(w_k) A_(k xor gx) via a full-partition exchange, butterfly
-static int mirror_begin(ps_state* h, const Pass& p) {
+// the paper's step (i): B <- A_(k xor gx) via a full-partition exchange
+static int mirror_fetch(ps_state* h, const Pass& p) {
     if (!h->d_mirror) return fail(PS_ESTATE, "mirror buffer missing (PS_OPT_LAYOUT=2)");
     const int partner = h->rank ^ (int)p.gx;
     const uint64_t N = local_amps(h);
     const size_t bytes = h->amp_bytes * N;
-    {
-        Timed t(h, PS_K_EXCHANGE);
-        if (h->p2p && h->transport) {
-            int rc = barrier(h);
-            if (rc) return rc;
-            CUDA_TRY(h, launch_p2p_copy(h->dtype, h->d_mirror, h->peers[partner], N, h->stream));
-            rc = barrier(h);  // the partner may overwrite its A (butterfly) only after my read
-            if (rc) return rc;
-        } else {
-            for (size_t off = 0; off < bytes; off += h->chunk_bytes) {
-                const size_t len = std::min(h->chunk_bytes, bytes - off);
-                NCCL_TRY(h, ncclGroupStart());
-                NCCL_TRY(h, ncclSend((const char*)h->d_state + off, len, ncclChar, partner, h->comm, h->stream));
-                NCCL_TRY(h, ncclRecv((char*)h->d_mirror + off, len, ncclChar, partner, h->comm, h->stream));
-                NCCL_TRY(h, ncclGroupEnd());
-            }
+    Timed t(h, PS_K_EXCHANGE);
+    if (h->p2p && h->transport) {
+        int rc = barrier(h);
+        if (rc) return rc;
+        CUDA_TRY(h, launch_p2p_copy(h->dtype, h->d_mirror, h->peers[partner], N, h->stream));
+        rc = barrier(h);  // the partner may overwrite its A (butterfly) only after my read
+        if (rc) return rc;
+    } else {
+        for (size_t off = 0; off < bytes; off += h->chunk_bytes) {
+            const size_t len = std::min(h->chunk_bytes, bytes - off);
+            NCCL_TRY(h, ncclGroupStart());
+            NCCL_TRY(h, ncclSend((const char*)h->d_state + off, len, ncclChar, partner, h->comm, h->stream));
+            NCCL_TRY(h, ncclRecv((char*)h->d_mirror + off, len, ncclChar, partner, h->comm, h->stream));
+            NCCL_TRY(h, ncclGroupEnd());
         }
-        h->stats.exchanges += 1;
-        h->stats.launches[PS_K_EXCHANGE] += 1;
-        h->stats.nvlink_bytes += (double)bytes;
-        h->stats.algo_bytes[PS_K_EXCHANGE] += (double)bytes * 2.0;
     }
-    Timed t(h, PS_K_MIRROR);
-    CUDA_TRY(h, launch_butterfly(h->dtype, h->d_state, h->d_mirror, N, (int)p.wr, (int)p.wi, h->stream));
-    h->stats.launches[PS_K_MIRROR] += 1;
-    h->stats.algo_bytes[PS_K_MIRROR] += 4.0 * (double)bytes;
+    h->stats.exchanges += 1;
+    h->stats.launches[PS_K_EXCHANGE] += 1;
+    h->stats.nvlink_bytes += (double)bytes;
+    h->stats.algo_bytes[PS_K_EXCHANGE] += (double)bytes * 2.0;
     return PS_OK;
 }
 
-static int execute_plan(ps_state* h, const Plan& plan) {
-    int rc = upload_plan(h, plan);
-    if (rc) return rc;
-    h->cur_plan = &plan;
+// step (ii): B <- conj(w_k) B, butterfly A, B
+static int mirror_butterfly(ps_state* h, const Pass& p) {
+    const uint64_t N = local_amps(h);
+    Timed t(h, PS_K_MIRROR);
+    CUDA_TRY(h, launch_butterfly(h->dtype, h->d_state, h->d_mirror, N, (int)p.wr, (int)p.wi, h->stream));
+    h->stats.launches[PS_K_MIRROR] += 1;
+    h->stats.algo_bytes[PS_K_MIRROR] += 4.0 * (double)(h->amp_bytes * N);
+    return PS_OK;
+}
+
+// one pass of one rank that needs no other rank's data in the same phase
+static int execute_pass(ps_state* h, const Plan& plan, size_t pi, void** target) {
+    const Pass& p = plan.passes[pi];
     const double pass_bytes = 2.0 * (double)h->amp_bytes * (double)local_amps(h);
-    void* target = h->d_state;  // MIRROR_SWITCH redirects passes to the mirror buffer
-    for (size_t pi = 0; pi < plan.passes.size(); ++pi) {
-        const Pass& p = plan.passes[pi];
-        const Pass* next = pi + 1 < plan.passes.size() ? &plan.passes[pi + 1] : nullptr;
-        if (p.kind == PASS_EXCHANGE && can_overlap(h, p, next)) {
-            rc = exchange_overlap(h, p, *next);
-            if (rc) return rc;
+    switch (p.kind) {
+    case PASS_STREAM: {
+        Timed t(h, PS_K_STREAM);
+        CUDA_TRY(h, launch_stream(h->dtype, *target, h->nl, p, h->d_rots, h->vec256, h->stream));
+        break;
+    }
+    case PASS_TILE:
+    case PASS_COSET: {
+        Timed t(h, p.kind);
+        CUDA_TRY(h, launch_tile(h->dtype, *target, h->nl, p, h->d_subs, h->d_trots, h->d_offs, h->tile_tma,
+                                h->tile_tune, h->stream, plan.subs.data(), plan.trots.data(), h->grid_cap));
+        break;
+    }
+    case PASS_MIRROR_SWITCH:
+        *target = h->d_mirror;
+        return PS_OK;
+    case PASS_MIRROR_END: {
+        Timed t(h, PS_K_MIRROR);
+        CUDA_TRY(h, launch_recombine(h->dtype, h->d_state, h->d_mirror, local_amps(h), h->stream));
+        h->stats.launches[PS_K_MIRROR] += 1;
+        h->stats.algo_bytes[PS_K_MIRROR] += 1.5 * pass_bytes;
+        *target = h->d_state;
+        return PS_OK;
+    }
+    case PASS_PERMUTE: {
+        Timed t(h, PS_K_PERMUTE);
+        CUDA_TRY(h, launch_permute(h->dtype, h->d_state, h->nl, p.ell, p.ell2, h->stream));
+        h->stats.launches[PS_K_PERMUTE] += 1;
+        h->stats.algo_bytes[PS_K_PERMUTE] += pass_bytes / 2;  // half the amplitudes move
+        return PS_OK;
+    }
+    case PASS_EXCHANGE: {
+        Timed t(h, PS_K_EXCHANGE);
+        int rc = p.full ? exchange_full(h, p, h->d_rots + p.rot_begin, plan.rots[p.rot_begin]) : exchange_half(h, p);
+        if (rc) return rc;
+        h->stats.launches[PS_K_EXCHANGE] += 1;
+        return PS_OK;
+    }
+    default:
+        return fail(PS_EINVAL, "internal: unknown pass kind");
+    }
+    h->stats.launches[p.kind] += 1;
+    h->stats.rotations_by[p.kind] += (uint64_t)p.rot_count;
+    h->stats.algo_bytes[p.kind] += pass_bytes;
+    h->stats.passes += 1;
+    return PS_OK;
+}
+
+// executes one plan per rank of the set, pass by pass in lockstep (SPMD plans: the same passes on
+// every rank, rank-specific signs and exchange sides)
+static int execute_plans(const RankSet& rs, const std::vector<Plan*>& plans) {
+    const size_t G = rs.size();
+    const size_t np = plans[0]->passes.size();
+    for (size_t k = 0; k < G; ++k) {
+        if (plans[k]->passes.size() != np) return fail(PS_EINVAL, "internal: rank plans differ");
+        int rc = upload_plan(rs[k], *plans[k]);
+        if (rc) return rc;
+        rs[k]->cur_plan = plans[k];
+    }
+    std::vector<void*> target(G);
+    for (size_t k = 0; k < G; ++k) target[k] = rs[k]->d_state;
+    int rc = PS_OK;
+    for (size_t pi = 0; pi < np && !rc; ++pi) {
+        const Pass& p0 = plans[0]->passes[pi];
+        const Pass* next = pi + 1 < np ? &plans[0]->passes[pi + 1] : nullptr;
+        if (p0.kind == PASS_EXCHANGE && G <= 8 && can_fuse(rs[0], p0, next)) {
+            rc = exchange_fused(rs, plans, pi);
+            ++pi;  // the next pass ran inside the fused kernel
+            continue;
+        }
+        if (G == 1 && p0.kind == PASS_EXCHANGE && can_overlap(rs[0], p0, next)) {
+            rc = exchange_overlap(rs[0], p0, *next);
             ++pi;  // the next pass ran inside the overlap
             continue;
         }
-        switch (p.kind) {
-        case PASS_STREAM: {
-            Timed t(h, PS_K_STREAM);
-            CUDA_TRY(h, launch_stream(h->dtype, target, h->nl, p, h->d_rots, h->vec256, h->stream));
-            break;
-        }
-        case PASS_TILE:
-        case PASS_COSET: {
-            Timed t(h, p.kind);
-            CUDA_TRY(h, launch_tile(h->dtype, target, h->nl, p, h->d_subs, h->d_trots, h->d_offs, h->tile_tma,
-                                    h->tile_tune, h->stream, plan.subs.data(), plan.trots.data()));
-            break;
-        }
-        case PASS_MIRROR_BEGIN:
-            rc = mirror_begin(h, p);
-            if (rc) return rc;
-            target = h->d_state;
-            continue;
-        case PASS_MIRROR_SWITCH:
-            target = h->d_mirror;
-            continue;
-        case PASS_MIRROR_END: {
-            Timed t(h, PS_K_MIRROR);
-            CUDA_TRY(h, launch_recombine(h->dtype, h->d_state, h->d_mirror, local_amps(h), h->stream));
-            h->stats.launches[PS_K_MIRROR] += 1;
-            h->stats.algo_bytes[PS_K_MIRROR] += 1.5 * pass_bytes;
-            target = h->d_state;
+        if (p0.kind == PASS_EXCHANGE && p0.full && rs[0]->emulated) {
+            rc = exchange_full_group(rs, plans, pi);
             continue;
         }
-        case PASS_PERMUTE: {
-            Timed t(h, PS_K_PERMUTE);
-            CUDA_TRY(h, launch_permute(h->dtype, h->d_state, h->nl, p.ell, p.ell2, h->stream));
-            h->stats.launches[PS_K_PERMUTE] += 1;
-            h->stats.algo_bytes[PS_K_PERMUTE] += pass_bytes / 2;  // half the amplitudes move
+        if (p0.kind == PASS_MIRROR_BEGIN) {
+            // every rank fetches its partner's A before any rank's butterfly overwrites its own
+            for (size_t k = 0; k < G && !rc; ++k) rc = mirror_fetch(rs[k], plans[k]->passes[pi]);
+            for (size_t k = 0; k < G && !rc; ++k) {
+                rc = mirror_butterfly(rs[k], plans[k]->passes[pi]);
+                target[k] = rs[k]->d_state;
+            }
             continue;
         }
-        case PASS_EXCHANGE: {
-            Timed t(h, PS_K_EXCHANGE);
-            if (p.full)
-                rc = exchange_full(h, p, h->d_rots + p.rot_begin, plan.rots[p.rot_begin]);
-            else
-                rc = exchange_half(h, p);
-            if (rc) return rc;
-            h->stats.launches[PS_K_EXCHANGE] += 1;
-            continue;
-        }
-        default:
-            return fail(PS_EINVAL, "internal: unknown pass kind");
-        }
-        h->stats.launches[p.kind] += 1;
-        h->stats.rotations_by[p.kind] += (uint64_t)p.rot_count;
-        h->stats.algo_bytes[p.kind] += pass_bytes;
-        h->stats.passes += 1;
+        for (size_t k = 0; k < G && !rc; ++k) rc = execute_pass(rs[k], *plans[k], pi, &target[k]);
     }
-    return PS_OK;
+    if (rc && np > 0) {
+        // passes already enqueued have transformed (part of) the state and its layout: the handle
+        // no longer describes its amplitudes
+        const std::string msg = ps_last_error();
+        poison_all(rs);
+        set_last_error(msg + " (handle poisoned: the plan failed after its first pass was enqueued)");
+    }
+    return rc;
 }
 
 static bool layout_canonical(const ps_state* h) {
@@ -1008,14 +1383,17 @@ static void reset_layout(ps_state* h) {
 }
 
 // brings the state back to the canonical layout (rank = top qubits, identity within ranks)
-static int restore_layout(ps_state* h) {
-    if (h->world == 1 || layout_canonical(h)) return PS_OK;
-    PlanConfig cfg = plan_config(h);
-    Plan rp;
-    make_restore_plan(cfg, h->perm, &rp);
-    int rc = execute_plan(h, rp);
+static int restore_layout(const RankSet& rs) {
+    if (rs[0]->world == 1 || layout_canonical(rs[0])) return PS_OK;
+    std::vector<Plan> rp(rs.size());
+    std::vector<Plan*> pp(rs.size());
+    for (size_t k = 0; k < rs.size(); ++k) {
+        make_restore_plan(plan_config(rs[k]), rs[k]->perm, &rp[k]);
+        pp[k] = &rp[k];
+    }
+    int rc = execute_plans(rs, pp);
     if (rc) return rc;
-    reset_layout(h);
+    for (ps_state* r : rs) reset_layout(r);
     return PS_OK;
 }
 
@@ -1026,74 +1404,212 @@ extern "C" int ps_apply_rotations(ps_handle h, const uint64_t* xmask, const uint
     int rc = validate_rotations(h->n, xmask, zmask, angle, count, &err);
     if (rc) return fail(rc, "ps_apply_rotations: " + err);
     if (count == 0) return PS_OK;
-    Plan& plan = h->plan;
-    make_plan(plan_config(h), xmask, zmask, angle, count, &plan);
-    rc = execute_plan(h, plan);
+    RankSet rs = ranks_of(h);
+    std::vector<Plan*> plans;
+    for (ps_state* r : rs) {
+        make_plan(plan_config(r), xmask, zmask, angle, count, &r->plan);
+        plans.push_back(&r->plan);
+    }
+    rc = execute_plans(rs, plans);
     if (rc) return rc;
-    if (plan.perm_out.size() == h->perm.size())
-        h->perm = plan.perm_out;
-    else
-        reset_layout(h);
-    h->stats.rotations += count;
+    for (ps_state* r : rs) {
+        if (r->plan.perm_out.size() == r->perm.size())
+            r->perm = r->plan.perm_out;
+        else
+            reset_layout(r);
+        r->stats.rotations += count;
+    }
     return PS_OK;
 }
 
 // ------------------------------------------------------------------------------------------
 // reductions
 
-static int allreduce_result(ps_state* h, int nvals) {
-    if (h->world > 1)
-        NCCL_TRY(h, ncclAllReduce(h->d_result, h->d_result, (size_t)nvals, ncclDouble, ncclSum, h->comm, h->stream));
-    CUDA_TRY(h, cudaMemcpyAsync(h->h_result, h->d_result, sizeof(double) * nvals, cudaMemcpyDeviceToHost, h->stream));
-    CUDA_TRY(h, cudaStreamSynchronize(h->stream));
-    return PS_OK;
-}
-
-static int reduce_norm(ps_state* h, double* out) {
-    {
+static int reduce_norm(const RankSet& rs, double* out) {
+    for (ps_state* h : rs) {
         Timed t(h, PS_K_REDUCE);
         CUDA_TRY(h, launch_norm(h->dtype, h->d_state, local_amps(h), h->d_partial, h->d_result, h->stream));
         h->stats.launches[PS_K_REDUCE] += 1;
         h->stats.algo_bytes[PS_K_REDUCE] += (double)h->amp_bytes * (double)local_amps(h);
     }
-    int rc = allreduce_result(h, 1);
-    if (rc) return rc;
-    *out = h->h_result[0];
-    return PS_OK;
+    return sum_results(rs, 1, out);
 }
 
 extern "C" int ps_norm(ps_handle h, double* out) {
     CHECK_HANDLE(h);
     if (!out) return fail(PS_EINVAL, "NULL out");
-    return reduce_norm(h, out);
+    return reduce_norm(ranks_of(h), out);
 }
 
 extern "C" int ps_inner(ps_handle a, ps_handle b, double* out) {
     CHECK_HANDLE(a);
     CHECK_HANDLE(b);
     if (!out) return fail(PS_EINVAL, "NULL out");
-    if (a->n != b->n || a->dtype != b->dtype || a->world != b->world || a->rank != b->rank || a->device != b->device)
-        return fail(PS_EINVAL, "ps_inner: handles differ in n, dtype, world, rank or device");
-    int rc0 = restore_layout(a);
-    if (!rc0) rc0 = restore_layout(b);
+    if (a->n != b->n || a->dtype != b->dtype || a->world != b->world || a->rank != b->rank || a->device != b->device ||
+        a->is_group() != b->is_group())
+        return fail(PS_EINVAL, "ps_inner: handles differ in n, dtype, world, rank, device or emulation");
+    RankSet ra = ranks_of(a), rb = ranks_of(b);
+    int rc0 = restore_layout(ra);
+    if (!rc0) rc0 = restore_layout(rb);
     if (rc0) return rc0;
     if (b->stream != a->stream) {
         CUDA_TRY(b, cudaStreamSynchronize(b->stream));
     }
-    {
-        Timed t(a, PS_K_REDUCE);
-        CUDA_TRY(a, launch_inner(a->dtype, a->d_state, b->d_state, local_amps(a), a->d_partial, a->d_result, a->stream));
-        a->stats.launches[PS_K_REDUCE] += 1;
-        a->stats.algo_bytes[PS_K_REDUCE] += 2.0 * (double)a->amp_bytes * (double)local_amps(a);
+    for (size_t k = 0; k < ra.size(); ++k) {
+        ps_state* x = ra[k];
+        Timed t(x, PS_K_REDUCE);
+        CUDA_TRY(x, launch_inner(x->dtype, x->d_state, rb[k]->d_state, local_amps(x), x->d_partial, x->d_result, x->stream));
+        x->stats.launches[PS_K_REDUCE] += 1;
+        x->stats.algo_bytes[PS_K_REDUCE] += 2.0 * (double)x->amp_bytes * (double)local_amps(x);
     }
-    int rc = allreduce_result(a, 2);
-    if (rc) return rc;
-    out[0] = a->h_result[0];
-    out[1] = a->h_result[1];
+    return sum_results(ra, 2, out);
+}
+
+// expectation (R17): terms are grouped by their upper X-part gx; a gx != 0 group runs after a half
+// exchange E(gx, ell) with a free local pivot ell (so every pair is local), grouped again by
+// physical x (one read pass per x); a term whose local X-part covers every local bit
+// (no free pivot) is summed against its partner's chunks (read-only full exchange)
+struct ExpSeg {
+    uint64_t gx = 0;
+    int ell = 0, keep = 0;
+    bool full = false;                // single term, no free pivot
+    uint64_t fx = 0, fz = 0;          // full: local x / z parts
+    int fy = 0, fsgn = 0;
+    double fcoeff = 0.0;
+    std::vector<uint64_t> xorder;
+    std::vector<DevTerm> flat;
+    std::vector<std::pair<size_t, size_t>> ranges;
+};
+
+static void expectation_plan(const ps_state* h, const uint64_t* xmask, const uint64_t* zmask, const double* coeff,
+                             size_t count, std::vector<ExpSeg>* segs) {
+    const int nl = h->nl;
+    const uint64_t lmask = (1ull << nl) - 1;
+    const uint64_t rank = (uint64_t)h->rank;
+    std::vector<uint64_t> gorder;
+    std::map<uint64_t, std::vector<size_t>> bygx;
+    for (size_t l = 0; l < count; ++l) {
+        const uint64_t gx = xmask[l] >> nl;
+        if (!bygx.count(gx)) gorder.push_back(gx);
+        bygx[gx].push_back(l);
+    }
+    std::stable_sort(gorder.begin(), gorder.end(), [](uint64_t a, uint64_t b) { return (a == 0) > (b == 0); });
+    for (uint64_t gx : gorder) {
+        const std::vector<size_t>& idx = bygx[gx];
+        size_t pos = 0;
+        while (pos < idx.size()) {
+            ExpSeg sg;
+            sg.gx = gx;
+            size_t end = pos;
+            uint64_t U = 0;
+            if (gx == 0) {
+                end = idx.size();
+            } else {
+                while (end < idx.size() && (U | (xmask[idx[end]] & lmask)) != lmask) U |= xmask[idx[end++]] & lmask;
+                if (end == pos) {
+                    const size_t l = idx[pos];
+                    sg.full = true;
+                    sg.fx = xmask[l] & lmask;
+                    sg.fz = zmask[l] & lmask;
+                    sg.fy = __builtin_popcountll(xmask[l] & zmask[l]) & 3;
+                    sg.fsgn = __builtin_parityll((zmask[l] >> nl) & rank);
+                    sg.fcoeff = coeff[l];
+                    segs->push_back(std::move(sg));
+                    ++pos;
+                    continue;
+                }
+            }
+            if (gx) {
+                sg.ell = highest_bit(lmask & ~U);
+                sg.keep = (int)((rank >> __builtin_ctzll(gx)) & 1);
+            }
+            std::map<uint64_t, std::vector<DevTerm>> byx;
+            for (size_t q = pos; q < end; ++q) {
+                const size_t l = idx[q];
+                const uint64_t xh = xmask[l] >> nl, xl = xmask[l] & lmask, zh = zmask[l] >> nl, zl = zmask[l] & lmask;
+                uint64_t xp = xl, zp = zl;
+                int sgn = __builtin_parityll(zh & rank);
+                if (gx) {
+                    const int kappa = __builtin_parityll(zh & gx) ^ (int)((zl >> sg.ell) & 1);
+                    xp = xl ^ (xh ? (1ull << sg.ell) : 0);
+                    zp = zl ^ (kappa ? (1ull << sg.ell) : 0);
+                    sgn ^= sg.keep & kappa;
+                }
+                const int y = __builtin_popcountll(xmask[l] & zmask[l]) & 3;
+                // Re(i^y sigma t): y=0 -> tr, 1 -> -ti, 2 -> -tr, 3 -> ti ; pairs counted twice (i and j)
+                const double w = (xp ? 2.0 : 1.0) * coeff[l] * (sgn ? -1.0 : 1.0);
+                DevTerm t;
+                t.z = zp;
+                t.kr = (y == 0) ? w : (y == 2 ? -w : 0.0);
+                t.ki = (y == 1) ? -w : (y == 3 ? w : 0.0);
+                if (!byx.count(xp)) sg.xorder.push_back(xp);
+                byx[xp].push_back(t);
+            }
+            for (uint64_t xp : sg.xorder) {
+                sg.ranges.push_back({sg.flat.size(), byx[xp].size()});
+                sg.flat.insert(sg.flat.end(), byx[xp].begin(), byx[xp].end());
+            }
+            segs->push_back(std::move(sg));
+            pos = end;
+        }
+    }
+}
+
+// Re sum_i conj(psi_(i xor x)) w(i) psi_i over the local i of every rank, for one term without a
+// free pivot: the partner's chunk u = t xor delta is staged (NCCL send/recv, or copied from the
+// group's slices) against every own chunk t; nothing is modified
+static int expectation_full(const RankSet& rs, const std::vector<const ExpSeg*>& sg, double* out) {
+    ps_state* h0 = rs[0];
+    const size_t s = h0->amp_bytes;
+    const uint64_t N = local_amps(h0);
+    uint64_t C = std::max<uint64_t>(1, h0->chunk_bytes / s);
+    if (C > N) C = N;
+    C = 1ull << highest_bit(C);
+    const uint64_t delta = sg[0]->fx / C;
+    for (ps_state* r : rs) {
+        int rc = ensure_xstage(r, C * s);
+        if (rc) return rc;
+    }
+    double total = 0.0;
+    const uint64_t nchunks = N / C;
+    for (uint64_t t0 = 0; t0 < nchunks; t0 += 64) {
+        const uint64_t nb = std::min<uint64_t>(64, nchunks - t0);
+        for (uint64_t q = 0; q < nb; ++q) {
+            const uint64_t t = t0 + q, u = t ^ delta;
+            for (size_t k = 0; k < rs.size(); ++k) {
+                ps_state* r = rs[k];
+                const int partner = r->rank ^ (int)sg[k]->gx;
+                if (r->emulated) {
+                    CUDA_TRY(r, cudaMemcpyAsync(r->d_xstage[0], (const char*)rs[partner]->d_state + u * C * s, C * s,
+                                                cudaMemcpyDeviceToDevice, r->stream));
+                } else {
+                    // the partner's own chunk t' = u pairs with my chunk u ^ delta = t: it sends u
+                    NCCL_TRY(r, ncclGroupStart());
+                    NCCL_TRY(r, ncclSend((const char*)r->d_state + u * C * s, C * s, ncclChar, partner, r->comm, r->stream));
+                    NCCL_TRY(r, ncclRecv(r->d_xstage[0], C * s, ncclChar, partner, r->comm, r->stream));
+                    NCCL_TRY(r, ncclGroupEnd());
+                }
+            }
+            for (size_t k = 0; k < rs.size(); ++k) {
+                ps_state* r = rs[k];
+                Timed tm(r, PS_K_REDUCE);
+                CUDA_TRY(r, launch_expect_cross(r->dtype, r->d_state, r->d_xstage[0], t * C, C, u * C, sg[k]->fx,
+                                                sg[k]->fz, sg[k]->fy, sg[k]->fsgn, r->d_partial, r->d_result + q,
+                                                r->stream));
+                r->stats.launches[PS_K_REDUCE] += 1;
+                r->stats.algo_bytes[PS_K_REDUCE] += 2.0 * (double)(C * s);
+                r->stats.nvlink_bytes += (double)(C * s);
+            }
+        }
+        double vals[64];
+        int rc = sum_results(rs, (int)nb, vals);
+        if (rc) return rc;
+        for (uint64_t q = 0; q < nb; ++q) total += vals[q];
+    }
+    *out = sg[0]->fcoeff * total;
     return PS_OK;
 }
 
-// expectation: terms grouped by physical x; global-X terms evaluated after a half exchange
 extern "C" int ps_expectation(ps_handle h, const uint64_t* xmask, const uint64_t* zmask, const double* coeff,
                               size_t count, double* out) {
     CHECK_HANDLE(h);
@@ -1103,114 +1619,65 @@ extern "C" int ps_expectation(ps_handle h, const uint64_t* xmask, const uint64_t
     if (rc) return fail(rc, "ps_expectation: " + err);
     *out = 0.0;
     if (count == 0) return PS_OK;
-    if ((rc = restore_layout(h))) return rc;
-    const int nl = h->nl;
-    const uint64_t lmask = (1ull << nl) - 1;
-    const uint64_t rank = (uint64_t)h->rank;
-    // segments: gx -> list of term indices (gx = 0 first), order of first appearance
-    std::vector<uint64_t> gorder;
-    std::map<uint64_t, std::vector<size_t>> bygx;
-    for (size_t l = 0; l < count; ++l) {
-        const uint64_t gx = xmask[l] >> nl;
-        if (!bygx.count(gx)) gorder.push_back(gx);
-        bygx[gx].push_back(l);
-    }
-    std::stable_sort(gorder.begin(), gorder.end(), [](uint64_t a, uint64_t b) { return (a == 0) > (b == 0); });
+    RankSet rs = ranks_of(h);
+    if ((rc = restore_layout(rs))) return rc;
+    std::vector<std::vector<ExpSeg>> segs(rs.size());
+    for (size_t k = 0; k < rs.size(); ++k) expectation_plan(rs[k], xmask, zmask, coeff, count, &segs[k]);
+    const uint64_t N = local_amps(rs[0]);
     double total = 0.0;
-    const uint64_t N = local_amps(h);
-    for (uint64_t gx : gorder) {
-        std::vector<size_t> idx = bygx[gx];
-        // split into sub-groups whose local x-parts leave a free pivot (always true for gx == 0)
-        size_t pos = 0;
-        while (pos < idx.size()) {
-            size_t end = pos;
-            uint64_t U = 0;
-            if (gx == 0) {
-                end = idx.size();
-            } else {
-                while (end < idx.size() && (U | (xmask[idx[end]] & lmask)) != lmask) U |= xmask[idx[end++]] & lmask;
-                if (end == pos) return fail(PS_EUNSUPPORTED, "ps_expectation: global-X term without a free local pivot");
-            }
-            int ell = 0, keep = 0;
-            if (gx) {
-                ell = highest_bit(lmask & ~U);
-                keep = (int)((rank >> __builtin_ctzll(gx)) & 1);
-            }
-            // physical terms grouped by physical x
-            std::map<uint64_t, std::vector<DevTerm>> byx;
-            std::vector<uint64_t> xorder;
-            for (size_t q = pos; q < end; ++q) {
-                const size_t l = idx[q];
-                const uint64_t xh = xmask[l] >> nl, xl = xmask[l] & lmask, zh = zmask[l] >> nl, zl = zmask[l] & lmask;
-                uint64_t xp = xl, zp = zl;
-                int sgn = __builtin_parityll(zh & rank);
-                if (gx) {
-                    const int kappa = __builtin_parityll(zh & gx) ^ (int)((zl >> ell) & 1);
-                    xp = xl ^ (xh ? (1ull << ell) : 0);
-                    zp = zl ^ (kappa ? (1ull << ell) : 0);
-                    sgn ^= keep & kappa;
-                }
-                const int y = __builtin_popcountll(xmask[l] & zmask[l]) & 3;
-                // Re(i^y sigma t): y=0 -> tr, 1 -> -ti, 2 -> -tr, 3 -> ti ; pairs counted twice (i and j)
-                const double w = (xp ? 2.0 : 1.0) * coeff[l] * (sgn ? -1.0 : 1.0);
-                DevTerm t;
-                t.z = zp;
-                t.kr = (y == 0) ? w : (y == 2 ? -w : 0.0);
-                t.ki = (y == 1) ? -w : (y == 3 ? w : 0.0);
-                if (!byx.count(xp)) xorder.push_back(xp);
-                byx[xp].push_back(t);
-            }
-            if (gx) {
-                Pass ex;
-                ex.kind = PASS_EXCHANGE;
-                ex.gx = gx;
-                ex.ell = ell;
-                ex.keep = keep;
-                Timed t(h, PS_K_EXCHANGE);
-                rc = exchange_half(h, ex);
-                if (rc) return rc;
-            }
-            size_t nterms = 0;
-            for (auto& kv : byx) nterms += kv.second.size();
-            rc = ensure_dev(h, &h->d_terms, &h->d_terms_cap, nterms);
-            if (rc) return rc;
-            std::vector<DevTerm> flat;
-            flat.reserve(nterms);
-            std::vector<std::pair<size_t, size_t>> ranges;
-            for (uint64_t xp : xorder) {
-                ranges.push_back({flat.size(), byx[xp].size()});
-                flat.insert(flat.end(), byx[xp].begin(), byx[xp].end());
-            }
-            CUDA_TRY(h, cudaMemcpyAsync(h->d_terms, flat.data(), flat.size() * sizeof(DevTerm), cudaMemcpyHostToDevice,
-                                        h->stream));
-            const size_t ng = xorder.size();
-            for (size_t gi = 0; gi < ng; gi += 64) {
-                const size_t nb = std::min<size_t>(64, ng - gi);
-                for (size_t q = 0; q < nb; ++q) {
-                    Timed t(h, PS_K_REDUCE);
-                    CUDA_TRY(h, launch_expect(h->dtype, h->d_state, N, xorder[gi + q], h->d_terms + ranges[gi + q].first,
-                                              (int)ranges[gi + q].second, h->d_partial, h->d_result + q, h->stream));
-                    h->stats.launches[PS_K_REDUCE] += 1;
-                    h->stats.algo_bytes[PS_K_REDUCE] += (double)h->amp_bytes * (double)N;
-                }
-                if (h->world > 1)
-                    NCCL_TRY(h, ncclAllReduce(h->d_result, h->d_result, nb, ncclDouble, ncclSum, h->comm, h->stream));
-                CUDA_TRY(h, cudaMemcpyAsync(h->h_result, h->d_result, sizeof(double) * nb, cudaMemcpyDeviceToHost, h->stream));
-                CUDA_TRY(h, cudaStreamSynchronize(h->stream));
-                for (size_t q = 0; q < nb; ++q) total += h->h_result[q];
-            }
-            if (gx) {
-                Pass ex;
-                ex.kind = PASS_EXCHANGE;
-                ex.gx = gx;
-                ex.ell = ell;
-                ex.keep = keep;
-                Timed t(h, PS_K_EXCHANGE);
-                rc = exchange_half(h, ex);
-                if (rc) return rc;
-            }
-            pos = end;
+    for (size_t si = 0; si < segs[0].size(); ++si) {
+        const ExpSeg& s0 = segs[0][si];
+        if (s0.full) {
+            std::vector<const ExpSeg*> sg;
+            for (auto& v : segs) sg.push_back(&v[si]);
+            double part = 0.0;
+            if ((rc = expectation_full(rs, sg, &part))) return rc;
+            total += part;
+            continue;
         }
+        auto exchange = [&]() -> int {
+            for (size_t k = 0; k < rs.size(); ++k) {
+                Pass ex;
+                ex.kind = PASS_EXCHANGE;
+                ex.gx = segs[k][si].gx;
+                ex.ell = segs[k][si].ell;
+                ex.keep = segs[k][si].keep;
+                Timed t(rs[k], PS_K_EXCHANGE);
+                int r2 = exchange_half(rs[k], ex);
+                if (r2) {
+                    poison_all(rs);  // the layout is half-way through an exchange
+                    return r2;
+                }
+            }
+            return PS_OK;
+        };
+        if (s0.gx && (rc = exchange())) return rc;
+        for (size_t k = 0; k < rs.size(); ++k) {
+            ps_state* r = rs[k];
+            const ExpSeg& sg = segs[k][si];
+            if ((rc = ensure_dev(r, &r->d_terms, &r->d_terms_cap, sg.flat.size()))) return rc;
+            CUDA_TRY(r, cudaMemcpyAsync(r->d_terms, sg.flat.data(), sg.flat.size() * sizeof(DevTerm),
+                                        cudaMemcpyHostToDevice, r->stream));
+        }
+        const size_t ng = s0.xorder.size();
+        for (size_t gi = 0; gi < ng; gi += 64) {
+            const size_t nb = std::min<size_t>(64, ng - gi);
+            for (size_t k = 0; k < rs.size(); ++k) {
+                ps_state* r = rs[k];
+                const ExpSeg& sg = segs[k][si];
+                for (size_t q = 0; q < nb; ++q) {
+                    Timed t(r, PS_K_REDUCE);
+                    CUDA_TRY(r, launch_expect(r->dtype, r->d_state, N, sg.xorder[gi + q], r->d_terms + sg.ranges[gi + q].first,
+                                              (int)sg.ranges[gi + q].second, r->d_partial, r->d_result + q, r->stream));
+                    r->stats.launches[PS_K_REDUCE] += 1;
+                    r->stats.algo_bytes[PS_K_REDUCE] += (double)r->amp_bytes * (double)N;
+                }
+            }
+            double vals[64];
+            if ((rc = sum_results(rs, (int)nb, vals))) return rc;
+            for (size_t q = 0; q < nb; ++q) total += vals[q];
+        }
+        if (s0.gx && (rc = exchange())) return rc;
     }
     *out = total;
     return PS_OK;
@@ -1220,40 +1687,46 @@ extern "C" int ps_expectation(ps_handle h, const uint64_t* xmask, const uint64_t
 
 extern "C" int ps_synchronize(ps_handle h) {
     CHECK_HANDLE(h);
-    CUDA_TRY(h, cudaStreamSynchronize(h->stream));
-    if (h->comm) {
-        ncclResult_t async_err = ncclSuccess;
-        ncclCommGetAsyncError(h->comm, &async_err);
-        if (async_err != ncclSuccess) {
-            h->poisoned = true;
-            return fail(PS_ENCCL, std::string("NCCL async error: ") + ncclGetErrorString(async_err));
+    for (ps_state* r : ranks_of(h)) {
+        CUDA_TRY(r, cudaStreamSynchronize(r->stream));
+        if (r->comm) {
+            ncclResult_t async_err = ncclSuccess;
+            ncclCommGetAsyncError(r->comm, &async_err);
+            if (async_err != ncclSuccess) {
+                r->poisoned = true;
+                return fail(PS_ENCCL, std::string("NCCL async error: ") + ncclGetErrorString(async_err));
+            }
         }
+        drain_timings(r);
     }
-    drain_timings(h);
     return PS_OK;
 }
 
+// a group reports its rank 0's counters (what rank 0 of a real run reports)
 extern "C" int ps_get_stats(ps_handle h, ps_stats* out) {
     if (!h || !out) return fail(PS_EINVAL, "NULL argument");
-    if (!h->poisoned) {
-        cudaSetDevice(h->device);
-        if (!h->pending.empty()) {
-            cudaStreamSynchronize(h->stream);
-            drain_timings(h);
+    ps_state* r = h->is_group() ? h->vranks[0] : h;
+    if (!any_poisoned(h)) {
+        cudaSetDevice(r->device);
+        if (!r->pending.empty()) {
+            cudaStreamSynchronize(r->stream);
+            drain_timings(r);
         }
     }
-    *out = h->stats;
+    *out = r->stats;
     return PS_OK;
 }
 
 extern "C" int ps_reset_stats(ps_handle h) {
     if (!h) return fail(PS_EINVAL, "NULL handle");
-    if (!h->poisoned) {
-        cudaSetDevice(h->device);
-        cudaStreamSynchronize(h->stream);
-        drain_timings(h);
+    for (ps_state* r : ranks_of(h)) {
+        if (!r->poisoned) {
+            cudaSetDevice(r->device);
+            cudaStreamSynchronize(r->stream);
+            drain_timings(r);
+        }
+        std::memset(&r->stats, 0, sizeof(r->stats));
     }
-    std::memset(&h->stats, 0, sizeof(h->stats));
     return PS_OK;
 }
 

@@ -823,6 +823,126 @@ __global__ void __launch_bounds__(MAXT, MINB)
 }
 
 // ------------------------------------------------------------------------------------------
+// K8 k_xtile: fused half-vector exchange + tile pass (NEXT-2; api.cpp exchange_fused).  The pass
+// runs in the layout AFTER the exchange E(gx, ell): a rank with keep = k finds the element of its
+// new slot j in its own slot j (bit ell of j == k) or in the partner's slot j ^ 2^ell.  Each tile's
+// sub-group 0 gathers straight from both (remote loads through the peer pointer); the CTA then
+// raises the partner's flag for this tile (release, system scope), and before its last sub-group
+// stores -- into its own slots, some of which the partner still has to read -- it waits until the
+// partner has raised this rank's flag for the partner's tile holding those slots (acquire).  The
+// rank with keep = 1 walks tile tau ^ dtau where the other walks tau (dtau: tile-index offset of
+// 2^ell), so CTA c of both ranks always waits on CTA c of the other in the same round (no
+// deadlock with co-resident grids).  Several ranks (an emulation group) run as one launch:
+// blockIdx.x / ctas_per_rank selects the rank.
+
+constexpr int kMaxXRanks = 8;
+struct XTileParams {
+    XTileRank r[kMaxXRanks];
+    BitRuns runs;
+    const uint64_t* offs;
+    uint64_t ntiles, free_mask, dtau;
+    int nranks, ctas_per_rank, kbits, cbits, nsub, ell;
+    uint32_t epoch;
+};
+
+__device__ __forceinline__ void flag_release(uint32_t* p, uint32_t v) {
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t flag_acquire(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kCosetThreads, 1) k_xtile(const __grid_constant__ XTileParams P) {
+    using V2 = typename SmemAmp<T>::V;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    const int rk = blockIdx.x / P.ctas_per_rank;
+    const uint32_t cta = blockIdx.x % P.ctas_per_rank;
+    const XTileRank& R = P.r[rk];
+    const int hbits = P.kbits - P.cbits;
+    uint64_t* soff = reinterpret_cast<uint64_t*>(smem_raw);
+    V2* tile = reinterpret_cast<V2*>(smem_raw + coset_off_bytes(hbits));
+    const uint32_t tid = threadIdx.x;
+    const uint32_t cmask = (1u << P.cbits) - 1u;
+    const int ncols = P.kbits - kSubDim;
+    for (uint32_t u = tid; u < (1u << hbits); u += blockDim.x) soff[u] = __ldg(&P.offs[u]);
+    __syncthreads();
+    V2* g = reinterpret_cast<V2*>(R.a);
+    const V2* peer = reinterpret_cast<const V2*>(R.peer);
+    const uint64_t lbit = 1ull << P.ell;
+    const uint64_t keepbit = (uint64_t)R.keep << P.ell;
+    for (uint64_t base = cta; base < P.ntiles; base += P.ctas_per_rank) {
+        const uint64_t tau = R.keep ? (base ^ P.dtau) : base;
+        const uint64_t i0 = deposit(tau, P.runs);
+        T vr[kSubAmps], vi[kSubAmps];
+        for (int s = 0; s < P.nsub; ++s) {
+            const SubHdr h = load_sub<0>(R.subs + s, tid, ncols);
+            if (s == 0) {
+                uint64_t gi[kSubAmps];
+                elem_index(gi, h, i0, soff, P.cbits, cmask);
+                V2 v[kSubAmps];
+#pragma unroll
+                for (int d = 0; d < kSubAmps; ++d)
+                    v[d] = ((gi[d] & lbit) == keepbit) ? __ldcs(&g[gi[d]]) : __ldcg(&peer[gi[d] ^ lbit]);
+#pragma unroll
+                for (int d = 0; d < kSubAmps; ++d) {
+                    vr[d] = v[d].x;
+                    vi[d] = v[d].y;
+                }
+            } else {
+#pragma unroll
+                for (int d = 0; d < kSubAmps; ++d) {
+                    const V2 v = tile[sub_local(h, d)];
+                    vr[d] = v.x;
+                    vi[d] = v.y;
+                }
+            }
+            sub_apply<T, 0, 0>(vr, vi, R.trots, h.rb, h.nr, h.r, i0);
+            if (h.F != 1.0) sub_scale<T>(vr, vi, (T)h.F);
+            if (s == 0) {
+                // every thread has consumed its loads of this tile: tell the partner its reads of my
+                // slots for this tile are done
+                __syncthreads();
+                if (tid == 0) flag_release(R.peer_flags + tau, P.epoch);
+            }
+            if (s == P.nsub - 1) {
+                // the partner's tile holding my slots of this tile (with bit ell != keep) is tau ^ dtau
+                if (tid == 0) {
+                    // bounded wait: a protocol error traps (a CUDA error) instead of hanging the GPU
+                    uint32_t spins = 0;
+                    while (flag_acquire(R.flags + (tau ^ P.dtau)) != P.epoch) {
+                        __nanosleep(128);
+                        if (++spins > (1u << 27)) __trap();
+                    }
+                }
+                __syncthreads();
+                uint64_t gi[kSubAmps];
+                elem_index(gi, h, i0, soff, P.cbits, cmask);
+#pragma unroll
+                for (int d = 0; d < kSubAmps; ++d) {
+                    V2 v;
+                    v.x = vr[d];
+                    v.y = vi[d];
+                    __stcs(&g[gi[d]], v);
+                }
+            } else {
+#pragma unroll
+                for (int d = 0; d < kSubAmps; ++d) {
+                    V2 v;
+                    v.x = vr[d];
+                    v.y = vi[d];
+                    tile[sub_local(h, d)] = v;
+                }
+                __syncthreads();
+            }
+        }
+        __syncthreads();  // last sub-group's shared reads before the next tile's writes
+    }
+}
+
+// ------------------------------------------------------------------------------------------
 // K2 / K7 (default): TMA-prefetched coset tile pass.  Each persistent CTA double-buffers tiles in
 // shared memory: while the sub-groups of tile m run on buffer m&1 (in place, the last one storing
 // straight to HBM), the TMA engine fills buffer (m+1)&1 with tile m+1 -- one cp.async.bulk per
@@ -1321,6 +1441,11 @@ int current_device() {
     return dev & 63;
 }
 
+// test knob (PS_OPT_GRID_CAP): caps the persistent tile grid so small states run several tiles per
+// CTA (the incremental tile bases and the next-tile prefetch); 0 = no cap
+thread_local int t_grid_cap = 0;
+uint64_t apply_grid_cap(uint64_t cap) { return (t_grid_cap > 0 && (uint64_t)t_grid_cap < cap) ? (uint64_t)t_grid_cap : cap; }
+
 int g_num_sms = 0;
 int num_sms() {
     if (g_num_sms == 0) {
@@ -1375,7 +1500,7 @@ cudaError_t launch_coset_k(T* a, int nl, const Pass& p, const DevSub* d_subs, co
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_coset<T, MAXT, MINB, SPEC>, threads, smem);
     if (occ < 1) occ = 1;
     const uint64_t ntiles = 1ull << __builtin_popcountll(p.free_mask);  // == 2^(nl - kbits) unless split
-    const uint64_t cap = (uint64_t)num_sms() * (uint64_t)occ * (uint64_t)(grid_mult > 0 ? grid_mult : 1);
+    const uint64_t cap = apply_grid_cap((uint64_t)num_sms() * (uint64_t)occ * (uint64_t)(grid_mult > 0 ? grid_mult : 1));
     const unsigned grid = (unsigned)(ntiles < cap ? ntiles : cap);
     k_coset<T, MAXT, MINB, SPEC><<<grid, threads, smem, s>>>(a, p.kbits, p.cbits, make_runs(p.free_mask),
                                                               d_offs + p.off_begin, ntiles, d_subs + p.sub_begin,
@@ -1393,6 +1518,13 @@ cudaError_t launch_coset_t(T* a, int nl, const Pass& p, const DevSub* d_subs, co
     if (occ_sel == 0 && sizeof(T) == 4 && !p.spec) occ_sel = 3;
     if (threads <= 128 && !p.spec && occ_sel == 3)
         return launch_coset_k<T, 128, 8, 0>(a, nl, p, d_subs, d_trots, d_offs, l2_prefetch, grid_mult, s);
+    // tiles of 2^13 (fp64) / 2^13..2^14 (fp32) amplitudes: one CTA of 512 / 1024 threads per SM
+    if (threads == 512 && !p.spec)
+        return launch_coset_k<T, 512, 1, 0>(a, nl, p, d_subs, d_trots, d_offs, l2_prefetch, grid_mult, s);
+    if constexpr (sizeof(T) == 4)
+        if (threads == 1024 && !p.spec)
+            return launch_coset_k<T, 1024, 1, 0>(a, nl, p, d_subs, d_trots, d_offs, l2_prefetch, grid_mult, s);
+    if (threads > kCosetThreads) return cudaErrorInvalidValue;
 #ifndef PS_ONLY_DEFAULT  // (development builds: the default kernels only, fast to compile)
     if (threads <= 128 && !p.spec && occ_sel == 1) return launch_coset_k<T, 128, 5, 0>(a, nl, p, d_subs, d_trots, d_offs, l2_prefetch, grid_mult, s);
     if (threads <= 128 && !p.spec && occ_sel == 2) return launch_coset_k<T, 128, 6, 0>(a, nl, p, d_subs, d_trots, d_offs, l2_prefetch, grid_mult, s);
@@ -1423,7 +1555,7 @@ cudaError_t launch_coset_param_k(T* a, const Pass& p, const PassRecs& recs, cons
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_coset_p<T, MAXT, MINB>, threads, smem);
     if (occ < 1) occ = 1;
     const uint64_t ntiles = 1ull << __builtin_popcountll(p.free_mask);
-    const uint64_t cap = (uint64_t)num_sms() * (uint64_t)occ * (uint64_t)(grid_mult > 0 ? grid_mult : 1);
+    const uint64_t cap = apply_grid_cap((uint64_t)num_sms() * (uint64_t)occ * (uint64_t)(grid_mult > 0 ? grid_mult : 1));
     const unsigned grid = (unsigned)(ntiles < cap ? ntiles : cap);
     k_coset_p<T, MAXT, MINB><<<grid, threads, smem, s>>>(a, p.kbits, p.cbits, make_runs(p.free_mask), d_offs + p.off_begin,
                                                           ntiles, p.sub_count, l2_prefetch, p.or_mask, p.free_mask,
@@ -1448,6 +1580,9 @@ cudaError_t launch_coset_param(T* a, const Pass& p, const DevSub* h_subs, const 
     const int threads = 1 << (p.kbits - kSubDim);
     if (sizeof(T) == 4 && occ_sel == 0 && threads <= 128)
         return launch_coset_param_k<T, 128, 8>(a, p, recs, d_offs, l2_prefetch, grid_mult, s);
+    if (threads == 512) return launch_coset_param_k<T, 512, 1>(a, p, recs, d_offs, l2_prefetch, grid_mult, s);
+    if constexpr (sizeof(T) == 4)
+        if (threads == 1024) return launch_coset_param_k<T, 1024, 1>(a, p, recs, d_offs, l2_prefetch, grid_mult, s);
     return launch_coset_param_k<T, kCosetThreads, PS_COSET_MINB>(a, p, recs, d_offs, l2_prefetch, grid_mult, s);
 }
 
@@ -1496,6 +1631,65 @@ cudaError_t launch_tile_t(T* a, int nl, const Pass& p, const DevSub* d_subs, con
     return cudaGetLastError();
 }
 
+template <typename T>
+cudaError_t launch_xtile_t(const XTileRank* ranks, int nranks, const Pass& p, const uint64_t* d_offs, int ell,
+                           uint64_t dtau, uint32_t epoch, cudaStream_t s, int grid_cap) {
+    if (nranks < 1 || nranks > kMaxXRanks) return cudaErrorInvalidValue;
+    const int threads = 1 << (p.kbits - kSubDim);
+    if (threads > kCosetThreads) return cudaErrorInvalidValue;
+    const size_t smem = coset_off_bytes(p.kbits - p.cbits) + ((size_t)(2 * sizeof(T)) << p.kbits);
+    static uint64_t attr_devices = 0;
+    const int dev = current_device();
+    if (!((attr_devices >> dev) & 1)) {
+        cudaFuncSetAttribute(k_xtile<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        attr_devices |= 1ull << dev;
+    }
+    int occ = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_xtile<T>, threads, smem);
+    if (occ < 1) return cudaErrorInvalidConfiguration;
+    // every CTA of the launch must be resident at once (CTAs wait on each other's flags)
+    const uint64_t ntiles = 1ull << __builtin_popcountll(p.free_mask);
+    uint64_t per = (uint64_t)num_sms() * (uint64_t)occ / (uint64_t)nranks;
+    if (grid_cap > 0 && (uint64_t)grid_cap < per) per = (uint64_t)grid_cap;
+    if (per > ntiles) per = ntiles;
+    if (per < 1) return cudaErrorInvalidConfiguration;
+    XTileParams P{};
+    for (int k = 0; k < nranks; ++k) P.r[k] = ranks[k];
+    P.runs = make_runs(p.free_mask);
+    P.offs = d_offs;
+    P.ntiles = ntiles;
+    P.free_mask = p.free_mask;
+    P.dtau = dtau;
+    P.nranks = nranks;
+    P.ctas_per_rank = (int)per;
+    P.kbits = p.kbits;
+    P.cbits = p.cbits;
+    P.nsub = p.sub_count;
+    P.ell = ell;
+    P.epoch = epoch;
+    void* args[] = {&P};
+    return cudaLaunchCooperativeKernel((const void*)k_xtile<T>, dim3((unsigned)(per * nranks)), dim3(threads), args,
+                                       smem, s);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) k_expect_cross(const T* __restrict__ a, const T* __restrict__ stage,
+                                                      uint64_t base, uint64_t count, uint64_t pbase, uint64_t xl,
+                                                      uint64_t zl, int y, int sgn, double* partial) {
+    double acc = 0.0;
+    for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < count; t += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t i = base + t, j = (i ^ xl) - pbase;
+        const double ar = (double)a[2 * i], ai = (double)a[2 * i + 1];
+        const double br = (double)stage[2 * j], bi = (double)stage[2 * j + 1];
+        // conj(b) a, then Re(i^y (.)) with the sign (-1)^popc(z & i)
+        const double re = __fma_rn(br, ar, __dmul_rn(bi, ai)), im = __fma_rn(br, ai, __dmul_rn(-bi, ar));
+        const double v = y == 0 ? re : y == 1 ? -im : y == 2 ? -re : im;
+        acc += (par64(zl & i) ^ sgn) ? -v : v;
+    }
+    const double s = block_sum(acc);
+    if (threadIdx.x == 0) partial[blockIdx.x] = s;
+}
+
 unsigned red_grid(uint64_t n) {
     const uint64_t want = (n + kRedThreads - 1) / kRedThreads;
     const uint64_t cap = (uint64_t)num_sms() * 4;
@@ -1522,7 +1716,8 @@ cudaError_t launch_stream(int dtype, void* a, int nl, const Pass& p, const DevRo
 
 cudaError_t launch_tile(int dtype, void* a, int nl, const Pass& p, const DevSub* d_subs, const DevTRot* d_trots,
                         const uint64_t* d_offs, int use_tma, int tune, cudaStream_t s, const DevSub* h_subs,
-                        const DevTRot* h_trots) {
+                        const DevTRot* h_trots, int grid_cap) {
+    t_grid_cap = grid_cap;
     // tune: bit 0 = L2 prefetch of the next tile (register-direct kernel); bits 4.. = grid multiplier
     // bit 0: TMA bulk L2 prefetch; bit 8: per-thread L2 prefetch; bit 9: L2::256B load hint
     // bit 11: LDGSTS prefetch of the next tile's first sub-group into shared memory
@@ -1672,6 +1867,45 @@ cudaError_t launch_scale(int dtype, void* a, uint64_t n, double f, cudaStream_t 
         k_scale<double><<<grid, kRedThreads, 0, s>>>((double*)a, n, f);
     else
         k_scale<float><<<grid, kRedThreads, 0, s>>>((float*)a, n, f);
+    return cudaGetLastError();
+}
+
+// tile-index offset dtau of the coset T xor 2^ell (0 when 2^ell lies in the tile space): the unit
+// vector reduced by the pass's gathered basis (RREF, pivot = highest bit) leaves free-mask bits only
+static uint64_t xtile_dtau(const Pass& p, const uint64_t* h_offs, int ell) {
+    if (ell < p.cbits) return 0;
+    uint64_t e = 1ull << ell;
+    for (int t = 0; t < p.hbits; ++t) {
+        const uint64_t v = h_offs[1u << t];
+        if (highest_bit(v) == ell) e ^= v;
+    }
+    e &= p.free_mask;
+    uint64_t out = 0;
+    int k = 0;
+    for (uint64_t m = p.free_mask; m; m &= m - 1, ++k)
+        if (e & m & (~m + 1)) out |= 1ull << k;
+    return out;
+}
+
+cudaError_t launch_xtile(int dtype, const XTileRank* ranks, int nranks, const Pass& p, const uint64_t* d_offs,
+                         const uint64_t* h_offs, int ell, uint32_t epoch, cudaStream_t s, int grid_cap) {
+    if (p.or_mask) return cudaErrorInvalidValue;
+    const uint64_t dtau = xtile_dtau(p, h_offs, ell);
+    if (dtype == PS_C128) return launch_xtile_t<double>(ranks, nranks, p, d_offs, ell, dtau, epoch, s, grid_cap);
+    return launch_xtile_t<float>(ranks, nranks, p, d_offs, ell, dtau, epoch, s, grid_cap);
+}
+
+cudaError_t launch_expect_cross(int dtype, const void* a, const void* stage, uint64_t base, uint64_t count,
+                                uint64_t pbase, uint64_t xl, uint64_t zl, int y, int sgn, double* d_partial,
+                                double* d_out_slot, cudaStream_t s) {
+    const unsigned grid = red_grid(count);
+    if (dtype == PS_C128)
+        k_expect_cross<double><<<grid, kRedThreads, 0, s>>>((const double*)a, (const double*)stage, base, count, pbase,
+                                                             xl, zl, y, sgn, d_partial);
+    else
+        k_expect_cross<float><<<grid, kRedThreads, 0, s>>>((const float*)a, (const float*)stage, base, count, pbase,
+                                                            xl, zl, y, sgn, d_partial);
+    k_final_sum<<<1, kRedThreads, 0, s>>>(d_partial, (int)grid, 1, 0, d_out_slot);
     return cudaGetLastError();
 }
 

@@ -152,6 +152,19 @@ struct Pass {
     double wr = 1.0, wi = 0.0;
 };
 
+// one rank of a fused exchange + tile pass (kernels.cu k_xtile): its slice, the partner's slice
+// (peer pointer), the per-tile handshake flags on both sides and its pass records (device)
+struct XTileRank {
+    void* a;                  // this rank's local slice (new layout after the pass)
+    const void* peer;         // the partner's local slice
+    uint32_t* flags;          // this rank's flags: the partner raises flag[tile] after reading it
+    uint32_t* peer_flags;     // the partner's flags: raised by this rank
+    const DevSub* subs;       // the pass's sub-groups (this rank's signs and factors)
+    const DevTRot* trots;     // the call's rotation records (sub-group rot_begin indexes them)
+    int rank;
+    int keep;                 // this rank keeps its slots with bit ell == keep
+};
+
 struct Plan {
     std::vector<Pass> passes;
     std::vector<DevRot> rots;

@@ -15,10 +15,11 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("PS_LIB_PATH") or os.path.join(_HERE, "libps.so")  # override for A/B builds
 
 C128, C64 = 0, 1
-K_STREAM, K_TILE, K_COSET, K_REDUCE, K_INIT, K_EXCHANGE, K_PERMUTE, K_MIRROR = range(8)
-KERNEL_NAMES = ["stream", "tile", "coset", "reduce", "init", "exchange", "permute", "mirror"]
-OP_MIRROR_BEGIN, OP_MIRROR_SWITCH, OP_MIRROR_END = 8, 9, 10
-OPT_PROFILE, OPT_FUSION, OPT_TILE_BITS, OPT_CHUNK_BYTES, OPT_MAX_PASS_ROTS, OPT_VEC256, OPT_TILE_TMA, OPT_CHUNK_BITS, OPT_TILE_TUNE, OPT_LAYOUT, OPT_TRANSPORT, OPT_OVERLAP, OPT_SPECIALIZE = range(13)
+K_STREAM, K_TILE, K_COSET, K_REDUCE, K_INIT, K_EXCHANGE, K_PERMUTE, K_MIRROR, K_XTILE = range(9)
+KERNEL_NAMES = ["stream", "tile", "coset", "reduce", "init", "exchange", "permute", "mirror", "xtile"]
+NK = len(KERNEL_NAMES)
+OP_MIRROR_BEGIN, OP_MIRROR_SWITCH, OP_MIRROR_END = 16, 17, 18
+OPT_PROFILE, OPT_FUSION, OPT_TILE_BITS, OPT_CHUNK_BYTES, OPT_MAX_PASS_ROTS, OPT_VEC256, OPT_TILE_TMA, OPT_CHUNK_BITS, OPT_TILE_TUNE, OPT_LAYOUT, OPT_TRANSPORT, OPT_OVERLAP, OPT_SPECIALIZE, OPT_GRID_CAP, OPT_FUSED_EXCHANGE = range(15)
 
 
 class PsError(RuntimeError):
@@ -32,11 +33,12 @@ class Stats(ctypes.Structure):
         ("rotations", ctypes.c_uint64),
         ("passes", ctypes.c_uint64),
         ("exchanges", ctypes.c_uint64),
-        ("launches", ctypes.c_uint64 * 8),
-        ("rotations_by", ctypes.c_uint64 * 8),
-        ("algo_bytes", ctypes.c_double * 8),
+        ("launches", ctypes.c_uint64 * NK),
+        ("rotations_by", ctypes.c_uint64 * NK),
+        ("algo_bytes", ctypes.c_double * NK),
         ("nvlink_bytes", ctypes.c_double),
-        ("kernel_ms", ctypes.c_double * 8),
+        ("kernel_ms", ctypes.c_double * NK),
+        ("nvlink_fused_bytes", ctypes.c_double),
     ]
 
     def as_dict(self):
@@ -49,6 +51,7 @@ class Stats(ctypes.Structure):
             "algo_bytes": {k: float(self.algo_bytes[i]) for i, k in enumerate(KERNEL_NAMES)},
             "nvlink_bytes": float(self.nvlink_bytes),
             "kernel_ms": {k: float(self.kernel_ms[i]) for i, k in enumerate(KERNEL_NAMES)},
+            "nvlink_fused_bytes": float(self.nvlink_fused_bytes),
         }
 
 
@@ -64,7 +67,7 @@ class PlanRot(ctypes.Structure):
 
 
 EXPORTS = [
-    "ps_create", "ps_create_ex", "ps_create_dist", "ps_get_unique_id", "ps_destroy", "ps_info", "ps_set_option",
+    "ps_create", "ps_create_ex", "ps_create_dist", "ps_create_emulated", "ps_get_unique_id", "ps_destroy", "ps_info", "ps_set_option",
     "ps_init_basis", "ps_init_random", "ps_normalize", "ps_set_state", "ps_get_amplitudes", "ps_apply_rotations",
     "ps_norm", "ps_expectation", "ps_inner", "ps_synchronize", "ps_get_stats", "ps_reset_stats",
     "ps_status_string", "ps_last_error", "ps_pauli_encode", "ps_pauli_encode_codes", "ps_gate_to_rotations",
@@ -88,6 +91,7 @@ def lib():
         "ps_create": [i32, i32, ctypes.POINTER(H)],
         "ps_create_ex": [i32, i32, vp, sz, vp, i32, i32, vp, ctypes.POINTER(H)],
         "ps_create_dist": [i32, i32, i32, i32, vp, ctypes.POINTER(H)],
+        "ps_create_emulated": [i32, i32, i32, vp, sz, vp, ctypes.POINTER(H)],
         "ps_get_unique_id": [vp],
         "ps_destroy": [H],
         "ps_info": [H, vp, vp, vp, vp, vp, vp],
@@ -227,7 +231,7 @@ class State:
     """
 
     def __init__(self, n: int, dtype: str = "c128", world: int = 1, rank: int = 0, torch_memory: bool = False,
-                 group=None):
+                 group=None, emulate: int = 0):
         self.n = int(n)
         self.dtype = C128 if dtype in ("c128", "complex128", C128) else C64
         self.world, self.rank = int(world), int(rank)
@@ -236,6 +240,25 @@ class State:
         self.torch_stream = None
         L = lib()
         nid = None
+        if emulate:
+            # G virtual ranks on this device (ps_create_emulated): one handle, global indices
+            self.world, self.rank, self.emulated = int(emulate), 0, True
+            dev_ptr, nbytes, stream = None, 0, None
+            if torch_memory:
+                import torch
+                tdt = torch.float64 if self.dtype == C128 else torch.float32
+                self._tensor = torch.empty(2 << self.n, dtype=tdt, device="cuda")
+                dev_ptr, nbytes = self._tensor.data_ptr(), self._tensor.numel() * self._tensor.element_size()
+                cur = torch.cuda.current_stream()
+                self.torch_stream = cur if cur.cuda_stream != 0 else torch.cuda.Stream()
+                stream = self.torch_stream.cuda_stream
+            _check("ps_create_emulated", L.ps_create_emulated(self.n, self.dtype, self.world, dev_ptr, nbytes, stream,
+                                                              ctypes.byref(self._h)))
+            nq, nl = ctypes.c_int(), ctypes.c_int()
+            L.ps_info(self._h, ctypes.byref(nq), ctypes.byref(nl), None, None, None, None)
+            self.n_local = nl.value
+            return
+        self.emulated = False
         if self.world > 1:
             nid = ctypes.create_string_buffer(bootstrap_nccl_id(self.rank, group), 128)
         dev_ptr, nbytes, stream = None, 0, None

@@ -23,10 +23,12 @@ from .ps import State
 
 
 def signal(n: int, HD, HR, delta: float, m: int, r: int, seed: int, init="random", init_seed: int = 250417881,
-           dtype: str = "c128", world: int = 1, rank: int = 0, offset: float = 0.0) -> complex:
-    """Z_m for one sampled circuit (the paper averages repeats for the randomized part)."""
+           dtype: str = "c128", world: int = 1, rank: int = 0, offset: float = 0.0, emulate: int = 0) -> complex:
+    """Z_m for one sampled circuit (the paper averages repeats for the randomized part).  emulate = G
+    runs both states as G virtual ranks on this device (ps_create_emulated)."""
     x, z, a = formulas.evolution_stream(HD, HR, delta, 2 ** m, r, seed)
-    with State(n, dtype, world=world, rank=rank) as psi0, State(n, dtype, world=world, rank=rank) as psi:
+    kw = dict(emulate=emulate) if emulate else dict(world=world, rank=rank)
+    with State(n, dtype, **kw) as psi0, State(n, dtype, **kw) as psi:
         for st in (psi0, psi):
             if init == "random":
                 st.init_random(init_seed)
