@@ -45,7 +45,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--qubits", dest="n", type=int, default=30)
     ap.add_argument("--layer", type=int, default=1000)
-    ap.add_argument("--kind", default="R10", help="R10 R4 D S8 LOW (random layers), JW (Trotter step), QAOA, GATES")
+    ap.add_argument("--kind", default="R10", help="R10 R4 D S8 LOW (random layers), JW (Trotter step), QAOA, GATES, UCC, HEA (VQE)")
     ap.add_argument("--terms", type=int, default=92968, help="JW: Hamiltonian terms (Table 3: 92,968 at 32q)")
     ap.add_argument("--lam", type=float, default=27.0, help="JW: lambda = sum |h| (Table 3)")
     ap.add_argument("--delta", type=float, default=0.5, help="JW: Trotter step size")
@@ -82,6 +82,11 @@ def workload_name(args):
         return f"{args.n}q {prec} QAOA MaxCut, random 3-regular graph, p = {args.layer} layers"
     if args.kind == "GATES":
         return f"{args.n}q {prec} random gate brickwork of depth {args.layer}, converted to rotations"
+    if args.kind == "UCC":
+        return (f"{args.n}q {prec} UCCSD-shaped VQE layer (JW; {args.n // 3} occupied spin orbitals, "
+                f"singles + {args.layer} sampled doubles x 8 strings)")
+    if args.kind == "HEA":
+        return f"{args.n}q {prec} hardware-efficient VQE ansatz, {args.layer} RY/RZ + CNOT-ladder layers"
     return (f"{args.n}q {prec} random Pauli-rotation layer "
             f"({args.kind}: weight 1-10, phi~U[-pi,pi)), {args.layer} rotations/step")
 
@@ -102,6 +107,13 @@ def layers(args, count, world=1):
         return [(x, z, ang)] * count
     if args.kind == "GATES":
         x, z, ang = P.circuit_to_rotations(workloads.gate_circuit(args.n, args.layer, seed=0))
+        return [(x, z, ang)] * count
+    if args.kind == "UCC":
+        codes, ang = workloads.ucc_layers(args.n, args.n // 3, seed=0, max_doubles=args.layer)
+        x, z = P.pauli_encode_codes(codes)
+        return [(x, z, ang)] * count
+    if args.kind == "HEA":
+        x, z, ang = P.circuit_to_rotations(workloads.hardware_efficient_vqe(args.n, args.layer, seed=0))
         return [(x, z, ang)] * count
     for s in range(count):
         codes, ang = workloads.random_layer(args.n, args.layer, seed=1000 + s, kind=args.kind)

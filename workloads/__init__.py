@@ -245,3 +245,62 @@ def gate_circuit(n: int, depth: int, seed: int = 0):
             params = (float(rng.uniform(-np.pi, np.pi)),) if g in ("CPHASE", "RZZ") else ()
             gates.append((g, (a, b), params))
     return gates
+
+
+def ucc_layers(n: int, n_occ: int | None = None, seed: int = 0, max_doubles: int | None = None):
+    """A unitary-coupled-cluster (UCCSD-shaped) VQE ansatz layer under Jordan-Wigner (BASELINE.json
+    config 4, "VQE-style layers").  Spin orbitals interleaved (qubit p: spin p % 2); the n_occ lowest
+    orbitals occupied.  Singles p -> a (occupied p, virtual a, same spin): exp(theta (a_a^dag a_p -
+    h.c.)) = exp(i theta/2 (X_p Z..Z Y_a - Y_p Z..Z X_a)) as two rotations; doubles (p<q) -> (a<b),
+    spin conserving: the 8 Pauli strings with an odd number of Y on {p, q, a, b} and Z strings on
+    (p, q) and (a, b), angles +-theta/8 (sign + for three X and one Y, - for one X and three Y).
+    Amplitudes theta ~ U[-0.1, 0.1] (seeded).  Returns (codes[L, n], angles[L]) in ansatz order."""
+    rng = _rng(4_000_000 + n * 10 + seed)
+    n_occ = n // 2 if n_occ is None else n_occ
+    occ = list(range(n_occ))
+    vir = list(range(n_occ, n))
+    rows, angles = [], []
+    for p in occ:
+        for a in vir:
+            if (a - p) % 2:
+                continue
+            th = float(rng.uniform(-0.1, 0.1))
+            for lp, la, sg in ((X, Y, 1.0), (Y, X, -1.0)):
+                rows.append(_jw_string(n, p, a, lp, la))
+                angles.append(sg * th / 2)
+    doubles = []
+    for i, p in enumerate(occ):
+        for q in occ[i + 1:]:
+            for j, a in enumerate(vir):
+                for b in vir[j + 1:]:
+                    if (p % 2) + (q % 2) == (a % 2) + (b % 2):
+                        doubles.append((p, q, a, b))
+    if max_doubles is not None and len(doubles) > max_doubles:
+        pick = np.sort(rng.choice(len(doubles), max_doubles, replace=False))
+        doubles = [doubles[k] for k in pick]
+    odd_y = [(X, X, X, Y), (X, X, Y, X), (X, Y, X, X), (Y, X, X, X),
+             (X, Y, Y, Y), (Y, X, Y, Y), (Y, Y, X, Y), (Y, Y, Y, X)]
+    for p, q, a, b in doubles:
+        th = float(rng.uniform(-0.1, 0.1))
+        for k, (l0, l1, l2, l3) in enumerate(odd_y):
+            w = np.zeros(n, np.uint8)
+            w[p + 1:q] = Z
+            w[a + 1:b] = Z
+            w[p], w[q], w[a], w[b] = l0, l1, l2, l3
+            rows.append(w)
+            angles.append((1.0 if k < 4 else -1.0) * th / 8)
+    return np.stack(rows).astype(np.uint8), np.array(angles)
+
+
+def hardware_efficient_vqe(n: int, depth: int, seed: int = 0):
+    """Hardware-efficient VQE ansatz as a gate list: per layer RY and RZ on every qubit, then a CNOT
+    ladder (q, q+1) -- converted to rotations by ps_gate_to_rotations."""
+    rng = _rng(3_000_000 + n * 10 + seed)
+    gates = []
+    for _ in range(depth):
+        for q in range(n):
+            gates.append(("RY", (q,), (float(rng.uniform(-np.pi, np.pi)),)))
+            gates.append(("RZ", (q,), (float(rng.uniform(-np.pi, np.pi)),)))
+        for q in range(n - 1):
+            gates.append(("CNOT", (q, q + 1), ()))
+    return gates
