@@ -422,33 +422,22 @@ __device__ __forceinline__ void cform_sub(T (&vr)[kSubAmps], T (&vi)[kSubAmps], 
     }
 }
 
-// case lists: Dz values whose bit highest(dx) is clear (the planner clears it)
-#define PS_LC(R, X, Z) \
-    case tr_case(R, X, Z): cform_sub<R, X, Z, T>(vr, vi, t); break;
-#define PS_LZ_P0(R, X) PS_LC(R, X, 0) PS_LC(R, X, 2) PS_LC(R, X, 4) PS_LC(R, X, 6) \
-    PS_LC(R, X, 8) PS_LC(R, X, 10) PS_LC(R, X, 12) PS_LC(R, X, 14)
-#define PS_LZ_P1(R, X) PS_LC(R, X, 0) PS_LC(R, X, 1) PS_LC(R, X, 4) PS_LC(R, X, 5) \
-    PS_LC(R, X, 8) PS_LC(R, X, 9) PS_LC(R, X, 12) PS_LC(R, X, 13)
-#define PS_LZ_P2(R, X) PS_LC(R, X, 0) PS_LC(R, X, 1) PS_LC(R, X, 2) PS_LC(R, X, 3) \
-    PS_LC(R, X, 8) PS_LC(R, X, 9) PS_LC(R, X, 10) PS_LC(R, X, 11)
-#define PS_LZ_P3(R, X) PS_LC(R, X, 0) PS_LC(R, X, 1) PS_LC(R, X, 2) PS_LC(R, X, 3) \
-    PS_LC(R, X, 4) PS_LC(R, X, 5) PS_LC(R, X, 6) PS_LC(R, X, 7)
-#define PS_LZ_ALL(R, X) PS_LZ_P3(R, X) PS_LC(R, X, 8) PS_LC(R, X, 9) PS_LC(R, X, 10) PS_LC(R, X, 11) \
-    PS_LC(R, X, 12) PS_LC(R, X, 13) PS_LC(R, X, 14) PS_LC(R, X, 15)
-#define PS_LX_LOW(R) PS_LZ_P0(R, 1) PS_LZ_P1(R, 2) PS_LZ_P1(R, 3) PS_LZ_P2(R, 4) PS_LZ_P2(R, 5) \
-    PS_LZ_P2(R, 6) PS_LZ_P2(R, 7)
-#define PS_LX_HIGH(R) PS_LZ_P3(R, 8) PS_LZ_P3(R, 9) PS_LZ_P3(R, 10) PS_LZ_P3(R, 11) PS_LZ_P3(R, 12) \
-    PS_LZ_P3(R, 13) PS_LZ_P3(R, 14) PS_LZ_P3(R, 15)
+// unit cases (ps_internal.h tu_case): diagonal by its 4-bit Dz, unit dx by (real, log2 dx, the three
+// Dz bits other than the pivot's); signs and the pair pattern are compile-time
+#define PS_UD(Z) case Z: cform_sub<0, 0, Z, T>(vr, vi, t); break;
+#define PS_UC(R, XI, Z3) case tu_case(R, XI, tu_dz(XI, Z3)): cform_sub<R, (1 << XI), tu_dz(XI, Z3), T>(vr, vi, t); break;
+#define PS_UC8(R, XI) PS_UC(R, XI, 0) PS_UC(R, XI, 1) PS_UC(R, XI, 2) PS_UC(R, XI, 3) PS_UC(R, XI, 4) \
+    PS_UC(R, XI, 5) PS_UC(R, XI, 6) PS_UC(R, XI, 7)
 
 template <typename T>
-__device__ __forceinline__ void cform_dispatch(T (&vr)[kSubAmps], T (&vi)[kSubAmps], uint32_t code, T t) {
-    switch (code & 0xffu) {
-        PS_LZ_ALL(0, 0)
-        PS_LX_LOW(0)
-        PS_LX_LOW(1)
+__device__ __forceinline__ void unit_dispatch(T (&vr)[kSubAmps], T (&vi)[kSubAmps], uint32_t ucase, T t) {
+    switch (ucase) {
+        PS_UD(0) PS_UD(1) PS_UD(2) PS_UD(3) PS_UD(4) PS_UD(5) PS_UD(6) PS_UD(7)
+        PS_UD(8) PS_UD(9) PS_UD(10) PS_UD(11) PS_UD(12) PS_UD(13) PS_UD(14) PS_UD(15)
+        PS_UC8(0, 0) PS_UC8(0, 1) PS_UC8(0, 2)
+        PS_UC8(1, 0) PS_UC8(1, 1) PS_UC8(1, 2)
 #if PS_SUBDIM >= 4
-        PS_LX_HIGH(0)
-        PS_LX_HIGH(1)
+        PS_UC8(0, 3) PS_UC8(1, 3)
 #endif
     default: break;
     }
@@ -474,9 +463,9 @@ __device__ __forceinline__ void sub_apply(T (&vr)[kSubAmps], T (&vi)[kSubAmps], 
             pn = ldr<PARAM>(&tn->p);
         }
         const int s0 = par32(zr & r) ^ par64(zt_c & i0);
-        if (SPEC && !(code & kTrSform)) {
+        if (SPEC && (code & kTrUnit)) {
             // the thread-wide sign flips t once; the per-pair signs are static
-            cform_dispatch<T>(vr, vi, code, flip((T)pc, s0));
+            unit_dispatch<T>(vr, vi, code & 0x7fu, flip((T)pc, s0));
         } else {
             uint32_t Ms = (code >> 16) ^ (s0 ? 0xffffu : 0u);
             if (code & kTrNeg) Ms ^= 0xffffu;
@@ -654,14 +643,27 @@ __host__ __device__ inline size_t coset_off_bytes(int hbits) {
     return ((sizeof(uint64_t) << hbits) + 127) & ~(size_t)127;
 }
 
-// per-thread coset representatives of the first rep_tab sub-groups, computed once per CTA (fp64
-// only: at 8 CTAs per SM the fp32 kernel loses more to the extra shared memory than it saves)
-__host__ __device__ constexpr int rep_tab(size_t amp_bytes) { return amp_bytes == 16 ? 16 : 0; }
+// per-thread coset representatives (tile-local, 16 bits) of the first rep_tab sub-groups, computed
+// once per CTA (fp64 only: at 8 CTAs per SM the fp32 kernel loses more to the extra shared memory
+// than it saves)
+__host__ __device__ constexpr int rep_tab(size_t amp_bytes) { return amp_bytes == 16 ? 32 : 0; }
 
-// dynamic shared memory of the register-direct tile kernels: offsets | tile | representatives
+// dynamic shared memory of the register-direct tile kernels: tile (at offset 0, so element
+// addresses are plain byte offsets) | representatives | chunk offsets
+__host__ __device__ inline size_t coset_rep_bytes(int kbits, size_t amp_bytes) {
+    return (((size_t)rep_tab(amp_bytes) << (kbits - kSubDim)) * sizeof(uint16_t) + 127) & ~(size_t)127;
+}
 __host__ __device__ inline size_t coset_smem_bytes(int kbits, int cbits, size_t amp_bytes) {
-    const size_t threads = (size_t)1 << (kbits - kSubDim);
-    return coset_off_bytes(kbits - cbits) + (amp_bytes << kbits) + rep_tab(amp_bytes) * threads * sizeof(uint32_t);
+    return (amp_bytes << kbits) + coset_rep_bytes(kbits, amp_bytes) + coset_off_bytes(kbits - cbits);
+}
+
+// shared-memory byte offsets of the thread's 16 elements l_d = r xor U(d): o_d = o_(d without its
+// lowest bit) xor (u_lowest << log2 amp bytes) -- one xor each (the tile sits at offset 0)
+template <int LB>
+__device__ __forceinline__ void smem_offsets(uint32_t (&o)[kSubAmps], const SubHdr& h) {
+    o[0] = h.r << LB;
+#pragma unroll
+    for (int d = 1; d < kSubAmps; ++d) o[d] = o[d & (d - 1)] ^ (h.u[lowbit_index(d)] << LB);
 }
 
 template <typename T, int SPEC, int PARAM>
@@ -670,21 +672,26 @@ __device__ __forceinline__ void coset_body(T* __restrict__ a, int kbits, int cbi
                                            const DevSub* __restrict__ subs, int nsub, const DevTRot* __restrict__ trots,
                                            int l2_prefetch, uint64_t or_mask, uint64_t free_mask) {
     using V2 = typename SmemAmp<T>::V;
+    constexpr int LB = sizeof(V2) == 16 ? 4 : 3;  // log2 bytes per amplitude
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int hbits = kbits - cbits;
-    uint64_t* soff = reinterpret_cast<uint64_t*>(smem_raw);
-    V2* tile = reinterpret_cast<V2*>(smem_raw + coset_off_bytes(hbits));
-    uint32_t* rtab = reinterpret_cast<uint32_t*>(smem_raw + coset_off_bytes(hbits) + (sizeof(V2) << kbits));
+    V2* tile = reinterpret_cast<V2*>(smem_raw);
+    uint16_t* rtab = reinterpret_cast<uint16_t*>(smem_raw + (sizeof(V2) << kbits));
+    uint64_t* soff = reinterpret_cast<uint64_t*>(smem_raw + (sizeof(V2) << kbits) + coset_rep_bytes(kbits, sizeof(V2)));
     const uint32_t tid = threadIdx.x;
+    const uint32_t nthr = blockDim.x;
     const uint32_t cmask = (1u << cbits) - 1u;
     const int ncols = kbits - kSubDim;
-    for (uint32_t u = tid; u < (1u << hbits); u += blockDim.x) soff[u] = __ldg(&offs[u]);
+    for (uint32_t u = tid; u < (1u << hbits); u += nthr) soff[u] = __ldg(&offs[u]);
     // representatives depend on (sub-group, thread) only: once per CTA (each thread reads its own)
     constexpr int kRepTab = rep_tab(sizeof(V2));
-    for (int s = 0; s < nsub && s < kRepTab; ++s) rtab[s * blockDim.x + tid] = sub_rep<PARAM>(subs + s, tid, ncols);
+    for (int s = 0; s < nsub && s < kRepTab; ++s) rtab[s * nthr + tid] = (uint16_t)sub_rep<PARAM>(subs + s, tid, ncols);
     __syncthreads();
+    auto rep = [&](int s) -> uint32_t {
+        if (kRepTab > 0 && s < kRepTab) return rtab[s * nthr + tid];
+        return sub_rep<PARAM>(subs + s, tid, ncols);
+    };
     V2* g = reinterpret_cast<V2*>(a);
-    const uint32_t chunk_bytes = (uint32_t)(2 * sizeof(T)) << cbits;
     // tile bases advance in the deposited domain: pdep(tau + G) = ((pdep(tau) | ~M) + pdep(G)) & M
     const uint64_t dstep = deposit((uint64_t)gridDim.x, runs);
     uint64_t dtau = deposit((uint64_t)blockIdx.x, runs);
@@ -693,10 +700,9 @@ __device__ __forceinline__ void coset_body(T* __restrict__ a, int kbits, int cbi
     // its inputs in registers, so the next tile's reads are in flight while this one is computed
     // and stored; sub-group 0 then reads its own slots instead of HBM
     const bool pf = (l2_prefetch & 8) != 0;
-    const uint32_t nthr = blockDim.x;
     auto prefetch_tile = [&](uint64_t i1) {
         SubHdr h0 = load_sub_hdr<PARAM>(subs);
-        h0.r = kRepTab > 0 ? rtab[tid] : sub_rep<PARAM>(subs, tid, ncols);
+        h0.r = rep(0);
         uint64_t gi[kSubAmps];
         elem_index(gi, h0, i1, soff, cbits, cmask);
 #pragma unroll
@@ -710,7 +716,7 @@ __device__ __forceinline__ void coset_body(T* __restrict__ a, int kbits, int cbi
         T vr[kSubAmps], vi[kSubAmps];
         for (int s = 0; s < nsub; ++s) {
             SubHdr h = load_sub_hdr<PARAM>(subs + s);
-            h.r = s < kRepTab ? rtab[s * blockDim.x + tid] : sub_rep<PARAM>(subs + s, tid, ncols);
+            h.r = rep(s);
             if (s == 0 && pf) {
                 asm volatile("cp.async.wait_group 0;" ::: "memory");
 #pragma unroll
@@ -736,31 +742,14 @@ __device__ __forceinline__ void coset_body(T* __restrict__ a, int kbits, int cbi
                     vi[d] = v[d].y;
                 }
             } else {
+                uint32_t o[kSubAmps];
+                smem_offsets<LB>(o, h);
 #pragma unroll
                 for (int d = 0; d < kSubAmps; ++d) {
-                    const V2 v = tile[sub_local(h, d)];
+                    const V2 v = *reinterpret_cast<const V2*>(smem_raw + o[d]);
                     vr[d] = v.x;
                     vi[d] = v.y;
                 }
-            }
-            if (s == 0 && (l2_prefetch & 2) && tau + gridDim.x < ntiles && (tid & 7) == 0) {
-                // per-thread L2 prefetch of the lines of this thread's next-tile coset (one lane of
-                // 8 covers a 128-B line of 16-B amplitudes)
-                const uint64_t i1 = deposit(tau + gridDim.x, runs) | or_mask;
-#pragma unroll
-                for (int d = 0; d < kSubAmps; ++d) {
-                    const uint32_t l = sub_local(h, d);
-                    asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(&g[(i1 ^ soff[l >> cbits]) | (l & cmask)]));
-                }
-            }
-            if (s == 0 && (l2_prefetch & 1) && tau + gridDim.x < ntiles) {
-                // this tile's loads have landed (sub_apply consumes them): warm L2 with the CTA's next
-                // tile while the rest of this one is computed and stored
-                const uint64_t i1 = deposit(tau + gridDim.x, runs) | or_mask;
-                for (uint32_t u = tid; u < (1u << hbits); u += blockDim.x)
-                    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a + 2 * (i1 ^ soff[u])),
-                                 "r"(chunk_bytes)
-                                 : "memory");
             }
             if (pf && (s == 0 || s == nsub - 1)) {
                 // every thread's shared-memory reads of this sub-group are done before the slots
@@ -782,12 +771,14 @@ __device__ __forceinline__ void coset_body(T* __restrict__ a, int kbits, int cbi
                     __stcs(&g[gi[d]], v);
                 }
             } else {
+                uint32_t o[kSubAmps];
+                smem_offsets<LB>(o, h);
 #pragma unroll
                 for (int d = 0; d < kSubAmps; ++d) {
                     V2 v;
                     v.x = vr[d];
                     v.y = vi[d];
-                    tile[sub_local(h, d)] = v;
+                    *reinterpret_cast<V2*>(smem_raw + o[d]) = v;
                 }
                 __syncthreads();
             }
@@ -813,13 +804,13 @@ struct PassRecs {
     DevTRot trots[kParamRots];
 };
 
-template <typename T, int MAXT, int MINB>
+template <typename T, int MAXT, int MINB, int SPEC = 0>
 __global__ void __launch_bounds__(MAXT, MINB)
     k_coset_p(T* __restrict__ a, int kbits, int cbits, const __grid_constant__ BitRuns runs,
               const uint64_t* __restrict__ offs, uint64_t ntiles, int nsub, int l2_prefetch, uint64_t or_mask,
               uint64_t free_mask, const __grid_constant__ PassRecs recs) {
-    coset_body<T, 0, 1>(a, kbits, cbits, runs, offs, ntiles, recs.subs, nsub, recs.trots, l2_prefetch, or_mask,
-                        free_mask);
+    coset_body<T, SPEC, 1>(a, kbits, cbits, runs, offs, ntiles, recs.subs, nsub, recs.trots, l2_prefetch, or_mask,
+                           free_mask);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -1240,26 +1231,42 @@ __device__ __forceinline__ double block_sum(double v) {
     return s;
 }
 
-template <typename T>
+// The reductions read the state once with 256-bit vector loads (V amplitudes per load: 2 fp64,
+// 4 fp32; V = 1 below V amplitudes), accumulate in fp64 per thread in a fixed order and sum per
+// block (deterministic two-stage sums).  HBM-bound: algorithmic bytes = the bytes read.
+template <typename T, int V>
 __global__ void __launch_bounds__(kRedThreads) k_norm(const T* __restrict__ a, uint64_t n, double* partial) {
     double acc = 0.0;
-    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
-        const double r = (double)a[2 * i], m = (double)a[2 * i + 1];
-        acc = __fma_rn(r, r, __fma_rn(m, m, acc));
+    const uint64_t units = n / V;
+    for (uint64_t u = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; u < units; u += (uint64_t)gridDim.x * blockDim.x) {
+        Vec<T, V> v;
+        ld_vec<T, V>(a + 2 * u * V, v);
+#pragma unroll
+        for (int e = 0; e < V; ++e) {
+            const double r = (double)v.r[e], m = (double)v.i[e];
+            acc = __fma_rn(r, r, __fma_rn(m, m, acc));
+        }
     }
     const double s = block_sum(acc);
     if (threadIdx.x == 0) partial[blockIdx.x] = s;
 }
 
-template <typename T>
+template <typename T, int V>
 __global__ void __launch_bounds__(kRedThreads) k_inner(const T* __restrict__ a, const T* __restrict__ b, uint64_t n,
                                                        double* partial) {
     double re = 0.0, im = 0.0;
-    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
-        const double ar = (double)a[2 * i], ai = (double)a[2 * i + 1];
-        const double br = (double)b[2 * i], bi = (double)b[2 * i + 1];
-        re = __fma_rn(ar, br, __fma_rn(ai, bi, re));
-        im = __fma_rn(ar, bi, __fma_rn(-ai, br, im));
+    const uint64_t units = n / V;
+    for (uint64_t u = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; u < units; u += (uint64_t)gridDim.x * blockDim.x) {
+        Vec<T, V> va, vb;
+        ld_vec<T, V>(a + 2 * u * V, va);
+        ld_vec<T, V>(b + 2 * u * V, vb);
+#pragma unroll
+        for (int e = 0; e < V; ++e) {
+            const double ar = (double)va.r[e], ai = (double)va.i[e];
+            const double br = (double)vb.r[e], bi = (double)vb.i[e];
+            re = __fma_rn(ar, br, __fma_rn(ai, bi, re));
+            im = __fma_rn(ar, bi, __fma_rn(-ai, br, im));
+        }
     }
     const double s0 = block_sum(re);
     const double s1 = block_sum(im);
@@ -1269,36 +1276,71 @@ __global__ void __launch_bounds__(kRedThreads) k_inner(const T* __restrict__ a, 
     }
 }
 
+// the terms of one x-group at pair (i, j = i ^ x0): sum_l sigma_l(i) (kr_l tr + ki_l ti), t = conj(a_j) a_i
+__device__ __forceinline__ double expect_pair(double ir, double ii, double jr, double ji, uint64_t i,
+                                              const DevTerm* __restrict__ terms, int nt) {
+    const double tr = __fma_rn(jr, ir, __dmul_rn(ji, ii));
+    const double ti = __fma_rn(jr, ii, __dmul_rn(-ji, ir));
+    double acc = 0.0;
+    for (int l = 0; l < nt; ++l) {
+        const double v = __fma_rn(__ldg(&terms[l].kr), tr, __dmul_rn(__ldg(&terms[l].ki), ti));
+        acc += par64(__ldg(&terms[l].z) & i) ? -v : v;
+    }
+    return acc;
+}
+
 // expectation over one x-group: terms[0..nt) share xor mask x0
-template <typename T>
+template <typename T, int V>
 __global__ void __launch_bounds__(kRedThreads) k_expect(const T* __restrict__ a, uint64_t nl_amps, uint64_t x0,
                                                         const DevTerm* __restrict__ terms, int nt,
                                                         double* partial) {
     double acc = 0.0;
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    const uint64_t t0 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (x0 == 0) {
-        for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nl_amps; i += stride) {
-            const double r = (double)a[2 * i], m = (double)a[2 * i + 1];
-            const double p = __fma_rn(r, r, __dmul_rn(m, m));
-            double w = 0.0;
-            for (int l = 0; l < nt; ++l) {
-                const double kr = __ldg(&terms[l].kr);
-                w += par64(__ldg(&terms[l].z) & i) ? -kr : kr;
+        for (uint64_t u = t0; u < nl_amps / V; u += stride) {
+            Vec<T, V> v;
+            ld_vec<T, V>(a + 2 * u * V, v);
+#pragma unroll
+            for (int e = 0; e < V; ++e) {
+                const uint64_t i = u * V + e;
+                const double r = (double)v.r[e], m = (double)v.i[e];
+                const double p = __fma_rn(r, r, __dmul_rn(m, m));
+                double w = 0.0;
+                for (int l = 0; l < nt; ++l) {
+                    const double kr = __ldg(&terms[l].kr);
+                    w += par64(__ldg(&terms[l].z) & i) ? -kr : kr;
+                }
+                acc = __fma_rn(w, p, acc);
             }
-            acc = __fma_rn(w, p, acc);
+        }
+    } else if ((1ull << (63 - __clzll(x0))) >= (uint64_t)V) {
+        // pairs across vectors: the i-vector has bit piv clear, its partners are the vector at
+        // ib ^ (x0 without its in-vector bits), permuted by xin
+        const int piv = 63 - __clzll(x0);
+        const uint64_t xv = x0 & ~(uint64_t)(V - 1);
+        const int xin = (int)(x0 & (V - 1));
+        for (uint64_t u = t0; u < (nl_amps >> 1) / V; u += stride) {
+            const uint64_t ib = insert0(u * V, piv);
+            Vec<T, V> vi, vj;
+            ld_vec<T, V>(a + 2 * ib, vi);
+            ld_vec<T, V>(a + 2 * (ib ^ xv), vj);
+#pragma unroll
+            for (int e = 0; e < V; ++e)
+                acc += expect_pair((double)vi.r[e], (double)vi.i[e], (double)vj.r[e ^ xin], (double)vj.i[e ^ xin], ib + e,
+                                   terms, nt);
         }
     } else {
+        // pairs inside one vector (x0 < V)
         const int piv = 63 - __clzll(x0);
-        for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < (nl_amps >> 1); t += stride) {
-            const uint64_t i = insert0(t, piv), j = i ^ x0;
-            const double ir = (double)a[2 * i], ii = (double)a[2 * i + 1];
-            const double jr = (double)a[2 * j], ji = (double)a[2 * j + 1];
-            // t = conj(a_j) a_i
-            const double tr = __fma_rn(jr, ir, __dmul_rn(ji, ii));
-            const double ti = __fma_rn(jr, ii, __dmul_rn(-ji, ir));
-            for (int l = 0; l < nt; ++l) {
-                const double v = __fma_rn(__ldg(&terms[l].kr), tr, __dmul_rn(__ldg(&terms[l].ki), ti));
-                acc += par64(__ldg(&terms[l].z) & i) ? -v : v;
+        for (uint64_t u = t0; u < nl_amps / V; u += stride) {
+            Vec<T, V> v;
+            ld_vec<T, V>(a + 2 * u * V, v);
+#pragma unroll
+            for (int e = 0; e < V; ++e) {
+                if ((e >> piv) & 1) continue;
+                const int f = e ^ (int)x0;
+                acc += expect_pair((double)v.r[e], (double)v.i[e], (double)v.r[f], (double)v.i[f], u * V + e, terms, nt);
             }
         }
     }
@@ -1539,25 +1581,25 @@ cudaError_t launch_coset_t(T* a, int nl, const Pass& p, const DevSub* d_subs, co
 
 // the pass's records in the launch's parameter block (tune bit 10; passes of <= kParamRots
 // rotations); cudaErrorNotSupported when the pass does not fit
-template <typename T, int MAXT, int MINB>
+template <typename T, int MAXT, int MINB, int SPEC = 0>
 cudaError_t launch_coset_param_k(T* a, const Pass& p, const PassRecs& recs, const uint64_t* d_offs, int l2_prefetch,
                                  int grid_mult, cudaStream_t s) {
     const size_t smem = coset_smem_bytes(p.kbits, p.cbits, 2 * sizeof(T));
     static uint64_t attr_devices = 0;
     const int dev = current_device();
     if (!((attr_devices >> dev) & 1)) {
-        cudaFuncSetAttribute(k_coset_p<T, MAXT, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        cudaFuncSetAttribute(k_coset_p<T, MAXT, MINB, SPEC>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         attr_devices |= 1ull << dev;
     }
     const int threads = 1 << (p.kbits - kSubDim);
     if (threads > MAXT) return cudaErrorNotSupported;
     int occ = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_coset_p<T, MAXT, MINB>, threads, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_coset_p<T, MAXT, MINB, SPEC>, threads, smem);
     if (occ < 1) occ = 1;
     const uint64_t ntiles = 1ull << __builtin_popcountll(p.free_mask);
     const uint64_t cap = apply_grid_cap((uint64_t)num_sms() * (uint64_t)occ * (uint64_t)(grid_mult > 0 ? grid_mult : 1));
     const unsigned grid = (unsigned)(ntiles < cap ? ntiles : cap);
-    k_coset_p<T, MAXT, MINB><<<grid, threads, smem, s>>>(a, p.kbits, p.cbits, make_runs(p.free_mask), d_offs + p.off_begin,
+    k_coset_p<T, MAXT, MINB, SPEC><<<grid, threads, smem, s>>>(a, p.kbits, p.cbits, make_runs(p.free_mask), d_offs + p.off_begin,
                                                           ntiles, p.sub_count, l2_prefetch, p.or_mask, p.free_mask,
                                                           recs);
     return cudaGetLastError();
@@ -1578,8 +1620,16 @@ cudaError_t launch_coset_param(T* a, const Pass& p, const DevSub* h_subs, const 
     }
     for (int q = 0; q < nrot; ++q) recs.trots[q] = h_trots[base + q];
     const int threads = 1 << (p.kbits - kSubDim);
-    if (sizeof(T) == 4 && occ_sel == 0 && threads <= 128)
-        return launch_coset_param_k<T, 128, 8>(a, p, recs, d_offs, l2_prefetch, grid_mult, s);
+    if (p.spec) {
+        if constexpr (sizeof(T) == 4)
+            if (occ_sel == 0 && threads <= 128)
+                return launch_coset_param_k<T, 128, 8, 1>(a, p, recs, d_offs, l2_prefetch, grid_mult, s);
+        if (threads <= kCosetThreads)
+            return launch_coset_param_k<T, kCosetThreads, PS_COSET_MINB, 1>(a, p, recs, d_offs, l2_prefetch, grid_mult, s);
+        return cudaErrorNotSupported;
+    }
+    if constexpr (sizeof(T) == 4)
+        if (occ_sel == 0 && threads <= 128) return launch_coset_param_k<T, 128, 8>(a, p, recs, d_offs, l2_prefetch, grid_mult, s);
     if (threads == 512) return launch_coset_param_k<T, 512, 1>(a, p, recs, d_offs, l2_prefetch, grid_mult, s);
     if constexpr (sizeof(T) == 4)
         if (threads == 1024) return launch_coset_param_k<T, 1024, 1>(a, p, recs, d_offs, l2_prefetch, grid_mult, s);
@@ -1724,7 +1774,7 @@ cudaError_t launch_tile(int dtype, void* a, int nl, const Pass& p, const DevSub*
     const int l2p = (tune & 1) | ((tune >> 7) & 2) | ((tune >> 7) & 4) | ((tune >> 8) & 8);
     const int occ_sel = (tune >> 1) & 7;
     const int gm = ((tune >> 4) & 15) ? ((tune >> 4) & 15) : 4;
-    if (use_tma == 2 && (tune & 1024) && h_subs && !p.spec) {
+    if (use_tma == 2 && (tune & 1024) && h_subs) {
         cudaError_t e = dtype == PS_C128
                             ? launch_coset_param<double>((double*)a, p, h_subs, h_trots, d_offs, l2p, gm, occ_sel, s)
                             : launch_coset_param<float>((float*)a, p, h_subs, h_trots, d_offs, l2p, gm, occ_sel, s);
@@ -1761,22 +1811,28 @@ cudaError_t launch_full_update(int dtype, void* a, const void* stage, uint64_t b
 }
 
 cudaError_t launch_norm(int dtype, const void* a, uint64_t n, double* d_partial, double* d_out, cudaStream_t s) {
-    const unsigned grid = red_grid(n);
-    if (dtype == PS_C128)
-        k_norm<double><<<grid, kRedThreads, 0, s>>>((const double*)a, n, d_partial);
-    else
-        k_norm<float><<<grid, kRedThreads, 0, s>>>((const float*)a, n, d_partial);
+    unsigned grid;
+    if (dtype == PS_C128) {
+        if (n >= 2) k_norm<double, 2><<<grid = red_grid(n / 2), kRedThreads, 0, s>>>((const double*)a, n, d_partial);
+        else k_norm<double, 1><<<grid = red_grid(n), kRedThreads, 0, s>>>((const double*)a, n, d_partial);
+    } else {
+        if (n >= 4) k_norm<float, 4><<<grid = red_grid(n / 4), kRedThreads, 0, s>>>((const float*)a, n, d_partial);
+        else k_norm<float, 1><<<grid = red_grid(n), kRedThreads, 0, s>>>((const float*)a, n, d_partial);
+    }
     k_final_sum<<<1, kRedThreads, 0, s>>>(d_partial, (int)grid, 1, 0, d_out);
     return cudaGetLastError();
 }
 
 cudaError_t launch_inner(int dtype, const void* a, const void* b, uint64_t n, double* d_partial, double* d_out,
                          cudaStream_t s) {
-    const unsigned grid = red_grid(n);
-    if (dtype == PS_C128)
-        k_inner<double><<<grid, kRedThreads, 0, s>>>((const double*)a, (const double*)b, n, d_partial);
-    else
-        k_inner<float><<<grid, kRedThreads, 0, s>>>((const float*)a, (const float*)b, n, d_partial);
+    unsigned grid;
+    if (dtype == PS_C128) {
+        if (n >= 2) k_inner<double, 2><<<grid = red_grid(n / 2), kRedThreads, 0, s>>>((const double*)a, (const double*)b, n, d_partial);
+        else k_inner<double, 1><<<grid = red_grid(n), kRedThreads, 0, s>>>((const double*)a, (const double*)b, n, d_partial);
+    } else {
+        if (n >= 4) k_inner<float, 4><<<grid = red_grid(n / 4), kRedThreads, 0, s>>>((const float*)a, (const float*)b, n, d_partial);
+        else k_inner<float, 1><<<grid = red_grid(n), kRedThreads, 0, s>>>((const float*)a, (const float*)b, n, d_partial);
+    }
     k_final_sum<<<1, kRedThreads, 0, s>>>(d_partial, (int)grid, 2, 0, d_out);
     k_final_sum<<<1, kRedThreads, 0, s>>>(d_partial, (int)grid, 2, 1, d_out);
     return cudaGetLastError();
@@ -1784,11 +1840,14 @@ cudaError_t launch_inner(int dtype, const void* a, const void* b, uint64_t n, do
 
 cudaError_t launch_expect(int dtype, const void* a, uint64_t n, uint64_t x0, const DevTerm* terms, int nt,
                           double* d_partial, double* d_out_slot, cudaStream_t s) {
-    const unsigned grid = red_grid(x0 ? n / 2 : n);
-    if (dtype == PS_C128)
-        k_expect<double><<<grid, kRedThreads, 0, s>>>((const double*)a, n, x0, terms, nt, d_partial);
-    else
-        k_expect<float><<<grid, kRedThreads, 0, s>>>((const float*)a, n, x0, terms, nt, d_partial);
+    unsigned grid;
+    if (dtype == PS_C128) {
+        if (n >= 4) k_expect<double, 2><<<grid = red_grid(n / 2), kRedThreads, 0, s>>>((const double*)a, n, x0, terms, nt, d_partial);
+        else k_expect<double, 1><<<grid = red_grid(n), kRedThreads, 0, s>>>((const double*)a, n, x0, terms, nt, d_partial);
+    } else {
+        if (n >= 8) k_expect<float, 4><<<grid = red_grid(n / 4), kRedThreads, 0, s>>>((const float*)a, n, x0, terms, nt, d_partial);
+        else k_expect<float, 1><<<grid = red_grid(n), kRedThreads, 0, s>>>((const float*)a, n, x0, terms, nt, d_partial);
+    }
     k_final_sum<<<1, kRedThreads, 0, s>>>(d_partial, (int)grid, 1, 0, d_out_slot);
     return cudaGetLastError();
 }

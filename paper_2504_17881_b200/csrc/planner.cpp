@@ -255,7 +255,9 @@ static void make_subgroups(const std::vector<LocalRot>& lr, int k, int phase_bit
             tr.zt = L.zt;
             if (std::fabs(c) >= std::ldexp(std::fabs(s0), -10) && !(dx == 0 && real)) {
                 // CFORM: f = cos(phi), cross coefficient +-t, t = ph * s0 / c, |t| <= 1024
-                tr.code = (uint32_t)tr_case(real, (int)dx, (int)dz) | (dx << 8) | (real ? kTrReal : 0u) | (M << 16);
+                tr.code = (dx << 8) | (real ? kTrReal : 0u) | (M << 16);
+                if (dx == 0 || (dx & (dx - 1)) == 0)  // diagonal or unit dx: a specialised case exists
+                    tr.code |= kTrUnit | (uint32_t)tu_case(real, dx ? __builtin_ctz(dx) : -1, (int)dz);
                 tr.p = ph * (s0 / c);
                 tr.s = 0.0;
                 F *= c;
@@ -289,32 +291,23 @@ static void make_subgroups(const std::vector<LocalRot>& lr, int k, int phase_bit
     }
 }
 
-// Tile-kernel variant of a pass.  The specialised kernel removes the per-pair sign flips (a
-// compile-time case per (real, dx, sign pattern)) but its 256 cases cost instruction-cache misses
-// and register shuffles; it wins on deep passes that reuse a few cases (Trotter steps, gate
-// layers) and loses on shallow memory-bound ones.
+// Tile-kernel variant of a pass.  The specialised kernel applies CFORM rotations whose dx is a unit
+// vector (or 0) with compile-time per-pair signs (80 cases), the rest generically; per-pass choice
+// (PS_OPT_SPECIALIZE=1): deep passes where most rotations have such a case.
 static void choose_spec(const PlanConfig& cfg, const Plan& plan, Pass* p) {
     if (cfg.specialize != 1) {
         p->spec = cfg.specialize == 2;
         return;
     }
-    int nrot = 0;
-    uint64_t seen[4] = {0, 0, 0, 0};
-    int distinct = 0;
+    int nrot = 0, unit = 0;
     for (int t = p->sub_begin; t < p->sub_begin + p->sub_count; ++t) {
         const DevSub& sb = plan.subs[t];
         for (int q = sb.rot_begin; q < sb.rot_begin + sb.nrot; ++q) {
-            const uint32_t code = plan.trots[q].code;
             ++nrot;
-            if (code & kTrSform) continue;
-            const uint32_t c = code & 0xffu;
-            if (!((seen[c >> 6] >> (c & 63)) & 1)) {
-                seen[c >> 6] |= 1ull << (c & 63);
-                ++distinct;
-            }
+            unit += (plan.trots[q].code & kTrUnit) ? 1 : 0;
         }
     }
-    p->spec = nrot >= kSpecMinRots && distinct <= kSpecMaxCases;
+    p->spec = nrot >= kSpecMinRots && 2 * unit >= nrot;
 }
 
 static void emit_tile(const std::vector<PhysRot>& seg, size_t b, size_t e, const PlanConfig& cfg,

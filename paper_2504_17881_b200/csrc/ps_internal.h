@@ -69,28 +69,31 @@ static_assert(sizeof(DevSub) == 56, "DevSub layout");
 // one rotation of a sub-group: pair (d, d xor dx) of the thread's 16 registers ("i" member: bit
 // highest(dx) of d is 0), sigma = parity(zr & r) xor parity(zt & i0) xor parity(Dz & d),
 // Dz_b = parity(Z_loc & u_b).
-//   code bits 0-7   CFORM case = tr_case(real, dx, Dz) (specialised kernel: a compile-time case
-//                   per (real, dx, sign pattern); dense index)
+//   code bits 0-6   (with bit 15) unit case = tu_case(real, log2 dx, Dz pattern) of a CFORM rotation
+//                   whose dx is 0 (diagonal) or a unit vector: the specialised kernel applies it with
+//                   compile-time per-pair signs
 //   code bits 8-11  dx (0: diagonal, imaginary only)
 //   code bit  12    REAL: B real (y odd) or imaginary (y even), as in DevRot
 //   code bit  13    SFORM (else CFORM)
 //   code bit  14    NEG (SFORM only): B/f = -1 (REAL) or -i (imaginary) instead of +1 / +i
+//   code bit  15    UNIT: bits 0-6 hold the unit case
 //   code bits 16-31 M, bit d = parity(Dz & d) (generic kernel: per-pair sign at run time)
-constexpr uint32_t kTrReal = 1u << 12, kTrSform = 1u << 13, kTrNeg = 1u << 14;
+constexpr uint32_t kTrReal = 1u << 12, kTrSform = 1u << 13, kTrNeg = 1u << 14, kTrUnit = 1u << 15;
 #ifdef __CUDACC__
 #define PS_HD __host__ __device__
 #else
 #define PS_HD
 #endif
-constexpr int kSpecMinRots = 16, kSpecMaxCases = 32;  // planner: choose_spec (auto)
-PS_HD constexpr int tr_hibit(int v) { return v >= 8 ? 3 : v >= 4 ? 2 : v >= 2 ? 1 : 0; }
-// CFORM case index: 0..15 diagonal (imaginary) by Dz; then 8 Dz patterns (bit highest(dx)
-// removed) per (real, dx), dx = 1..15
-PS_HD constexpr int tr_case(int real, int dx, int dz) {
-    return dx == 0 ? (dz & 15)
-                   : 16 + (real * 15 + dx - 1) * 8 +
-                         ((dz & ((1 << tr_hibit(dx)) - 1)) | ((dz >> (tr_hibit(dx) + 1)) << tr_hibit(dx)));
+constexpr int kSpecMinRots = 16;  // planner: choose_spec (per-pass choice)
+// unit case index: 0..15 diagonal (imaginary) by Dz; 16 + ((real * 4 + log2 dx) * 8 + the three Dz
+// bits other than the pivot's), dx in {1, 2, 4, 8}
+constexpr int kUnitCases = 80;
+PS_HD constexpr int tu_case(int real, int dxi, int dz) {
+    return dxi < 0 ? (dz & 15)
+                   : 16 + ((real * 4 + dxi) << 3) + ((dz & ((1 << dxi) - 1)) | ((dz >> (dxi + 1)) << dxi));
 }
+// inverse of the pattern compression: the 4-bit Dz (pivot bit clear) of unit case pattern z3
+PS_HD constexpr int tu_dz(int dxi, int z3) { return (z3 & ((1 << dxi) - 1)) | ((z3 >> dxi) << (dxi + 1)); }
 struct DevTRot {
     uint32_t code;
     uint32_t zr;   // tile-local phase mask (parity with the coset representative r)

@@ -373,3 +373,41 @@ def test_option_validation_and_restore():
         a0 = st.get_amplitudes()
         st.set_option(ps.OPT_TILE_BITS, 5)  # valid options leave the state alone
         assert np.array_equal(st.get_amplitudes(), a0)
+
+
+def test_create_entry_points_directly():
+    """ps_create and ps_create_dist called through the C ABI (not via the State class): |0> after
+    creation, a layer against the oracle, and every argument check of include/ps.h."""
+    import ctypes
+    L = P.lib()
+    h = ctypes.c_void_p()
+    assert L.ps_create(10, ps.C128, ctypes.byref(h)) == 0
+    nq, nl, rk, wd, dt = (ctypes.c_int() for _ in range(5))
+    assert L.ps_info(h, ctypes.byref(nq), ctypes.byref(nl), ctypes.byref(rk), ctypes.byref(wd), ctypes.byref(dt), None) == 0
+    assert (nq.value, nl.value, rk.value, wd.value, dt.value) == (10, 10, 0, 1, ps.C128)
+    out = np.zeros(1 << 10, np.complex128)
+    assert L.ps_get_amplitudes(h, 0, 1 << 10, out.ctypes.data_as(ctypes.c_void_p)) == 0
+    assert out[0] == 1 and np.count_nonzero(out) == 1
+    codes, ang, want = _want(10, "R10", 200, 1)
+    x, z = P.pauli_encode_codes(codes)
+    assert L.ps_init_random(h, SEED) == 0
+    assert L.ps_apply_rotations(h, x.ctypes.data_as(ctypes.c_void_p), z.ctypes.data_as(ctypes.c_void_p),
+                                np.ascontiguousarray(ang).ctypes.data_as(ctypes.c_void_p), len(ang)) == 0
+    assert L.ps_get_amplitudes(h, 0, 1 << 10, out.ctypes.data_as(ctypes.c_void_p)) == 0
+    assert np.max(np.abs(out - want)) <= 1e-10
+    assert L.ps_destroy(h) == 0
+    h2 = ctypes.c_void_p()
+    assert L.ps_create_dist(9, ps.C64, 0, 1, None, ctypes.byref(h2)) == 0  # world 1: no NCCL id needed
+    assert L.ps_info(h2, ctypes.byref(nq), ctypes.byref(nl), None, ctypes.byref(wd), ctypes.byref(dt), None) == 0
+    assert (nq.value, nl.value, wd.value, dt.value) == (9, 9, 1, ps.C64)
+    assert L.ps_destroy(h2) == 0
+    bad = ctypes.c_void_p()
+    assert L.ps_create(0, ps.C128, ctypes.byref(bad)) == -1
+    assert L.ps_create(63, ps.C128, ctypes.byref(bad)) == -1
+    assert L.ps_create(10, 7, ctypes.byref(bad)) == -1
+    assert L.ps_create_dist(10, ps.C128, 0, 3, None, ctypes.byref(bad)) == -1   # world not a power of two
+    assert L.ps_create_dist(10, ps.C128, 2, 2, None, ctypes.byref(bad)) == -1   # rank >= world
+    assert L.ps_create_dist(10, ps.C128, 0, 2, None, ctypes.byref(bad)) == -1   # world > 1 without an id
+    assert L.ps_create_dist(1, ps.C128, 0, 2, None, ctypes.byref(bad)) == -1    # no local qubit left
+    assert L.ps_create(10, ps.C128, None) == -1
+    assert not bad.value
