@@ -45,7 +45,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--qubits", dest="n", type=int, default=30)
     ap.add_argument("--layer", type=int, default=1000)
-    ap.add_argument("--kind", default="R10", help="R10 R4 D S8 LOW (random layers), JW (Trotter step), QAOA, GATES, UCC, HEA (VQE)")
+    ap.add_argument("--kind", default="R10", help="R10 R4 D S8 LOW (random layers), JW (Trotter step), QAOA, GATES, UCC, HEA (VQE), SUFFIX (L-groups)")
     ap.add_argument("--terms", type=int, default=92968, help="JW: Hamiltonian terms (Table 3: 92,968 at 32q)")
     ap.add_argument("--lam", type=float, default=27.0, help="JW: lambda = sum |h| (Table 3)")
     ap.add_argument("--delta", type=float, default=0.5, help="JW: Trotter step size")
@@ -61,6 +61,10 @@ def parse():
     ap.add_argument("--overlap", type=int, default=1, help="world > 1: overlap swaps with the next pass")
     ap.add_argument("--specialize", type=int, default=0,
                     help="tile-kernel variant: 0 generic (default), 2 specialised, 1 planner's per-pass choice")
+    ap.add_argument("--group", type=int, default=10, help="SUFFIX: rotations per group sharing an upper string")
+    ap.add_argument("--fused", type=int, default=1, help="world > 1: fused exchange + tile kernel (1) or swaps (0)")
+    ap.add_argument("--emulate", type=int, default=0,
+                    help="run the multi-rank path as G virtual ranks on this one GPU (ps_create_emulated)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     return ap.parse_args()
@@ -82,6 +86,9 @@ def workload_name(args):
         return f"{args.n}q {prec} QAOA MaxCut, random 3-regular graph, p = {args.layer} layers"
     if args.kind == "GATES":
         return f"{args.n}q {prec} random gate brickwork of depth {args.layer}, converted to rotations"
+    if args.kind == "SUFFIX":
+        return (f"{args.n}q {prec} groups of L={args.group} rotations sharing an upper string on the "
+                f"partitioned qubits (P:502-508), {args.layer} rotations/step")
     if args.kind == "UCC":
         return (f"{args.n}q {prec} UCCSD-shaped VQE layer (JW; {args.n // 3} occupied spin orbitals, "
                 f"singles + {args.layer} sampled doubles x 8 strings)")
@@ -108,6 +115,14 @@ def layers(args, count, world=1):
     if args.kind == "GATES":
         x, z, ang = P.circuit_to_rotations(workloads.gate_circuit(args.n, args.layer, seed=0))
         return [(x, z, ang)] * count
+    if args.kind == "SUFFIX":
+        m = max(1, world.bit_length() - 1)
+        out = []
+        for s in range(count):
+            codes, ang = workloads.suffix_groups(args.n, args.layer, args.group, m, seed=1000 + s)
+            x, z = P.pauli_encode_codes(codes)
+            out.append((x, z, ang))
+        return out
     if args.kind == "UCC":
         codes, ang = workloads.ucc_layers(args.n, args.n // 3, seed=0, max_doubles=args.layer)
         x, z = P.pauli_encode_codes(codes)
@@ -374,7 +389,12 @@ def run_ours(args):
         if world > 1:
             dist.barrier()
 
-    st = P.State(args.n, args.dtype, world=world, rank=rank, torch_memory=True)
+    if args.emulate and world > 1:
+        raise SystemExit("--emulate runs on one GPU (no torchrun)")
+    if args.emulate:
+        st = P.State(args.n, args.dtype, emulate=args.emulate, torch_memory=True)
+    else:
+        st = P.State(args.n, args.dtype, world=world, rank=rank, torch_memory=True)
     st.set_option(ps.OPT_FUSION, args.fusion)
     if args.tile_bits:
         st.set_option(ps.OPT_TILE_BITS, args.tile_bits)
@@ -387,8 +407,9 @@ def run_ours(args):
     st.set_option(ps.OPT_TRANSPORT, args.transport)
     st.set_option(ps.OPT_OVERLAP, args.overlap)
     st.set_option(ps.OPT_SPECIALIZE, args.specialize)
+    st.set_option(ps.OPT_FUSED_EXCHANGE, args.fused)
     st.set_option(ps.OPT_PROFILE, 1)
-    enc = layers(args, args.warmup + args.steps, world)
+    enc = layers(args, args.warmup + args.steps, args.emulate or world)
     rot_per_step = len(enc[0][2])
     st.init_random(workloads.BASE_SEED)
 
@@ -422,8 +443,10 @@ def run_ours(args):
     ms_per_step = ms / args.steps
     value = rot_per_step / (ms_per_step / 1e3)
     amp_bytes = 16 if args.dtype == "c128" else 8
+    # emulation: every virtual rank's slice lives on this GPU; stats are rank 0's
+    ranks = args.emulate or world
     local_state = amp_bytes << (args.n - (world.bit_length() - 1))
-    hbm_alg = sum(stats["algo_bytes"][k] for k in PASS_FAMS) / (ms / 1e3) / 1e9 * world
+    hbm_alg = sum(stats["algo_bytes"][k] for k in PASS_FAMS) / (ms / 1e3) / 1e9 * ranks
 
     # dominant kernel roofline (CUDA events around each launch on the launching stream)
     fam = max(PASS_FAMS, key=lambda k: stats["kernel_ms"][k])
@@ -441,20 +464,22 @@ def run_ours(args):
     e2e = None
     if not args.no_e2e:
         tdt = torch.float64 if args.dtype == "c128" else torch.float32
-        host = torch.empty(local_state // (amp_bytes // 2), dtype=tdt, pin_memory=True)
+        host = torch.empty((amp_bytes << args.n if args.emulate else local_state) // (amp_bytes // 2), dtype=tdt,
+                           pin_memory=True)
         st.init_random(workloads.BASE_SEED)
         host.copy_(st._tensor)  # the seeded initial state, staged in pinned host memory (untimed)
-        h2d = local_state + 24 * rot_per_step
+        h2d = (amp_bytes << args.n if args.emulate else local_state) + 24 * rot_per_step
         e_steps = min(args.steps, 2)
         x, z, a = enc[0]
-        st.set_state_ptr(host.data_ptr(), 1 << (args.n - (world.bit_length() - 1)), first=rank << st.n_local)
+        cnt, first = (1 << args.n, 0) if args.emulate else (1 << st.n_local, rank << st.n_local)
+        st.set_state_ptr(host.data_ptr(), cnt, first=first)
         st.apply_rotations(x, z, a)
         st.norm()
         barrier()
         t0 = time.perf_counter()
         for s in range(e_steps):
             x, z, a = enc[(args.warmup + s) % len(enc)]
-            st.set_state_ptr(host.data_ptr(), 1 << st.n_local, first=rank << st.n_local)
+            st.set_state_ptr(host.data_ptr(), cnt, first=first)
             st.apply_rotations(x, z, a)
             st.norm()
         barrier()
@@ -478,7 +503,9 @@ def run_ours(args):
             "config": {"workload": workload_name(args), "n_qubits": args.n, "rotations_per_step": rot_per_step,
                        "fusion": args.fusion, "tile_mode": args.tile_mode, "tile_bits": args.tile_bits or (12 if args.dtype == "c128" else 11),
                        "layout": args.layout, "transport": args.transport, "overlap": args.overlap, "specialize": args.specialize,
-                       "parallelism": f"state sharded over {world} GPU(s) by top qubits",
+                       "parallelism": (f"state sharded over {args.emulate} virtual ranks on 1 GPU (emulation)"
+                                       if args.emulate else f"state sharded over {world} GPU(s) by top qubits"),
+                       "fused_exchange": args.fused, "group": args.group if args.kind == "SUFFIX" else None,
                        "l2": "inputs larger than L2 (state %.1f GiB per GPU)" % (local_state / 2 ** 30)},
             "hbm_gbs": hbm_alg,
             "bytes_per_rotation": stats["algo_bytes"]["stream"] / max(1, stats["rotations_by"]["stream"])

@@ -55,3 +55,23 @@ def estimate(zs, delta: float) -> float:
         theta = (base + 2 * math.pi * j) / k
     theta = (theta + math.pi) % (2 * math.pi) - math.pi
     return theta / delta
+
+
+def z0_basis(n: int, HD, HR, delta: float, r: int, seed: int, b: int, dtype: str = "c128", world: int = 1,
+             rank: int = 0, emulate: int = 0, offset: float = 0.0, state=None) -> complex:
+    """Z_0 = <b| e^{i delta H~(delta)} |b> for a basis guiding state |b> (Fig. 4):
+    one partially randomized second-order step applied to |b> through ps_apply_rotations, then the
+    amplitude b read back (no second state: the overlap with a basis state is one amplitude).  A
+    caller-provided `state` (a State of n qubits) is reused instead of allocating one."""
+    x, z, a = formulas.evolution_stream(HD, HR, delta, 1, r, seed)
+    kw = dict(emulate=emulate) if emulate else dict(world=world, rank=rank)
+    own = state is None
+    st = State(n, dtype, **kw) if own else state
+    try:
+        st.init_basis(int(b))
+        st.apply_rotations(x, z, a)
+        z0 = complex(st.get_amplitudes(int(b), 1)[0])
+    finally:
+        if own:
+            st.close()
+    return z0 * cmath.exp(1j * offset * delta)

@@ -228,3 +228,26 @@ def test_rpe_signal_emulated():
         sx, sz, sa = formulas.evolution_stream(HD, HR, 0.3, 2 ** m, r, 3)
         want = oracle.inner(n, psi0, oracle.apply_masks(n, psi0, sx, sz, sa))
         assert abs(zm - want) <= 1e-10
+
+
+def test_z0_basis_coset_oracle():
+    """NEXT-3 (Fig. 4 analog): Z_0 = <b|e^{i delta H~}|b> of one partially randomized
+    second-order step of a JW-shaped Hamiltonian whose X support lies on 14 qubits of a 24-qubit
+    register (Z letters everywhere), on 1 GPU and on 4 virtual ranks, against the coset oracle."""
+    from paper_2504_17881_b200 import formulas, rpe
+    n = 24
+    pos = list(range(n - 14, n))
+    codes, coeffs = workloads.jw_embedded(n, pos, 3000, 20.0, seed=3)
+    x, z = P.pauli_encode_codes(codes)
+    H = formulas.from_masks(n, x, z, coeffs)
+    HD, HR = formulas.split_deterministic(H, 400)
+    b = sum(1 << q for q in range(0, n, 2))
+    for d in (0.05, 0.3):
+        r = formulas.sample_count(HR.lam, d, 0)
+        sx, sz, sa = formulas.evolution_stream(HD, HR, d, 1, r, 11)
+        mem = oracle.coset_members(n, b, np.unique(sx))
+        out = oracle.apply_coset(n, mem, (mem == b).astype(np.complex128), oracle.decode_masks(n, sx, sz), sa)
+        want = complex(out[np.searchsorted(mem, b)])
+        assert abs(rpe.z0_basis(n, HD, HR, d, r, 11, b) - want) <= 1e-10
+        assert abs(rpe.z0_basis(n, HD, HR, d, r, 11, b, emulate=4) - want) <= 1e-10
+        assert 0.0 < abs(want) <= 1.0 + 1e-12

@@ -304,3 +304,24 @@ def hardware_efficient_vqe(n: int, depth: int, seed: int = 0):
         for q in range(n - 1):
             gates.append(("CNOT", (q, q + 1), ()))
     return gates
+
+
+def suffix_groups(n: int, count: int, L: int, m: int, seed: int = 0):
+    """The paper's benchmark workload: groups of L consecutive rotations sharing a
+    common upper string Q~ on the top m qubits (Eq. (1); at least one X/Y letter, so every
+    group needs an exchange on m >= 1 partitioned qubits) with random lower strings (R10 recipe on
+    the n - m low qubits), `count` rotations in total.  Returns (codes, angles)."""
+    if m < 1:
+        raise ValueError("suffix groups need m >= 1 upper qubits")
+    rng = _rng(2_000_000 + n * 100 + L * 7 + m + seed)
+    codes = np.zeros((count, n), dtype=np.uint8)
+    low, _ = random_layer(n - m, count, seed=seed + 17, kind="R10")
+    codes[:, :n - m] = low
+    for g0 in range(0, count, L):
+        while True:
+            up = rng.integers(0, 4, size=m, dtype=np.uint8)
+            if np.any((up == X) | (up == Y)):
+                break
+        codes[g0:g0 + L, n - m:] = up
+    angles = rng.uniform(-np.pi, np.pi, size=count)
+    return codes, angles
