@@ -130,11 +130,12 @@ enum {
                                  available (default); 0 = NCCL send/recv with staging */
     PS_OPT_OVERLAP = 11,      /* world > 1, P2P: 1 = overlap each swap with the following tile pass
                                  on a second stream (default); 0 = serialise */
-    PS_OPT_SPECIALIZE = 12    /* tile-kernel variant: 0 = generic (default; per-pair signs at run
-                                 time), 2 = specialised (a compile-time case per (real, dx, sign
-                                 pattern): no per-pair sign flips, but 256 cases cost i-cache
-                                 misses and register shuffles), 1 = planner's per-pass choice
-                                 (specialised for passes of >= 16 rotations using <= 32 cases).
+    PS_OPT_SPECIALIZE = 12    /* tile-kernel variant: 2 = specialised (default for C128): CFORM
+                                 rotations whose sub-group xor mask dx is a unit vector or 0 run
+                                 through one of 80 compile-time cases (per-pair signs and pairing
+                                 fixed, no sign flips), the rest generically; 0 = generic (default
+                                 for C64: per-pair signs at run time); 1 = planner's per-pass choice
+                                 (specialised for passes of >= 16 rotations, half of them unit).
                                  Bitwise-identical results (same operations in the same order) */,
     PS_OPT_GRID_CAP = 13,     /* test knob: cap on the persistent tile grid (CTAs), so small states
                                  run several tiles per CTA (incremental tile bases, next-tile

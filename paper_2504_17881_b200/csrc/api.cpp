@@ -412,6 +412,9 @@ static int make_state(int n_qubits, int dtype, void* dev_buf, size_t bytes, void
     // where the prefetch costs more occupancy than it hides
     h->tile_bits = dtype == PS_C128 ? 12 : 11;
     h->tile_tune = dtype == PS_C128 ? (1536 | 2048) : 1536;
+    // fp64: unit-dx CFORM rotations with compile-time signs (+6 % R10, +9 % JW, +15 % gates;
+    // profiles/r02/kernel_ab.md); fp32 keeps the generic kernel (its 64-register 8-CTA build spills)
+    h->specialize = dtype == PS_C128 ? 2 : 0;
     cudaError_t e = cudaGetDevice(&h->device);
     if (e != cudaSuccess) {
         delete h;

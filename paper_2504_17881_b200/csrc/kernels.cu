@@ -1443,6 +1443,9 @@ __global__ void k_p2p_swap(T* __restrict__ local, T* __restrict__ peer, uint64_t
             }
         }
     }
+    // the stores into the partner's memory are performed at system scope before this thread
+    // retires (the NCCL barrier after the launch then orders them before the partner's next reads)
+    __threadfence_system();
 }
 
 // Eq. (core_state) helpers (PS_OPT_LAYOUT=2)

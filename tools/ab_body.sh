@@ -22,3 +22,8 @@ for lib in old new; do
   done
 done
 unset PS_LIB_PATH
+# deep-pass profile (JW Trotter step) with the new body and unit specialisation
+B1="python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu --kind JW --specialize 2"
+$B1 > gpurun_out/body/jw_plain.log 2>&1 && \
+ncu --set full --clock-control none --import-source on -k regex:k_coset -s 20 -c 1 -o gpurun_out/body/prof_jw $B1 > gpurun_out/body/ncu_jw.log 2>&1
+echo "ncu jw rc=$?"
