@@ -1125,7 +1125,7 @@ static int exchange_full_group(const RankSet& rs, const std::vector<Plan*>& plan
 
 static bool can_fuse(const ps_state* h, const Pass& ex, const Pass* np) {
     return h->fused && h->p2p && h->transport && h->world > 1 && ex.kind == PASS_EXCHANGE && !ex.full && np &&
-           (np->kind == PASS_TILE || np->kind == PASS_COSET) && h->tile_tma == 2 && !np->spec;
+           (np->kind == PASS_TILE || np->kind == PASS_COSET) && h->tile_tma == 2;
 }
 
 static int exchange_fused(const RankSet& rs, const std::vector<Plan*>& plans, size_t pi) {

@@ -636,7 +636,10 @@ __device__ __forceinline__ uint64_t pdep64(uint64_t v, uint64_t mask) {
 // indices, so each warp load covers contiguous 256-B chunks), the last sub-group scatters
 // straight back; shared memory holds the tile only between sub-groups.
 
-constexpr int kCosetThreads = 256;
+#ifndef PS_COSET_THREADS
+#define PS_COSET_THREADS 256
+#endif
+constexpr int kCosetThreads = PS_COSET_THREADS;  // 2^12 fp64 tiles: 256 threads x 16 amplitudes
 
 // chunk-offset table size in shared memory, rounded up so the tile that follows is 128-B aligned
 __host__ __device__ inline size_t coset_off_bytes(int hbits) {
@@ -845,7 +848,7 @@ __device__ __forceinline__ uint32_t flag_acquire(const uint32_t* p) {
     return v;
 }
 
-template <typename T>
+template <typename T, int SPEC>
 __global__ void __launch_bounds__(kCosetThreads, 1) k_xtile(const __grid_constant__ XTileParams P) {
     using V2 = typename SmemAmp<T>::V;
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -890,7 +893,7 @@ __global__ void __launch_bounds__(kCosetThreads, 1) k_xtile(const __grid_constan
                     vi[d] = v.y;
                 }
             }
-            sub_apply<T, 0, 0>(vr, vi, R.trots, h.rb, h.nr, h.r, i0);
+            sub_apply<T, SPEC, 0>(vr, vi, R.trots, h.rb, h.nr, h.r, i0);
             if (h.F != 1.0) sub_scale<T>(vr, vi, (T)h.F);
             if (s == 0) {
                 // every thread has consumed its loads of this tile: tell the partner its reads of my
@@ -1624,9 +1627,12 @@ cudaError_t launch_coset_param(T* a, const Pass& p, const DevSub* h_subs, const 
     for (int q = 0; q < nrot; ++q) recs.trots[q] = h_trots[base + q];
     const int threads = 1 << (p.kbits - kSubDim);
     if (p.spec) {
-        if constexpr (sizeof(T) == 4)
+        if constexpr (sizeof(T) == 4) {
             if (occ_sel == 0 && threads <= 128)
                 return launch_coset_param_k<T, 128, 8, 1>(a, p, recs, d_offs, l2_prefetch, grid_mult, s);
+            if (occ_sel == 2 && threads <= 128)  // 6 CTAs per SM (85 registers): room for the 80 cases
+                return launch_coset_param_k<T, 128, 6, 1>(a, p, recs, d_offs, l2_prefetch, grid_mult, s);
+        }
         if (threads <= kCosetThreads)
             return launch_coset_param_k<T, kCosetThreads, PS_COSET_MINB, 1>(a, p, recs, d_offs, l2_prefetch, grid_mult, s);
         return cudaErrorNotSupported;
@@ -1684,7 +1690,7 @@ cudaError_t launch_tile_t(T* a, int nl, const Pass& p, const DevSub* d_subs, con
     return cudaGetLastError();
 }
 
-template <typename T>
+template <typename T, int SPEC>
 cudaError_t launch_xtile_t(const XTileRank* ranks, int nranks, const Pass& p, const uint64_t* d_offs, int ell,
                            uint64_t dtau, uint32_t epoch, cudaStream_t s, int grid_cap) {
     if (nranks < 1 || nranks > kMaxXRanks) return cudaErrorInvalidValue;
@@ -1694,11 +1700,11 @@ cudaError_t launch_xtile_t(const XTileRank* ranks, int nranks, const Pass& p, co
     static uint64_t attr_devices = 0;
     const int dev = current_device();
     if (!((attr_devices >> dev) & 1)) {
-        cudaFuncSetAttribute(k_xtile<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        cudaFuncSetAttribute(k_xtile<T, SPEC>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         attr_devices |= 1ull << dev;
     }
     int occ = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_xtile<T>, threads, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_xtile<T, SPEC>, threads, smem);
     if (occ < 1) return cudaErrorInvalidConfiguration;
     // every CTA of the launch must be resident at once (CTAs wait on each other's flags)
     const uint64_t ntiles = 1ull << __builtin_popcountll(p.free_mask);
@@ -1721,7 +1727,7 @@ cudaError_t launch_xtile_t(const XTileRank* ranks, int nranks, const Pass& p, co
     P.ell = ell;
     P.epoch = epoch;
     void* args[] = {&P};
-    return cudaLaunchCooperativeKernel((const void*)k_xtile<T>, dim3((unsigned)(per * nranks)), dim3(threads), args,
+    return cudaLaunchCooperativeKernel((const void*)k_xtile<T, SPEC>, dim3((unsigned)(per * nranks)), dim3(threads), args,
                                        smem, s);
 }
 
@@ -1953,8 +1959,11 @@ cudaError_t launch_xtile(int dtype, const XTileRank* ranks, int nranks, const Pa
                          const uint64_t* h_offs, int ell, uint32_t epoch, cudaStream_t s, int grid_cap) {
     if (p.or_mask) return cudaErrorInvalidValue;
     const uint64_t dtau = xtile_dtau(p, h_offs, ell);
-    if (dtype == PS_C128) return launch_xtile_t<double>(ranks, nranks, p, d_offs, ell, dtau, epoch, s, grid_cap);
-    return launch_xtile_t<float>(ranks, nranks, p, d_offs, ell, dtau, epoch, s, grid_cap);
+    if (dtype == PS_C128)
+        return p.spec ? launch_xtile_t<double, 1>(ranks, nranks, p, d_offs, ell, dtau, epoch, s, grid_cap)
+                      : launch_xtile_t<double, 0>(ranks, nranks, p, d_offs, ell, dtau, epoch, s, grid_cap);
+    return p.spec ? launch_xtile_t<float, 1>(ranks, nranks, p, d_offs, ell, dtau, epoch, s, grid_cap)
+                  : launch_xtile_t<float, 0>(ranks, nranks, p, d_offs, ell, dtau, epoch, s, grid_cap);
 }
 
 cudaError_t launch_expect_cross(int dtype, const void* a, const void* stage, uint64_t base, uint64_t count,
