@@ -109,16 +109,15 @@ enum {
                                  3 = TMA-bulk-prefetched double buffer (A/B) */
     PS_OPT_CHUNK_BITS = 7,    /* min log2 contiguous amplitudes per gathered chunk (0 = default 4:
                                  256 B for C128, 128 B for C64) */
-    PS_OPT_TILE_TUNE = 8,     /* register-direct tile kernel tuning bits: 0 = TMA bulk L2 prefetch of
-                                 the next tile, 1-3 = CTAs per SM: 0 per-dtype default (fp64
-                                 uncapped, fp32 8), 1/2/3 register cap for 5/6/8, 4 uncapped, 4-7 =
-                                 persistent-grid multiplier, 8 = per-thread L2 prefetch, 9 = L2::256B
-                                 sector promotion on the gathered loads, 10 = the pass's records
-                                 in the launch's parameter block (uniform constant-bank loads;
-                                 passes of <= 256 rotations), 11 = LDGSTS prefetch of the next
-                                 tile's first sub-group into shared memory while the current
-                                 tile's last sub-group is computed and stored (default C128 3584
-                                 = bits 9 + 10 + 11, C64 1536 = bits 9 + 10) */
+    PS_OPT_TILE_TUNE = 8,     /* register-direct tile kernel tuning bits: 1-3 = CTAs per SM (0 per-dtype
+                                 default: fp64 uncapped = 2, fp32 8; 1/2/3 register cap for 5/6/8
+                                 CTAs of 128 threads), 4-7 = persistent-grid multiplier (default 4),
+                                 9 = L2::256B sector promotion on the gathered loads, 10 = the pass's
+                                 records in the launch's parameter block (uniform constant loads;
+                                 passes of <= 256 rotations), 11 = LDGSTS prefetch of the next tile's
+                                 first sub-group into shared memory while the current tile's last
+                                 sub-group is computed and stored (default C128 3584 = bits
+                                 9 + 10 + 11, C64 1536 = bits 9 + 10) */
     PS_OPT_LAYOUT = 9,        /* world > 1: 1 = lazy qubit-swap layout kept across calls, swaps chosen
                                  by furthest next use (default); 0 = one half-vector exchange per run
                                  sharing the upper X-part, swapped back at once (Eq. (1) economy);

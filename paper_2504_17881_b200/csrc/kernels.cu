@@ -392,14 +392,25 @@ __host__ __device__ constexpr int par4(int v) { return (v ^ (v >> 1) ^ (v >> 2) 
 
 // one CFORM rotation with a compile-time pair pattern (dx = DX) and sign pattern parity(DZ & d):
 // four fused multiply-adds per pair, the signs ride on the FMA operands
-template <int REAL, int DX, int DZ, typename T>
-__device__ __forceinline__ void cform_sub(T (&vr)[kSubAmps], T (&vi)[kSubAmps], T t) {
+// one CFORM rotation with a compile-time pair pattern (dx = DX) and sign pattern parity(DZ & d):
+// four fused multiply-adds per pair, the signs ride on the FMA operands.
+// MODE 0: registers -> registers.  The update of each pair's two-cycles writes one member to a
+// temporary that has to be moved back to its register before the next rotation.
+// MODE 1 ("ping"): the new values of the i-members (pivot bit clear; diagonal: every real part)
+// go to tb[] and stay there; MODE 2 ("pong"): the next rotation, with the SAME dx, reads them from
+// tb[] and writes every value back to its register.  A run of same-dx rotations (a same-x run
+// of a Trotter step, consecutive ZZ terms) then needs no register moves.  Same operations, same
+// order: bitwise identical to MODE 0.
+template <int REAL, int DX, int DZ, int MODE, typename T>
+__device__ __forceinline__ void cform_sub(T (&vr)[kSubAmps], T (&vi)[kSubAmps], T (&tb)[kSubAmps], T t) {
     if constexpr (DX == 0) {
 #pragma unroll
         for (int d = 0; d < kSubAmps; ++d) {
             const T b = par4(DZ & d) ? -t : t;
-            const T nr = pfma(-b, vi[d], vr[d]), ni = pfma(b, vr[d], vi[d]);
-            vr[d] = nr;
+            const T re = MODE == 2 ? tb[d] : vr[d];
+            const T nr = pfma(-b, vi[d], re), ni = pfma(b, re, vi[d]);
+            if (MODE == 1) tb[d] = nr;
+            else vr[d] = nr;
             vi[d] = ni;
         }
     } else if constexpr (DX < kSubAmps) {
@@ -408,29 +419,40 @@ __device__ __forceinline__ void cform_sub(T (&vr)[kSubAmps], T (&vi)[kSubAmps], 
         for (int d = 0; d < kSubAmps; ++d) {
             if ((d >> piv) & 1) continue;
             const int e = d ^ DX;
+            const int k = (d & ((1 << piv) - 1)) | ((d >> (piv + 1)) << piv);  // i-member index
             const T b = par4(DZ & d) ? -t : t;
+            const T ir = MODE == 2 ? tb[2 * k] : vr[d], ii = MODE == 2 ? tb[2 * k + 1] : vi[d];
+            T nir, nii, njr, nji;
             if (REAL) {
-                const T nir = pfma(-b, vr[e], vr[d]), nii = pfma(-b, vi[e], vi[d]);
-                const T njr = pfma(b, vr[d], vr[e]), nji = pfma(b, vi[d], vi[e]);
-                vr[d] = nir; vi[d] = nii; vr[e] = njr; vi[e] = nji;
+                nir = pfma(-b, vr[e], ir); nii = pfma(-b, vi[e], ii);
+                njr = pfma(b, ir, vr[e]); nji = pfma(b, ii, vi[e]);
             } else {
-                const T nir = pfma(-b, vi[e], vr[d]), nii = pfma(b, vr[e], vi[d]);
-                const T njr = pfma(-b, vi[d], vr[e]), nji = pfma(b, vr[d], vi[e]);
-                vr[d] = nir; vi[d] = nii; vr[e] = njr; vi[e] = nji;
+                nir = pfma(-b, vi[e], ir); nii = pfma(b, vr[e], ii);
+                njr = pfma(-b, ii, vr[e]); nji = pfma(b, ir, vi[e]);
             }
+            if (MODE == 1) {
+                tb[2 * k] = nir;
+                tb[2 * k + 1] = nii;
+            } else {
+                vr[d] = nir;
+                vi[d] = nii;
+            }
+            vr[e] = njr;
+            vi[e] = nji;
         }
     }
 }
 
 // unit cases (ps_internal.h tu_case): diagonal by its 4-bit Dz, unit dx by (real, log2 dx, the three
 // Dz bits other than the pivot's); signs and the pair pattern are compile-time
-#define PS_UD(Z) case Z: cform_sub<0, 0, Z, T>(vr, vi, t); break;
-#define PS_UC(R, XI, Z3) case tu_case(R, XI, tu_dz(XI, Z3)): cform_sub<R, (1 << XI), tu_dz(XI, Z3), T>(vr, vi, t); break;
+#define PS_UD(Z) case Z: cform_sub<0, 0, Z, MODE, T>(vr, vi, tb, t); break;
+#define PS_UC(R, XI, Z3) case tu_case(R, XI, tu_dz(XI, Z3)): cform_sub<R, (1 << XI), tu_dz(XI, Z3), MODE, T>(vr, vi, tb, t); break;
 #define PS_UC8(R, XI) PS_UC(R, XI, 0) PS_UC(R, XI, 1) PS_UC(R, XI, 2) PS_UC(R, XI, 3) PS_UC(R, XI, 4) \
     PS_UC(R, XI, 5) PS_UC(R, XI, 6) PS_UC(R, XI, 7)
 
-template <typename T>
-__device__ __forceinline__ void unit_dispatch(T (&vr)[kSubAmps], T (&vi)[kSubAmps], uint32_t ucase, T t) {
+template <int MODE, typename T>
+__device__ __forceinline__ void unit_dispatch(T (&vr)[kSubAmps], T (&vi)[kSubAmps], T (&tb)[kSubAmps], uint32_t ucase,
+                                              T t) {
     switch (ucase) {
         PS_UD(0) PS_UD(1) PS_UD(2) PS_UD(3) PS_UD(4) PS_UD(5) PS_UD(6) PS_UD(7)
         PS_UD(8) PS_UD(9) PS_UD(10) PS_UD(11) PS_UD(12) PS_UD(13) PS_UD(14) PS_UD(15)
@@ -446,37 +468,72 @@ __device__ __forceinline__ void unit_dispatch(T (&vr)[kSubAmps], T (&vi)[kSubAmp
 // applies the rotations [rb, rb + nr) of a sub-group to the thread's 16 registers; the next
 // record is fetched while the current one is applied.  SPEC = 0: generic (one switch on dx, the
 // per-pair signs from M at run time); SPEC = 1: CFORM rotations through the specialised cases.
+// one rotation record decoded for the thread: the code, the coefficient with the thread-wide sign
+// s0 = parity(zr & r) xor parity(zt & i0) folded in (specialised unit cases), and the per-pair
+// sign mask (generic cases)
+template <typename T>
+struct RotPrep {
+    uint32_t code, ms;
+    T t, tf;
+};
+
+template <typename T, int PARAM>
+__device__ __forceinline__ RotPrep<T> prep_rot(const DevTRot* __restrict__ tr, uint32_t r, uint64_t i0) {
+    const uint4 h = ldr<PARAM>(reinterpret_cast<const uint4*>(tr));
+    const double pc = ldr<PARAM>(&tr->p);
+    RotPrep<T> o;
+    o.code = h.x;
+    const uint64_t zt = ((uint64_t)h.w << 32) | h.z;
+    const int s0 = par32(h.y & r) ^ par64(zt & i0);
+    o.t = (T)pc;
+    o.tf = flip(o.t, s0);
+    uint32_t ms = (o.code >> 16) ^ (s0 ? 0xffffu : 0u);
+    if (o.code & kTrNeg) ms ^= 0xffffu;
+    o.ms = ms;
+    return o;
+}
+
+// applies the rotations [rb, rb + nr) of a sub-group to the thread's 16 registers.  Software
+// pipelined: rotation q + 1 is loaded and decoded (its sign, coefficient and case) before rotation
+// q's pair updates, so the dispatch chain of q + 1 overlaps q's arithmetic.  SPEC = 0: generic
+// (one switch on dx, the per-pair signs from M at run time); SPEC = 1: unit-dx CFORM rotations
+// through the compile-time cases.
 template <typename T, int SPEC, int PARAM = 0>
 __device__ __forceinline__ void sub_apply(T (&vr)[kSubAmps], T (&vi)[kSubAmps], const DevTRot* __restrict__ trots,
                                           int rb, int nr, uint32_t r, uint64_t i0) {
     if (nr <= 0) return;
     const DevTRot* tr = trots + rb;
-    uint4 h = ldr<PARAM>(reinterpret_cast<const uint4*>(tr));
-    double pn = ldr<PARAM>(&tr->p);
+    RotPrep<T> cur = prep_rot<T, PARAM>(tr, r, i0);
+    T tb[kSubAmps];  // ping-pong buffer of the unit cases (see cform_sub)
+#pragma unroll
+    for (int d = 0; d < kSubAmps; ++d) tb[d] = T(0);
+    int pp = 0;  // 1: the previous rotation left its i-members in tb (this one has the same dx)
     for (int q = 0; q < nr; ++q) {
-        const uint32_t code = h.x, zr = h.y;
-        const uint64_t zt_c = ((uint64_t)h.w << 32) | h.z;
-        const double pc = pn;
-        if (q + 1 < nr) {
-            const DevTRot* tn = trots + rb + q + 1;
-            h = ldr<PARAM>(reinterpret_cast<const uint4*>(tn));
-            pn = ldr<PARAM>(&tn->p);
-        }
-        const int s0 = par32(zr & r) ^ par64(zt_c & i0);
+        RotPrep<T> nxt = cur;
+        if (q + 1 < nr) nxt = prep_rot<T, PARAM>(tr + q + 1, r, i0);
+        const uint32_t code = cur.code;
         if (SPEC && (code & kTrUnit)) {
             // the thread-wide sign flips t once; the per-pair signs are static
-            unit_dispatch<T>(vr, vi, code & 0x7fu, flip((T)pc, s0));
+#ifdef PS_PINGPONG
+            if (pp) {
+                unit_dispatch<2, T>(vr, vi, tb, code & 0x7fu, cur.tf);
+                pp = 0;
+            } else if (q + 1 < nr && (nxt.code & kTrUnit) && ((nxt.code ^ code) & 0xf00u) == 0) {
+                unit_dispatch<1, T>(vr, vi, tb, code & 0x7fu, cur.tf);
+                pp = 1;
+            } else
+#endif
+                unit_dispatch<0, T>(vr, vi, tb, code & 0x7fu, cur.tf);
         } else {
-            uint32_t Ms = (code >> 16) ^ (s0 ? 0xffffu : 0u);
-            if (code & kTrNeg) Ms ^= 0xffffu;
             const uint32_t dx = (code >> 8) & 15u;
             switch (((code & kTrReal) ? 1u : 0u) | ((code & kTrSform) ? 2u : 0u)) {
-            case 0: sub_rotation<0, 0, T>(vr, vi, dx, Ms, (T)pc); break;
-            case 1: sub_rotation<1, 0, T>(vr, vi, dx, Ms, (T)pc); break;
-            case 2: sub_rotation<0, 1, T>(vr, vi, dx, Ms, (T)pc); break;
-            default: sub_rotation<1, 1, T>(vr, vi, dx, Ms, (T)pc); break;
+            case 0: sub_rotation<0, 0, T>(vr, vi, dx, cur.ms, cur.t); break;
+            case 1: sub_rotation<1, 0, T>(vr, vi, dx, cur.ms, cur.t); break;
+            case 2: sub_rotation<0, 1, T>(vr, vi, dx, cur.ms, cur.t); break;
+            default: sub_rotation<1, 1, T>(vr, vi, dx, cur.ms, cur.t); break;
             }
         }
+        cur = nxt;
     }
 }
 
