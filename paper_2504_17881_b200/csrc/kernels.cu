@@ -18,6 +18,7 @@
 // Every kernel applies the SAME per-pair arithmetic (arith.cuh).
 #include <cuda_runtime.h>
 #include <cstdint>
+#include <type_traits>
 
 #include "arith.cuh"
 #include "ps_internal.h"
@@ -392,25 +393,14 @@ __host__ __device__ constexpr int par4(int v) { return (v ^ (v >> 1) ^ (v >> 2) 
 
 // one CFORM rotation with a compile-time pair pattern (dx = DX) and sign pattern parity(DZ & d):
 // four fused multiply-adds per pair, the signs ride on the FMA operands
-// one CFORM rotation with a compile-time pair pattern (dx = DX) and sign pattern parity(DZ & d):
-// four fused multiply-adds per pair, the signs ride on the FMA operands.
-// MODE 0: registers -> registers.  The update of each pair's two-cycles writes one member to a
-// temporary that has to be moved back to its register before the next rotation.
-// MODE 1 ("ping"): the new values of the i-members (pivot bit clear; diagonal: every real part)
-// go to tb[] and stay there; MODE 2 ("pong"): the next rotation, with the SAME dx, reads them from
-// tb[] and writes every value back to its register.  A run of same-dx rotations (a same-x run
-// of a Trotter step, consecutive ZZ terms) then needs no register moves.  Same operations, same
-// order: bitwise identical to MODE 0.
-template <int REAL, int DX, int DZ, int MODE, typename T>
-__device__ __forceinline__ void cform_sub(T (&vr)[kSubAmps], T (&vi)[kSubAmps], T (&tb)[kSubAmps], T t) {
+template <int REAL, int DX, int DZ, typename T>
+__device__ __forceinline__ void cform_sub(T (&vr)[kSubAmps], T (&vi)[kSubAmps], T t) {
     if constexpr (DX == 0) {
 #pragma unroll
         for (int d = 0; d < kSubAmps; ++d) {
             const T b = par4(DZ & d) ? -t : t;
-            const T re = MODE == 2 ? tb[d] : vr[d];
-            const T nr = pfma(-b, vi[d], re), ni = pfma(b, re, vi[d]);
-            if (MODE == 1) tb[d] = nr;
-            else vr[d] = nr;
+            const T nr = pfma(-b, vi[d], vr[d]), ni = pfma(b, vr[d], vi[d]);
+            vr[d] = nr;
             vi[d] = ni;
         }
     } else if constexpr (DX < kSubAmps) {
@@ -419,40 +409,29 @@ __device__ __forceinline__ void cform_sub(T (&vr)[kSubAmps], T (&vi)[kSubAmps], 
         for (int d = 0; d < kSubAmps; ++d) {
             if ((d >> piv) & 1) continue;
             const int e = d ^ DX;
-            const int k = (d & ((1 << piv) - 1)) | ((d >> (piv + 1)) << piv);  // i-member index
             const T b = par4(DZ & d) ? -t : t;
-            const T ir = MODE == 2 ? tb[2 * k] : vr[d], ii = MODE == 2 ? tb[2 * k + 1] : vi[d];
-            T nir, nii, njr, nji;
             if (REAL) {
-                nir = pfma(-b, vr[e], ir); nii = pfma(-b, vi[e], ii);
-                njr = pfma(b, ir, vr[e]); nji = pfma(b, ii, vi[e]);
+                const T nir = pfma(-b, vr[e], vr[d]), nii = pfma(-b, vi[e], vi[d]);
+                const T njr = pfma(b, vr[d], vr[e]), nji = pfma(b, vi[d], vi[e]);
+                vr[d] = nir; vi[d] = nii; vr[e] = njr; vi[e] = nji;
             } else {
-                nir = pfma(-b, vi[e], ir); nii = pfma(b, vr[e], ii);
-                njr = pfma(-b, ii, vr[e]); nji = pfma(b, ir, vi[e]);
+                const T nir = pfma(-b, vi[e], vr[d]), nii = pfma(b, vr[e], vi[d]);
+                const T njr = pfma(-b, vi[d], vr[e]), nji = pfma(b, vr[d], vi[e]);
+                vr[d] = nir; vi[d] = nii; vr[e] = njr; vi[e] = nji;
             }
-            if (MODE == 1) {
-                tb[2 * k] = nir;
-                tb[2 * k + 1] = nii;
-            } else {
-                vr[d] = nir;
-                vi[d] = nii;
-            }
-            vr[e] = njr;
-            vi[e] = nji;
         }
     }
 }
 
 // unit cases (ps_internal.h tu_case): diagonal by its 4-bit Dz, unit dx by (real, log2 dx, the three
 // Dz bits other than the pivot's); signs and the pair pattern are compile-time
-#define PS_UD(Z) case Z: cform_sub<0, 0, Z, MODE, T>(vr, vi, tb, t); break;
-#define PS_UC(R, XI, Z3) case tu_case(R, XI, tu_dz(XI, Z3)): cform_sub<R, (1 << XI), tu_dz(XI, Z3), MODE, T>(vr, vi, tb, t); break;
+#define PS_UD(Z) case Z: cform_sub<0, 0, Z, T>(vr, vi, t); break;
+#define PS_UC(R, XI, Z3) case tu_case(R, XI, tu_dz(XI, Z3)): cform_sub<R, (1 << XI), tu_dz(XI, Z3), T>(vr, vi, t); break;
 #define PS_UC8(R, XI) PS_UC(R, XI, 0) PS_UC(R, XI, 1) PS_UC(R, XI, 2) PS_UC(R, XI, 3) PS_UC(R, XI, 4) \
     PS_UC(R, XI, 5) PS_UC(R, XI, 6) PS_UC(R, XI, 7)
 
-template <int MODE, typename T>
-__device__ __forceinline__ void unit_dispatch(T (&vr)[kSubAmps], T (&vi)[kSubAmps], T (&tb)[kSubAmps], uint32_t ucase,
-                                              T t) {
+template <typename T>
+__device__ __forceinline__ void unit_dispatch(T (&vr)[kSubAmps], T (&vi)[kSubAmps], uint32_t ucase, T t) {
     switch (ucase) {
         PS_UD(0) PS_UD(1) PS_UD(2) PS_UD(3) PS_UD(4) PS_UD(5) PS_UD(6) PS_UD(7)
         PS_UD(8) PS_UD(9) PS_UD(10) PS_UD(11) PS_UD(12) PS_UD(13) PS_UD(14) PS_UD(15)
@@ -468,72 +447,42 @@ __device__ __forceinline__ void unit_dispatch(T (&vr)[kSubAmps], T (&vi)[kSubAmp
 // applies the rotations [rb, rb + nr) of a sub-group to the thread's 16 registers; the next
 // record is fetched while the current one is applied.  SPEC = 0: generic (one switch on dx, the
 // per-pair signs from M at run time); SPEC = 1: CFORM rotations through the specialised cases.
-// one rotation record decoded for the thread: the code, the coefficient with the thread-wide sign
-// s0 = parity(zr & r) xor parity(zt & i0) folded in (specialised unit cases), and the per-pair
-// sign mask (generic cases)
-template <typename T>
-struct RotPrep {
-    uint32_t code, ms;
-    T t, tf;
-};
-
-template <typename T, int PARAM>
-__device__ __forceinline__ RotPrep<T> prep_rot(const DevTRot* __restrict__ tr, uint32_t r, uint64_t i0) {
-    const uint4 h = ldr<PARAM>(reinterpret_cast<const uint4*>(tr));
-    const double pc = ldr<PARAM>(&tr->p);
-    RotPrep<T> o;
-    o.code = h.x;
-    const uint64_t zt = ((uint64_t)h.w << 32) | h.z;
-    const int s0 = par32(h.y & r) ^ par64(zt & i0);
-    o.t = (T)pc;
-    o.tf = flip(o.t, s0);
-    uint32_t ms = (o.code >> 16) ^ (s0 ? 0xffffu : 0u);
-    if (o.code & kTrNeg) ms ^= 0xffffu;
-    o.ms = ms;
-    return o;
-}
-
-// applies the rotations [rb, rb + nr) of a sub-group to the thread's 16 registers.  Software
-// pipelined: rotation q + 1 is loaded and decoded (its sign, coefficient and case) before rotation
-// q's pair updates, so the dispatch chain of q + 1 overlaps q's arithmetic.  SPEC = 0: generic
-// (one switch on dx, the per-pair signs from M at run time); SPEC = 1: unit-dx CFORM rotations
-// through the compile-time cases.
+// applies the rotations [rb, rb + nr) of a sub-group to the thread's 16 registers; the next
+// record is fetched while the current one is applied.  SPEC = 0: generic (one switch on dx, the
+// per-pair signs from M at run time); SPEC = 1: unit-dx CFORM rotations through the compile-time
+// cases.  (Decoding rotation q + 1 -- sign, coefficient, case -- before rotation q's updates was
+// measured 3-10 % slower: profiles/r02/kernel_ab.md section 5.)
 template <typename T, int SPEC, int PARAM = 0>
 __device__ __forceinline__ void sub_apply(T (&vr)[kSubAmps], T (&vi)[kSubAmps], const DevTRot* __restrict__ trots,
                                           int rb, int nr, uint32_t r, uint64_t i0) {
     if (nr <= 0) return;
     const DevTRot* tr = trots + rb;
-    RotPrep<T> cur = prep_rot<T, PARAM>(tr, r, i0);
-    T tb[kSubAmps];  // ping-pong buffer of the unit cases (see cform_sub)
-#pragma unroll
-    for (int d = 0; d < kSubAmps; ++d) tb[d] = T(0);
-    int pp = 0;  // 1: the previous rotation left its i-members in tb (this one has the same dx)
+    uint4 h = ldr<PARAM>(reinterpret_cast<const uint4*>(tr));
+    double pn = ldr<PARAM>(&tr->p);
     for (int q = 0; q < nr; ++q) {
-        RotPrep<T> nxt = cur;
-        if (q + 1 < nr) nxt = prep_rot<T, PARAM>(tr + q + 1, r, i0);
-        const uint32_t code = cur.code;
+        const uint32_t code = h.x, zr = h.y;
+        const uint64_t zt_c = ((uint64_t)h.w << 32) | h.z;
+        const double pc = pn;
+        if (q + 1 < nr) {
+            const DevTRot* tn = trots + rb + q + 1;
+            h = ldr<PARAM>(reinterpret_cast<const uint4*>(tn));
+            pn = ldr<PARAM>(&tn->p);
+        }
+        const int s0 = par32(zr & r) ^ par64(zt_c & i0);
         if (SPEC && (code & kTrUnit)) {
             // the thread-wide sign flips t once; the per-pair signs are static
-#ifdef PS_PINGPONG
-            if (pp) {
-                unit_dispatch<2, T>(vr, vi, tb, code & 0x7fu, cur.tf);
-                pp = 0;
-            } else if (q + 1 < nr && (nxt.code & kTrUnit) && ((nxt.code ^ code) & 0xf00u) == 0) {
-                unit_dispatch<1, T>(vr, vi, tb, code & 0x7fu, cur.tf);
-                pp = 1;
-            } else
-#endif
-                unit_dispatch<0, T>(vr, vi, tb, code & 0x7fu, cur.tf);
+            unit_dispatch<T>(vr, vi, code & 0x7fu, flip((T)pc, s0));
         } else {
+            uint32_t Ms = (code >> 16) ^ (s0 ? 0xffffu : 0u);
+            if (code & kTrNeg) Ms ^= 0xffffu;
             const uint32_t dx = (code >> 8) & 15u;
             switch (((code & kTrReal) ? 1u : 0u) | ((code & kTrSform) ? 2u : 0u)) {
-            case 0: sub_rotation<0, 0, T>(vr, vi, dx, cur.ms, cur.t); break;
-            case 1: sub_rotation<1, 0, T>(vr, vi, dx, cur.ms, cur.t); break;
-            case 2: sub_rotation<0, 1, T>(vr, vi, dx, cur.ms, cur.t); break;
-            default: sub_rotation<1, 1, T>(vr, vi, dx, cur.ms, cur.t); break;
+            case 0: sub_rotation<0, 0, T>(vr, vi, dx, Ms, (T)pc); break;
+            case 1: sub_rotation<1, 0, T>(vr, vi, dx, Ms, (T)pc); break;
+            case 2: sub_rotation<0, 1, T>(vr, vi, dx, Ms, (T)pc); break;
+            default: sub_rotation<1, 1, T>(vr, vi, dx, Ms, (T)pc); break;
             }
         }
-        cur = nxt;
     }
 }
 
@@ -595,12 +544,15 @@ __device__ __forceinline__ uint32_t sub_local(const SubHdr& h, int d) {
 // disjoint), so gi[d] = gi[d without its lowest bit] xor Lin(u_lowest): one 64-bit xor each
 __host__ __device__ constexpr int lowbit_index(int d) { return (d & 1) ? 0 : (d & 2) ? 1 : (d & 4) ? 2 : 3; }
 
-__device__ __forceinline__ void elem_index(uint64_t (&gi)[kSubAmps], const SubHdr& h, uint64_t i0,
+// IDX = uint32_t when every local index fits 32 bits (n_local <= 32): one 32-bit xor per element
+// and one wide multiply-add for the address instead of two 64-bit ops each
+template <typename IDX = uint64_t>
+__device__ __forceinline__ void elem_index(IDX (&gi)[kSubAmps], const SubHdr& h, uint64_t i0,
                                            const uint64_t* soff, int cbits, uint32_t cmask) {
-    uint64_t E[kSubDim];
+    IDX E[kSubDim];
 #pragma unroll
-    for (int b = 0; b < kSubDim; ++b) E[b] = soff[h.u[b] >> cbits] ^ (uint64_t)(h.u[b] & cmask);
-    gi[0] = i0 ^ soff[h.r >> cbits] ^ (uint64_t)(h.r & cmask);
+    for (int b = 0; b < kSubDim; ++b) E[b] = (IDX)soff[h.u[b] >> cbits] ^ (IDX)(h.u[b] & cmask);
+    gi[0] = (IDX)i0 ^ (IDX)soff[h.r >> cbits] ^ (IDX)(h.r & cmask);
 #pragma unroll
     for (int d = 1; d < kSubAmps; ++d) gi[d] = gi[d & (d - 1)] ^ E[lowbit_index(d)];
 }
@@ -726,7 +678,7 @@ __device__ __forceinline__ void smem_offsets(uint32_t (&o)[kSubAmps], const SubH
     for (int d = 1; d < kSubAmps; ++d) o[d] = o[d & (d - 1)] ^ (h.u[lowbit_index(d)] << LB);
 }
 
-template <typename T, int SPEC, int PARAM>
+template <typename T, int SPEC, int PARAM, typename IDX = uint64_t>
 __device__ __forceinline__ void coset_body(T* __restrict__ a, int kbits, int cbits, const BitRuns& runs,
                                            const uint64_t* __restrict__ offs, uint64_t ntiles,
                                            const DevSub* __restrict__ subs, int nsub, const DevTRot* __restrict__ trots,
@@ -763,8 +715,8 @@ __device__ __forceinline__ void coset_body(T* __restrict__ a, int kbits, int cbi
     auto prefetch_tile = [&](uint64_t i1) {
         SubHdr h0 = load_sub_hdr<PARAM>(subs);
         h0.r = rep(0);
-        uint64_t gi[kSubAmps];
-        elem_index(gi, h0, i1, soff, cbits, cmask);
+        IDX gi[kSubAmps];
+        elem_index<IDX>(gi, h0, i1, soff, cbits, cmask);
 #pragma unroll
         for (int d = 0; d < kSubAmps; ++d) cp_async_amp(&tile[d * nthr + tid], &g[gi[d]]);
         asm volatile("cp.async.commit_group;" ::: "memory");
@@ -786,8 +738,8 @@ __device__ __forceinline__ void coset_body(T* __restrict__ a, int kbits, int cbi
                     vi[d] = v.y;
                 }
             } else if (s == 0) {
-                uint64_t gi[kSubAmps];
-                elem_index(gi, h, i0, soff, cbits, cmask);
+                IDX gi[kSubAmps];
+                elem_index<IDX>(gi, h, i0, soff, cbits, cmask);
                 V2 v[kSubAmps];
                 if (l2_prefetch & 4) {
 #pragma unroll
@@ -821,8 +773,8 @@ __device__ __forceinline__ void coset_body(T* __restrict__ a, int kbits, int cbi
             sub_apply<T, SPEC, PARAM>(vr, vi, trots, h.rb, h.nr, h.r, i0);
             if (h.F != 1.0) sub_scale<T>(vr, vi, (T)h.F);
             if (s == nsub - 1) {
-                uint64_t gi[kSubAmps];
-                elem_index(gi, h, i0, soff, cbits, cmask);
+                IDX gi[kSubAmps];
+                elem_index<IDX>(gi, h, i0, soff, cbits, cmask);
 #pragma unroll
                 for (int d = 0; d < kSubAmps; ++d) {
                     V2 v;
@@ -864,13 +816,14 @@ struct PassRecs {
     DevTRot trots[kParamRots];
 };
 
-template <typename T, int MAXT, int MINB, int SPEC = 0>
+template <typename T, int MAXT, int MINB, int SPEC = 0, int NARROW = 0>
 __global__ void __launch_bounds__(MAXT, MINB)
     k_coset_p(T* __restrict__ a, int kbits, int cbits, const __grid_constant__ BitRuns runs,
               const uint64_t* __restrict__ offs, uint64_t ntiles, int nsub, int l2_prefetch, uint64_t or_mask,
               uint64_t free_mask, const __grid_constant__ PassRecs recs) {
-    coset_body<T, SPEC, 1>(a, kbits, cbits, runs, offs, ntiles, recs.subs, nsub, recs.trots, l2_prefetch, or_mask,
-                           free_mask);
+    using IDX = typename std::conditional<NARROW != 0, uint32_t, uint64_t>::type;
+    coset_body<T, SPEC, 1, IDX>(a, kbits, cbits, runs, offs, ntiles, recs.subs, nsub, recs.trots, l2_prefetch,
+                                or_mask, free_mask);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -906,7 +859,7 @@ __device__ __forceinline__ uint32_t flag_acquire(const uint32_t* p) {
 }
 
 template <typename T, int SPEC>
-__global__ void __launch_bounds__(kCosetThreads, 1) k_xtile(const __grid_constant__ XTileParams P) {
+__global__ void __launch_bounds__(kCosetThreads, 2) k_xtile(const __grid_constant__ XTileParams P) {
     using V2 = typename SmemAmp<T>::V;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int rk = blockIdx.x / P.ctas_per_rank;
@@ -1624,10 +1577,10 @@ cudaError_t launch_coset_t(T* a, int nl, const Pass& p, const DevSub* d_subs, co
     if (threads <= 128 && !p.spec && occ_sel == 3)
         return launch_coset_k<T, 128, 8, 0>(a, nl, p, d_subs, d_trots, d_offs, l2_prefetch, grid_mult, s);
     // tiles of 2^13 (fp64) / 2^13..2^14 (fp32) amplitudes: one CTA of 512 / 1024 threads per SM
-    if (threads == 512 && !p.spec)
+    if (threads == 512)
         return launch_coset_k<T, 512, 1, 0>(a, nl, p, d_subs, d_trots, d_offs, l2_prefetch, grid_mult, s);
     if constexpr (sizeof(T) == 4)
-        if (threads == 1024 && !p.spec)
+        if (threads == 1024)
             return launch_coset_k<T, 1024, 1, 0>(a, nl, p, d_subs, d_trots, d_offs, l2_prefetch, grid_mult, s);
     if (threads > kCosetThreads) return cudaErrorInvalidValue;
 #ifndef PS_ONLY_DEFAULT  // (development builds: the default kernels only, fast to compile)
@@ -1637,39 +1590,39 @@ cudaError_t launch_coset_t(T* a, int nl, const Pass& p, const DevSub* d_subs, co
 #ifndef PS_COSET_MINB
 #define PS_COSET_MINB 2
 #endif
-    if (p.spec)
+    if (p.spec && threads <= kCosetThreads)
         return launch_coset_k<T, kCosetThreads, PS_COSET_MINB, 1>(a, nl, p, d_subs, d_trots, d_offs, l2_prefetch, grid_mult, s);
     return launch_coset_k<T, kCosetThreads, PS_COSET_MINB, 0>(a, nl, p, d_subs, d_trots, d_offs, l2_prefetch, grid_mult, s);
 }
 
 // the pass's records in the launch's parameter block (tune bit 10; passes of <= kParamRots
 // rotations); cudaErrorNotSupported when the pass does not fit
-template <typename T, int MAXT, int MINB, int SPEC = 0>
+template <typename T, int MAXT, int MINB, int SPEC = 0, int NARROW = 0>
 cudaError_t launch_coset_param_k(T* a, const Pass& p, const PassRecs& recs, const uint64_t* d_offs, int l2_prefetch,
                                  int grid_mult, cudaStream_t s) {
     const size_t smem = coset_smem_bytes(p.kbits, p.cbits, 2 * sizeof(T));
     static uint64_t attr_devices = 0;
     const int dev = current_device();
     if (!((attr_devices >> dev) & 1)) {
-        cudaFuncSetAttribute(k_coset_p<T, MAXT, MINB, SPEC>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        cudaFuncSetAttribute(k_coset_p<T, MAXT, MINB, SPEC, NARROW>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         attr_devices |= 1ull << dev;
     }
     const int threads = 1 << (p.kbits - kSubDim);
     if (threads > MAXT) return cudaErrorNotSupported;
     int occ = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_coset_p<T, MAXT, MINB, SPEC>, threads, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_coset_p<T, MAXT, MINB, SPEC, NARROW>, threads, smem);
     if (occ < 1) occ = 1;
     const uint64_t ntiles = 1ull << __builtin_popcountll(p.free_mask);
     const uint64_t cap = apply_grid_cap((uint64_t)num_sms() * (uint64_t)occ * (uint64_t)(grid_mult > 0 ? grid_mult : 1));
     const unsigned grid = (unsigned)(ntiles < cap ? ntiles : cap);
-    k_coset_p<T, MAXT, MINB, SPEC><<<grid, threads, smem, s>>>(a, p.kbits, p.cbits, make_runs(p.free_mask), d_offs + p.off_begin,
+    k_coset_p<T, MAXT, MINB, SPEC, NARROW><<<grid, threads, smem, s>>>(a, p.kbits, p.cbits, make_runs(p.free_mask), d_offs + p.off_begin,
                                                           ntiles, p.sub_count, l2_prefetch, p.or_mask, p.free_mask,
                                                           recs);
     return cudaGetLastError();
 }
 
 template <typename T>
-cudaError_t launch_coset_param(T* a, const Pass& p, const DevSub* h_subs, const DevTRot* h_trots,
+cudaError_t launch_coset_param(T* a, int nl, const Pass& p, const DevSub* h_subs, const DevTRot* h_trots,
                                const uint64_t* d_offs, int l2_prefetch, int grid_mult, int occ_sel, cudaStream_t s) {
     if (p.sub_count < 1 || p.sub_count > kParamSubs) return cudaErrorNotSupported;
     const int base = h_subs[p.sub_begin].rot_begin;
@@ -1683,23 +1636,36 @@ cudaError_t launch_coset_param(T* a, const Pass& p, const DevSub* h_subs, const 
     }
     for (int q = 0; q < nrot; ++q) recs.trots[q] = h_trots[base + q];
     const int threads = 1 << (p.kbits - kSubDim);
-    if (p.spec) {
+    // the default kernels with 32-bit element indices when every local index fits (n_local <= 32)
+#ifdef PS_NO_NARROW
+    const bool narrow = false;
+#else
+    const bool narrow = nl <= 32;
+#endif
+    if (p.spec && threads <= kCosetThreads) {
         if constexpr (sizeof(T) == 4) {
             if (occ_sel == 0 && threads <= 128)
-                return launch_coset_param_k<T, 128, 8, 1>(a, p, recs, d_offs, l2_prefetch, grid_mult, s);
+                return narrow ? launch_coset_param_k<T, 128, 8, 1, 1>(a, p, recs, d_offs, l2_prefetch, grid_mult, s)
+                              : launch_coset_param_k<T, 128, 8, 1>(a, p, recs, d_offs, l2_prefetch, grid_mult, s);
             if (occ_sel == 2 && threads <= 128)  // 6 CTAs per SM (85 registers): room for the 80 cases
                 return launch_coset_param_k<T, 128, 6, 1>(a, p, recs, d_offs, l2_prefetch, grid_mult, s);
         }
         if (threads <= kCosetThreads)
-            return launch_coset_param_k<T, kCosetThreads, PS_COSET_MINB, 1>(a, p, recs, d_offs, l2_prefetch, grid_mult, s);
+            return narrow ? launch_coset_param_k<T, kCosetThreads, PS_COSET_MINB, 1, 1>(a, p, recs, d_offs, l2_prefetch,
+                                                                                      grid_mult, s)
+                          : launch_coset_param_k<T, kCosetThreads, PS_COSET_MINB, 1>(a, p, recs, d_offs, l2_prefetch,
+                                                                                   grid_mult, s);
         return cudaErrorNotSupported;
     }
     if constexpr (sizeof(T) == 4)
-        if (occ_sel == 0 && threads <= 128) return launch_coset_param_k<T, 128, 8>(a, p, recs, d_offs, l2_prefetch, grid_mult, s);
+        if (occ_sel == 0 && threads <= 128)
+            return narrow ? launch_coset_param_k<T, 128, 8, 0, 1>(a, p, recs, d_offs, l2_prefetch, grid_mult, s)
+                          : launch_coset_param_k<T, 128, 8>(a, p, recs, d_offs, l2_prefetch, grid_mult, s);
     if (threads == 512) return launch_coset_param_k<T, 512, 1>(a, p, recs, d_offs, l2_prefetch, grid_mult, s);
     if constexpr (sizeof(T) == 4)
         if (threads == 1024) return launch_coset_param_k<T, 1024, 1>(a, p, recs, d_offs, l2_prefetch, grid_mult, s);
-    return launch_coset_param_k<T, kCosetThreads, PS_COSET_MINB>(a, p, recs, d_offs, l2_prefetch, grid_mult, s);
+    return narrow ? launch_coset_param_k<T, kCosetThreads, PS_COSET_MINB, 0, 1>(a, p, recs, d_offs, l2_prefetch, grid_mult, s)
+                  : launch_coset_param_k<T, kCosetThreads, PS_COSET_MINB>(a, p, recs, d_offs, l2_prefetch, grid_mult, s);
 }
 
 template <typename T, int CPASYNC>
@@ -1842,8 +1808,8 @@ cudaError_t launch_tile(int dtype, void* a, int nl, const Pass& p, const DevSub*
     const int gm = ((tune >> 4) & 15) ? ((tune >> 4) & 15) : 4;
     if (use_tma == 2 && (tune & 1024) && h_subs) {
         cudaError_t e = dtype == PS_C128
-                            ? launch_coset_param<double>((double*)a, p, h_subs, h_trots, d_offs, l2p, gm, occ_sel, s)
-                            : launch_coset_param<float>((float*)a, p, h_subs, h_trots, d_offs, l2p, gm, occ_sel, s);
+                            ? launch_coset_param<double>((double*)a, nl, p, h_subs, h_trots, d_offs, l2p, gm, occ_sel, s)
+                            : launch_coset_param<float>((float*)a, nl, p, h_subs, h_trots, d_offs, l2p, gm, occ_sel, s);
         if (e != cudaErrorNotSupported) return e;
     }
     if (use_tma == 2) {

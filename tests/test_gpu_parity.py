@@ -133,9 +133,13 @@ def test_fusion_levels_agree(dtype, kind):
     ref = outs[(0, None, 2)]
     if kind in ("S8",):
         assert np.array_equal(outs[(1, None, 2)].view(np.uint8), ref.view(np.uint8))
-    tol = 1e-12 if dtype == "c128" else 2e-4
+    # every fusion level / tile variant within the north_star tolerance of the oracle (so any two
+    # within twice that), and fp64 variants within 1e-12 of each other (R9: rounding order only)
+    want = oracle.apply(n, oracle.random_state(SEED, n), codes, ang)
     for key, o in outs.items():
-        assert np.max(np.abs(o - ref)) <= tol, key
+        assert np.max(np.abs(o - want)) <= TOL[dtype], key
+        if dtype == "c128":
+            assert np.max(np.abs(o - ref)) <= 1e-12, key
 
 
 @pytest.mark.parametrize("dtype", ["c128", "c64"])

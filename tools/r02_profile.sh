@@ -30,7 +30,7 @@ summ stream 34359738368 "30q fp64 K1 k_stream (fusion 0), 21st launch"
 summ reduce 0 "30q fp64 reductions: k_norm / k_inner / k_expect (algorithmic bytes: norm 16 GiB read, inner 32 GiB, expect 16 GiB per x-group)"
 summ swap 0 "30q fp64 on 2 virtual ranks: k_p2p_swap / k_xtile / k_permute (peer = the other slice on the same GPU)"
 echo "ncu probes done"
-timeout 1200 python tools/z0_curve.py --qubits 30 --embedded --terms 20000 --ldet 1500 --out $D/z0_30_embedded.json > $D/z0_30e.log 2>&1; echo "z0e rc=$?"
+timeout 1200 python tools/z0_curve.py --qubits 30 --embedded --terms 4000 --ldet 600 --out $D/z0_30_embedded.json > $D/z0_30e.log 2>&1; echo "z0e rc=$?"
 timeout 1800 python tools/z0_curve.py --qubits 32 --terms 60000 --ldet 4000 --out $D/z0_32.json > $D/z0_32.log 2>&1; echo "z0 rc=$?"
 # fp32 with the specialised cases at 6 CTAs per SM (occupancy select 2 = tune bits 1-3 -> 4)
 for t in 1536 1540; do timeout 300 python bench.py --dtype c64 --specialize 2 --tile-tune $t --no-e2e --no-cpu > $D/c64_sp2_t$t.log 2>&1; done
