@@ -1636,11 +1636,13 @@ cudaError_t launch_coset_param(T* a, int nl, const Pass& p, const DevSub* h_subs
     }
     for (int q = 0; q < nrot; ++q) recs.trots[q] = h_trots[base + q];
     const int threads = 1 << (p.kbits - kSubDim);
-    // the default kernels with 32-bit element indices when every local index fits (n_local <= 32)
+    // fp32: the default kernels with 32-bit element indices when every local index fits (n_local <=
+    // 32): +0.8 %; fp64 keeps 64-bit indices (the 32-bit build takes 128 registers: -1 % R10, -2 % JW;
+    // profiles/r02/kernel_ab.md section 6)
 #ifdef PS_NO_NARROW
     const bool narrow = false;
 #else
-    const bool narrow = nl <= 32;
+    const bool narrow = sizeof(T) == 4 && nl <= 32;
 #endif
     if (p.spec && threads <= kCosetThreads) {
         if constexpr (sizeof(T) == 4) {
@@ -1650,11 +1652,13 @@ cudaError_t launch_coset_param(T* a, int nl, const Pass& p, const DevSub* h_subs
             if (occ_sel == 2 && threads <= 128)  // 6 CTAs per SM (85 registers): room for the 80 cases
                 return launch_coset_param_k<T, 128, 6, 1>(a, p, recs, d_offs, l2_prefetch, grid_mult, s);
         }
-        if (threads <= kCosetThreads)
-            return narrow ? launch_coset_param_k<T, kCosetThreads, PS_COSET_MINB, 1, 1>(a, p, recs, d_offs, l2_prefetch,
-                                                                                      grid_mult, s)
-                          : launch_coset_param_k<T, kCosetThreads, PS_COSET_MINB, 1>(a, p, recs, d_offs, l2_prefetch,
-                                                                                   grid_mult, s);
+        if (threads <= kCosetThreads) {
+            if constexpr (sizeof(T) == 4)
+                if (narrow)
+                    return launch_coset_param_k<T, kCosetThreads, PS_COSET_MINB, 1, 1>(a, p, recs, d_offs, l2_prefetch,
+                                                                                      grid_mult, s);
+            return launch_coset_param_k<T, kCosetThreads, PS_COSET_MINB, 1>(a, p, recs, d_offs, l2_prefetch, grid_mult, s);
+        }
         return cudaErrorNotSupported;
     }
     if constexpr (sizeof(T) == 4)
@@ -1664,8 +1668,9 @@ cudaError_t launch_coset_param(T* a, int nl, const Pass& p, const DevSub* h_subs
     if (threads == 512) return launch_coset_param_k<T, 512, 1>(a, p, recs, d_offs, l2_prefetch, grid_mult, s);
     if constexpr (sizeof(T) == 4)
         if (threads == 1024) return launch_coset_param_k<T, 1024, 1>(a, p, recs, d_offs, l2_prefetch, grid_mult, s);
-    return narrow ? launch_coset_param_k<T, kCosetThreads, PS_COSET_MINB, 0, 1>(a, p, recs, d_offs, l2_prefetch, grid_mult, s)
-                  : launch_coset_param_k<T, kCosetThreads, PS_COSET_MINB>(a, p, recs, d_offs, l2_prefetch, grid_mult, s);
+    if constexpr (sizeof(T) == 4)
+        if (narrow) return launch_coset_param_k<T, kCosetThreads, PS_COSET_MINB, 0, 1>(a, p, recs, d_offs, l2_prefetch, grid_mult, s);
+    return launch_coset_param_k<T, kCosetThreads, PS_COSET_MINB>(a, p, recs, d_offs, l2_prefetch, grid_mult, s);
 }
 
 template <typename T, int CPASYNC>
