@@ -13,10 +13,11 @@ run R10_30_fused0_ovl0 --fused 0 --overlap 0
 run R10_30_layout0 --layout 0
 nw=$((30 + $(python -c "print(($N).bit_length()-1)")))
 run R10_${nw}_weak --qubits $nw
-for L in ${LS:-1 10 100}; do
+for L in ${LS-1 10 100}; do
   for lay in 0 1 2; do
     run SUFFIX_L${L}_layout${lay} --kind SUFFIX --group $L --layout $lay --layer 1000 --qubits 30
   done
   run SUFFIX_L${L}_layout1_fused0 --kind SUFFIX --group $L --layout 1 --fused 0 --layer 1000 --qubits 30
 done
-run JW_32 --kind JW --qubits 32 --specialize 2
+run JW_32 --kind JW --qubits 32
+run JW_32_fused0 --kind JW --qubits 32 --fused 0
