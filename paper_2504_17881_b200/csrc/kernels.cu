@@ -669,6 +669,32 @@ __host__ __device__ inline size_t coset_smem_bytes(int kbits, int cbits, size_t 
     return (amp_bytes << kbits) + coset_rep_bytes(kbits, amp_bytes) + coset_off_bytes(kbits - cbits);
 }
 
+// TMA bulk copy of one contiguous chunk HBM -> shared memory, completing on an mbarrier (tx bytes)
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            (uint32_t)__cvta_generic_to_shared(dst)),
+        "l"(src), "r"(bytes), "r"((uint32_t)__cvta_generic_to_shared(bar))
+        : "memory");
+}
+__device__ __forceinline__ void mbar_expect(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"((uint32_t)__cvta_generic_to_shared(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait_phase(uint64_t* bar, uint32_t parity) {
+    uint32_t done = 0;
+    while (!done) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done)
+            : "r"((uint32_t)__cvta_generic_to_shared(bar)), "r"(parity)
+            : "memory");
+    }
+}
+
 // shared-memory byte offsets of the thread's 16 elements l_d = r xor U(d): o_d = o_(d without its
 // lowest bit) xor (u_lowest << log2 amp bytes) -- one xor each (the tile sits at offset 0)
 template <int LB>
@@ -678,11 +704,32 @@ __device__ __forceinline__ void smem_offsets(uint32_t (&o)[kSubAmps], const SubH
     for (int d = 1; d < kSubAmps; ++d) o[d] = o[d & (d - 1)] ^ (h.u[lowbit_index(d)] << LB);
 }
 
-template <typename T, int SPEC, int PARAM, typename IDX = uint64_t>
+// per-tile handshake flags of the fused exchange (system scope: the partner is another GPU)
+__device__ __forceinline__ void flag_release(uint32_t* p, uint32_t v) {
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t flag_acquire(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// the fused exchange + tile pass (K8, XT = 1): this rank's view of the exchange E(gx, ell)
+struct XtArgs {
+    const void* peer;        // the partner's slice
+    uint32_t* flags;         // raised by the partner: it has read its tile tau of my slots
+    uint32_t* peer_flags;    // raised by me for the partner
+    uint64_t lbit, keepbit;  // 2^ell and keep * 2^ell
+    uint64_t dtau, dtau_dep; // tile-index offset of 2^ell (tau space) and its deposit
+    uint32_t epoch, cta, ncta;
+};
+
+template <typename T, int SPEC, int PARAM, typename IDX = uint64_t, int XT = 0>
 __device__ __forceinline__ void coset_body(T* __restrict__ a, int kbits, int cbits, const BitRuns& runs,
                                            const uint64_t* __restrict__ offs, uint64_t ntiles,
                                            const DevSub* __restrict__ subs, int nsub, const DevTRot* __restrict__ trots,
-                                           int l2_prefetch, uint64_t or_mask, uint64_t free_mask) {
+                                           int l2_prefetch, uint64_t or_mask, uint64_t free_mask,
+                                           const XtArgs& xt = XtArgs{}) {
     using V2 = typename SmemAmp<T>::V;
     constexpr int LB = sizeof(V2) == 16 ? 4 : 3;  // log2 bytes per amplitude
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -704,32 +751,74 @@ __device__ __forceinline__ void coset_body(T* __restrict__ a, int kbits, int cbi
         return sub_rep<PARAM>(subs + s, tid, ncols);
     };
     V2* g = reinterpret_cast<V2*>(a);
+    // XT: the element of new slot j lives in my slot j (bit ell of j == keep) or in the partner's
+    // slot j ^ 2^ell; the rank with keep = 1 walks tile tau ^ dtau (see k_xtile)
+    const V2* gp = reinterpret_cast<const V2*>(xt.peer);
+    auto src = [&](uint64_t gi) -> const V2* {
+        if (XT && (gi & xt.lbit) != xt.keepbit) return gp + (gi ^ xt.lbit);
+        return g + gi;
+    };
+    const uint32_t cta0 = XT ? xt.cta : blockIdx.x, ncta = XT ? xt.ncta : gridDim.x;
+    const uint64_t xorD = XT && xt.keepbit ? xt.dtau_dep : 0, xorT = XT && xt.keepbit ? xt.dtau : 0;
     // tile bases advance in the deposited domain: pdep(tau + G) = ((pdep(tau) | ~M) + pdep(G)) & M
-    const uint64_t dstep = deposit((uint64_t)gridDim.x, runs);
-    uint64_t dtau = deposit((uint64_t)blockIdx.x, runs);
+    const uint64_t dstep = deposit((uint64_t)ncta, runs);
+    uint64_t dtau = deposit((uint64_t)cta0, runs);
     // tune bit 11 (l2_prefetch & 8): sub-group 0 of the CTA's next tile is copied HBM -> shared
     // memory (LDGSTS, one slot per thread and element) as soon as this tile's last sub-group has
     // its inputs in registers, so the next tile's reads are in flight while this one is computed
     // and stored; sub-group 0 then reads its own slots instead of HBM
-    const bool pf = (l2_prefetch & 8) != 0;
+    // tune bit 12 (l2_prefetch & 16): the same prefetch by the TMA engine -- one cp.async.bulk per
+    // contiguous chunk into the tile in tile order, completion on an mbarrier -- instead of 16
+    // LDGSTS per thread; sub-group 0 then reads the tile like every later sub-group
+    const bool bulk = !XT && (l2_prefetch & 16) != 0;  // (a fused chunk may straddle both slices)
+    const bool pf = XT || (l2_prefetch & 8) != 0 || bulk;
+    __shared__ __align__(8) uint64_t tma_bar;
+    uint32_t tma_phase = 0;
+    if (bulk) {
+        if (tid == 0) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"((uint32_t)__cvta_generic_to_shared(&tma_bar)));
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
+        __syncthreads();
+    }
+    const uint32_t chunk_bytes = (uint32_t)sizeof(V2) << cbits;
     auto prefetch_tile = [&](uint64_t i1) {
+        if (bulk) {
+            // every thread's shared-memory reads of the buffer are done (barrier before the call)
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            if (tid == 0) mbar_expect(&tma_bar, chunk_bytes << hbits);
+            for (uint32_t u = tid; u < (1u << hbits); u += nthr)
+                bulk_g2s(smem_raw + (size_t)u * chunk_bytes, &g[i1 ^ soff[u]], chunk_bytes, &tma_bar);
+            return;
+        }
         SubHdr h0 = load_sub_hdr<PARAM>(subs);
         h0.r = rep(0);
         IDX gi[kSubAmps];
         elem_index<IDX>(gi, h0, i1, soff, cbits, cmask);
 #pragma unroll
-        for (int d = 0; d < kSubAmps; ++d) cp_async_amp(&tile[d * nthr + tid], &g[gi[d]]);
+        for (int d = 0; d < kSubAmps; ++d) cp_async_amp(&tile[d * nthr + tid], src(gi[d]));
         asm volatile("cp.async.commit_group;" ::: "memory");
     };
-    if (pf && blockIdx.x < ntiles) prefetch_tile(dtau | or_mask);
-    for (uint64_t tau = blockIdx.x; tau < ntiles;
-         tau += gridDim.x, dtau = ((dtau | ~free_mask) + dstep) & free_mask) {
-        const uint64_t i0 = dtau | or_mask;
+    if (pf && cta0 < ntiles) prefetch_tile((dtau ^ xorD) | or_mask);
+    for (uint64_t tau = cta0; tau < ntiles; tau += ncta, dtau = ((dtau | ~free_mask) + dstep) & free_mask) {
+        const uint64_t i0 = (dtau ^ xorD) | or_mask;
+        const uint64_t tau_x = tau ^ xorT;  // this tile's index (flag slot)
         T vr[kSubAmps], vi[kSubAmps];
         for (int s = 0; s < nsub; ++s) {
             SubHdr h = load_sub_hdr<PARAM>(subs + s);
             h.r = rep(s);
-            if (s == 0 && pf) {
+            if (s == 0 && bulk) {
+                mbar_wait_phase(&tma_bar, tma_phase);
+                tma_phase ^= 1u;
+                uint32_t o[kSubAmps];
+                smem_offsets<LB>(o, h);
+#pragma unroll
+                for (int d = 0; d < kSubAmps; ++d) {
+                    const V2 v = *reinterpret_cast<const V2*>(smem_raw + o[d]);
+                    vr[d] = v.x;
+                    vi[d] = v.y;
+                }
+            } else if (s == 0 && pf) {
                 asm volatile("cp.async.wait_group 0;" ::: "memory");
 #pragma unroll
                 for (int d = 0; d < kSubAmps; ++d) {
@@ -743,10 +832,10 @@ __device__ __forceinline__ void coset_body(T* __restrict__ a, int kbits, int cbi
                 V2 v[kSubAmps];
                 if (l2_prefetch & 4) {
 #pragma unroll
-                    for (int d = 0; d < kSubAmps; ++d) v[d] = ld_l2_256(&g[gi[d]]);
+                    for (int d = 0; d < kSubAmps; ++d) v[d] = ld_l2_256(src(gi[d]));
                 } else {
 #pragma unroll
-                    for (int d = 0; d < kSubAmps; ++d) v[d] = __ldcs(&g[gi[d]]);
+                    for (int d = 0; d < kSubAmps; ++d) v[d] = __ldcs(src(gi[d]));
                 }
 #pragma unroll
                 for (int d = 0; d < kSubAmps; ++d) {
@@ -764,11 +853,25 @@ __device__ __forceinline__ void coset_body(T* __restrict__ a, int kbits, int cbi
                 }
             }
             if (pf && (s == 0 || s == nsub - 1)) {
+                if (XT && s == 0) {
+                    // every thread has its (partly remote) inputs of this tile: the partner may now
+                    // overwrite its slots that this tile read
+                    __syncthreads();
+                    if (tid == 0) flag_release(xt.peer_flags + tau_x, xt.epoch);
+                }
+                if (XT && s == nsub - 1 && tid == 0) {
+                    // before any store of this tile: the partner has read its tile holding my slots
+                    uint32_t spins = 0;
+                    while (flag_acquire(xt.flags + (tau_x ^ xt.dtau)) != xt.epoch) {
+                        __nanosleep(64);
+                        if (++spins > (1u << 28)) __trap();
+                    }
+                }
                 // every thread's shared-memory reads of this sub-group are done before the slots
                 // (s == 0) or the tile (last sub-group) are overwritten
                 __syncthreads();
-                if (s == nsub - 1 && tau + gridDim.x < ntiles)
-                    prefetch_tile((((dtau | ~free_mask) + dstep) & free_mask) | or_mask);
+                if (s == nsub - 1 && tau + ncta < ntiles)
+                    prefetch_tile(((((dtau | ~free_mask) + dstep) & free_mask) ^ xorD) | or_mask);
             }
             sub_apply<T, SPEC, PARAM>(vr, vi, trots, h.rb, h.nr, h.r, i0);
             if (h.F != 1.0) sub_scale<T>(vr, vi, (T)h.F);
@@ -844,106 +947,30 @@ struct XTileParams {
     XTileRank r[kMaxXRanks];
     BitRuns runs;
     const uint64_t* offs;
-    uint64_t ntiles, free_mask, dtau;
+    uint64_t ntiles, free_mask, dtau, dtau_dep;
     int nranks, ctas_per_rank, kbits, cbits, nsub, ell;
     uint32_t epoch;
 };
 
-__device__ __forceinline__ void flag_release(uint32_t* p, uint32_t v) {
-    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-__device__ __forceinline__ uint32_t flag_acquire(const uint32_t* p) {
-    uint32_t v;
-    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
-
 template <typename T, int SPEC>
 __global__ void __launch_bounds__(kCosetThreads, 2) k_xtile(const __grid_constant__ XTileParams P) {
-    using V2 = typename SmemAmp<T>::V;
-    extern __shared__ __align__(128) unsigned char smem_raw[];
     const int rk = blockIdx.x / P.ctas_per_rank;
-    const uint32_t cta = blockIdx.x % P.ctas_per_rank;
     const XTileRank& R = P.r[rk];
-    const int hbits = P.kbits - P.cbits;
-    uint64_t* soff = reinterpret_cast<uint64_t*>(smem_raw);
-    V2* tile = reinterpret_cast<V2*>(smem_raw + coset_off_bytes(hbits));
-    const uint32_t tid = threadIdx.x;
-    const uint32_t cmask = (1u << P.cbits) - 1u;
-    const int ncols = P.kbits - kSubDim;
-    for (uint32_t u = tid; u < (1u << hbits); u += blockDim.x) soff[u] = __ldg(&P.offs[u]);
-    __syncthreads();
-    V2* g = reinterpret_cast<V2*>(R.a);
-    const V2* peer = reinterpret_cast<const V2*>(R.peer);
-    const uint64_t lbit = 1ull << P.ell;
-    const uint64_t keepbit = (uint64_t)R.keep << P.ell;
-    for (uint64_t base = cta; base < P.ntiles; base += P.ctas_per_rank) {
-        const uint64_t tau = R.keep ? (base ^ P.dtau) : base;
-        const uint64_t i0 = deposit(tau, P.runs);
-        T vr[kSubAmps], vi[kSubAmps];
-        for (int s = 0; s < P.nsub; ++s) {
-            const SubHdr h = load_sub<0>(R.subs + s, tid, ncols);
-            if (s == 0) {
-                uint64_t gi[kSubAmps];
-                elem_index(gi, h, i0, soff, P.cbits, cmask);
-                V2 v[kSubAmps];
-#pragma unroll
-                for (int d = 0; d < kSubAmps; ++d)
-                    v[d] = ((gi[d] & lbit) == keepbit) ? __ldcs(&g[gi[d]]) : __ldcg(&peer[gi[d] ^ lbit]);
-#pragma unroll
-                for (int d = 0; d < kSubAmps; ++d) {
-                    vr[d] = v[d].x;
-                    vi[d] = v[d].y;
-                }
-            } else {
-#pragma unroll
-                for (int d = 0; d < kSubAmps; ++d) {
-                    const V2 v = tile[sub_local(h, d)];
-                    vr[d] = v.x;
-                    vi[d] = v.y;
-                }
-            }
-            sub_apply<T, SPEC, 0>(vr, vi, R.trots, h.rb, h.nr, h.r, i0);
-            if (h.F != 1.0) sub_scale<T>(vr, vi, (T)h.F);
-            if (s == 0) {
-                // every thread has consumed its loads of this tile: tell the partner its reads of my
-                // slots for this tile are done
-                __syncthreads();
-                if (tid == 0) flag_release(R.peer_flags + tau, P.epoch);
-            }
-            if (s == P.nsub - 1) {
-                // the partner's tile holding my slots of this tile (with bit ell != keep) is tau ^ dtau
-                if (tid == 0) {
-                    // bounded wait: a protocol error traps (a CUDA error) instead of hanging the GPU
-                    uint32_t spins = 0;
-                    while (flag_acquire(R.flags + (tau ^ P.dtau)) != P.epoch) {
-                        __nanosleep(128);
-                        if (++spins > (1u << 27)) __trap();
-                    }
-                }
-                __syncthreads();
-                uint64_t gi[kSubAmps];
-                elem_index(gi, h, i0, soff, P.cbits, cmask);
-#pragma unroll
-                for (int d = 0; d < kSubAmps; ++d) {
-                    V2 v;
-                    v.x = vr[d];
-                    v.y = vi[d];
-                    __stcs(&g[gi[d]], v);
-                }
-            } else {
-#pragma unroll
-                for (int d = 0; d < kSubAmps; ++d) {
-                    V2 v;
-                    v.x = vr[d];
-                    v.y = vi[d];
-                    tile[sub_local(h, d)] = v;
-                }
-                __syncthreads();
-            }
-        }
-        __syncthreads();  // last sub-group's shared reads before the next tile's writes
-    }
+    XtArgs xa;
+    xa.peer = R.peer;
+    xa.flags = R.flags;
+    xa.peer_flags = R.peer_flags;
+    xa.lbit = 1ull << P.ell;
+    xa.keepbit = (uint64_t)R.keep << P.ell;
+    xa.dtau = P.dtau;
+    xa.dtau_dep = P.dtau_dep;
+    xa.epoch = P.epoch;
+    xa.cta = blockIdx.x % P.ctas_per_rank;
+    xa.ncta = P.ctas_per_rank;
+    // the tile kernel's body with the partner's half gathered through the peer pointer, the
+    // LDGSTS next-tile prefetch (remote elements included) and the per-tile handshake
+    coset_body<T, SPEC, 0, uint64_t, 1>(reinterpret_cast<T*>(R.a), P.kbits, P.cbits, P.runs, P.offs, P.ntiles, R.subs,
+                                        P.nsub, R.trots, 4, 0, P.free_mask, xa);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -1718,13 +1745,20 @@ cudaError_t launch_tile_t(T* a, int nl, const Pass& p, const DevSub* d_subs, con
     return cudaGetLastError();
 }
 
+uint64_t pdep_host(uint64_t v, uint64_t mask) {
+    uint64_t out = 0;
+    for (uint64_t m = mask; m; m &= m - 1, v >>= 1)
+        if (v & 1) out |= m & (~m + 1);
+    return out;
+}
+
 template <typename T, int SPEC>
 cudaError_t launch_xtile_t(const XTileRank* ranks, int nranks, const Pass& p, const uint64_t* d_offs, int ell,
                            uint64_t dtau, uint32_t epoch, cudaStream_t s, int grid_cap) {
     if (nranks < 1 || nranks > kMaxXRanks) return cudaErrorInvalidValue;
     const int threads = 1 << (p.kbits - kSubDim);
     if (threads > kCosetThreads) return cudaErrorInvalidValue;
-    const size_t smem = coset_off_bytes(p.kbits - p.cbits) + ((size_t)(2 * sizeof(T)) << p.kbits);
+    const size_t smem = coset_smem_bytes(p.kbits, p.cbits, 2 * sizeof(T));
     static uint64_t attr_devices = 0;
     const int dev = current_device();
     if (!((attr_devices >> dev) & 1)) {
@@ -1747,6 +1781,7 @@ cudaError_t launch_xtile_t(const XTileRank* ranks, int nranks, const Pass& p, co
     P.ntiles = ntiles;
     P.free_mask = p.free_mask;
     P.dtau = dtau;
+    P.dtau_dep = pdep_host(dtau, p.free_mask);
     P.nranks = nranks;
     P.ctas_per_rank = (int)per;
     P.kbits = p.kbits;
@@ -1808,7 +1843,7 @@ cudaError_t launch_tile(int dtype, void* a, int nl, const Pass& p, const DevSub*
     // tune: bit 0 = L2 prefetch of the next tile (register-direct kernel); bits 4.. = grid multiplier
     // bit 0: TMA bulk L2 prefetch; bit 8: per-thread L2 prefetch; bit 9: L2::256B load hint
     // bit 11: LDGSTS prefetch of the next tile's first sub-group into shared memory
-    const int l2p = (tune & 1) | ((tune >> 7) & 2) | ((tune >> 7) & 4) | ((tune >> 8) & 8);
+    const int l2p = ((tune >> 7) & 4) | ((tune >> 8) & 8) | ((tune >> 8) & 16);
     const int occ_sel = (tune >> 1) & 7;
     const int gm = ((tune >> 4) & 15) ? ((tune >> 4) & 15) : 4;
     if (use_tma == 2 && (tune & 1024) && h_subs) {

@@ -59,12 +59,18 @@ def test_large_n_default_options(n, count, kind, dtype):
 @pytest.mark.parametrize("dtype", ["c128", "c64"])
 @pytest.mark.parametrize("kind", ["R10", "R4", "S8"])
 @pytest.mark.parametrize("n,cap", [(14, 1), (16, 3), (18, 7)])
-def test_grid_cap_many_tiles_per_cta(n, cap, kind, dtype):
+@pytest.mark.parametrize("tune", [0, 5632])
+def test_grid_cap_many_tiles_per_cta(n, cap, kind, dtype, tune):
+    """Many tiles per CTA; tune 5632 = the next tile prefetched by TMA bulk copies (mbarrier phases
+    alternate per tile)."""
     codes, ang, want = _want(n, kind, 300, 32)
-    got, _ = _run(n, dtype, codes, ang, grid_cap=cap)
+    opts = dict(grid_cap=cap)
+    if tune:
+        opts["tile_tune"] = tune
+    got, _ = _run(n, dtype, codes, ang, **opts)
     assert np.max(np.abs(got - want)) <= TOL[dtype]
     ref, _ = _run(n, dtype, codes, ang)
-    assert np.array_equal(got, ref)  # the tile schedule does not change any arithmetic
+    assert np.array_equal(got, ref)  # the tile schedule and the prefetch do not change any arithmetic
 
 
 @pytest.mark.parametrize("dtype,tile_bits", [("c128", 13), ("c64", 12), ("c64", 13), ("c64", 14)])
