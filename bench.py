@@ -63,7 +63,7 @@ def parse():
                     help="tile-kernel variant: -1 library default (fp64 2, fp32 0), 0 generic, 2 unit-dx specialised, "
                          "1 planner's per-pass choice")
     ap.add_argument("--group", type=int, default=10, help="SUFFIX: rotations per group sharing an upper string")
-    ap.add_argument("--fused", type=int, default=1, help="world > 1: fused exchange + tile kernel (1) or swaps (0)")
+    ap.add_argument("--fused", type=int, default=0, help="world > 1: fused exchange + tile kernel (1) or swaps (0, default)")
     ap.add_argument("--emulate", type=int, default=0,
                     help="run the multi-rank path as G virtual ranks on this one GPU (ps_create_emulated)")
     ap.add_argument("--no-e2e", action="store_true")

@@ -142,8 +142,10 @@ enum {
     PS_OPT_FUSED_EXCHANGE = 14 /* world > 1 with peer access (P2P transport or emulation): 1 = a
                                  half-vector exchange followed by a tile pass runs as ONE kernel that
                                  reads the partner's half through the peer pointer and stores in the
-                                 new layout, with per-tile release/acquire flags instead of a swap
-                                 (default); 0 = swap, then the pass */
+                                 new layout, with per-tile release/acquire flags instead of a swap;
+                                 0 = swap, then the pass, overlapped on two streams (default: the
+                                 fused kernel measured slower, profiles/r02/multi_gpu.md)
+                                  */
 };
 
 /* ------------------------------------------------------------------------------------------ */

@@ -116,7 +116,7 @@ struct ps_state {
     size_t flags_cap = 0;
     std::vector<uint32_t*> peer_flags;
     uint32_t epoch = 0;
-    int fused = 1;
+    int fused = 0;  // off by default: measured slower than swap + overlap (profiles/r02/multi_gpu.md)
     void* d_mirror = nullptr;  // PS_OPT_LAYOUT=2 mirror buffer B_k
     cudaStream_t xstream = nullptr;  // second stream: swaps overlapped with the next pass
     static constexpr int kMaxPieceBits = 3;

@@ -669,32 +669,6 @@ __host__ __device__ inline size_t coset_smem_bytes(int kbits, int cbits, size_t 
     return (amp_bytes << kbits) + coset_rep_bytes(kbits, amp_bytes) + coset_off_bytes(kbits - cbits);
 }
 
-// TMA bulk copy of one contiguous chunk HBM -> shared memory, completing on an mbarrier (tx bytes)
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-            (uint32_t)__cvta_generic_to_shared(dst)),
-        "l"(src), "r"(bytes), "r"((uint32_t)__cvta_generic_to_shared(bar))
-        : "memory");
-}
-__device__ __forceinline__ void mbar_expect(uint64_t* bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"((uint32_t)__cvta_generic_to_shared(bar)),
-                 "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_wait_phase(uint64_t* bar, uint32_t parity) {
-    uint32_t done = 0;
-    while (!done) {
-        asm volatile(
-            "{\n\t.reg .pred p;\n\t"
-            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-            "selp.u32 %0, 1, 0, p;\n\t}"
-            : "=r"(done)
-            : "r"((uint32_t)__cvta_generic_to_shared(bar)), "r"(parity)
-            : "memory");
-    }
-}
-
 // shared-memory byte offsets of the thread's 16 elements l_d = r xor U(d): o_d = o_(d without its
 // lowest bit) xor (u_lowest << log2 amp bytes) -- one xor each (the tile sits at offset 0)
 template <int LB>
@@ -767,30 +741,8 @@ __device__ __forceinline__ void coset_body(T* __restrict__ a, int kbits, int cbi
     // memory (LDGSTS, one slot per thread and element) as soon as this tile's last sub-group has
     // its inputs in registers, so the next tile's reads are in flight while this one is computed
     // and stored; sub-group 0 then reads its own slots instead of HBM
-    // tune bit 12 (l2_prefetch & 16): the same prefetch by the TMA engine -- one cp.async.bulk per
-    // contiguous chunk into the tile in tile order, completion on an mbarrier -- instead of 16
-    // LDGSTS per thread; sub-group 0 then reads the tile like every later sub-group
-    const bool bulk = !XT && (l2_prefetch & 16) != 0;  // (a fused chunk may straddle both slices)
-    const bool pf = XT || (l2_prefetch & 8) != 0 || bulk;
-    __shared__ __align__(8) uint64_t tma_bar;
-    uint32_t tma_phase = 0;
-    if (bulk) {
-        if (tid == 0) {
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"((uint32_t)__cvta_generic_to_shared(&tma_bar)));
-            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        }
-        __syncthreads();
-    }
-    const uint32_t chunk_bytes = (uint32_t)sizeof(V2) << cbits;
+    const bool pf = XT || (l2_prefetch & 8) != 0;
     auto prefetch_tile = [&](uint64_t i1) {
-        if (bulk) {
-            // every thread's shared-memory reads of the buffer are done (barrier before the call)
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            if (tid == 0) mbar_expect(&tma_bar, chunk_bytes << hbits);
-            for (uint32_t u = tid; u < (1u << hbits); u += nthr)
-                bulk_g2s(smem_raw + (size_t)u * chunk_bytes, &g[i1 ^ soff[u]], chunk_bytes, &tma_bar);
-            return;
-        }
         SubHdr h0 = load_sub_hdr<PARAM>(subs);
         h0.r = rep(0);
         IDX gi[kSubAmps];
@@ -807,18 +759,7 @@ __device__ __forceinline__ void coset_body(T* __restrict__ a, int kbits, int cbi
         for (int s = 0; s < nsub; ++s) {
             SubHdr h = load_sub_hdr<PARAM>(subs + s);
             h.r = rep(s);
-            if (s == 0 && bulk) {
-                mbar_wait_phase(&tma_bar, tma_phase);
-                tma_phase ^= 1u;
-                uint32_t o[kSubAmps];
-                smem_offsets<LB>(o, h);
-#pragma unroll
-                for (int d = 0; d < kSubAmps; ++d) {
-                    const V2 v = *reinterpret_cast<const V2*>(smem_raw + o[d]);
-                    vr[d] = v.x;
-                    vi[d] = v.y;
-                }
-            } else if (s == 0 && pf) {
+            if (s == 0 && pf) {
                 asm volatile("cp.async.wait_group 0;" ::: "memory");
 #pragma unroll
                 for (int d = 0; d < kSubAmps; ++d) {
@@ -1843,7 +1784,7 @@ cudaError_t launch_tile(int dtype, void* a, int nl, const Pass& p, const DevSub*
     // tune: bit 0 = L2 prefetch of the next tile (register-direct kernel); bits 4.. = grid multiplier
     // bit 0: TMA bulk L2 prefetch; bit 8: per-thread L2 prefetch; bit 9: L2::256B load hint
     // bit 11: LDGSTS prefetch of the next tile's first sub-group into shared memory
-    const int l2p = ((tune >> 7) & 4) | ((tune >> 8) & 8) | ((tune >> 8) & 16);
+    const int l2p = ((tune >> 7) & 4) | ((tune >> 8) & 8);
     const int occ_sel = (tune >> 1) & 7;
     const int gm = ((tune >> 4) & 15) ? ((tune >> 4) & 15) : 4;
     if (use_tma == 2 && (tune & 1024) && h_subs) {

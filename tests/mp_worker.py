@@ -64,10 +64,12 @@ def main():
             codes, ang = layer_with_global(n, 300, n, world)
             x, z = P.pauli_encode_codes(codes)
             want = oracle.apply(n, oracle.random_state(SEED, n), codes, ang) if rank == 0 else None
-            for fusion, chunk, layout, transport, ovl in ((0, 4096, 0, 0, 1), (1, 1 << 28, 0, 1, 1), (2, 4096, 0, 0, 1),
-                                                          (2, 1 << 28, 1, 1, 1), (0, 1 << 28, 1, 0, 1), (2, 4096, 1, 1, 0),
-                                                          (2, 1 << 28, 2, 1, 1), (1, 4096, 2, 0, 1)):
+            for fusion, chunk, layout, transport, ovl, fused in (
+                    (0, 4096, 0, 0, 1, 0), (1, 1 << 28, 0, 1, 1, 0), (2, 4096, 0, 0, 1, 0), (2, 1 << 28, 1, 1, 1, 0),
+                    (0, 1 << 28, 1, 0, 1, 0), (2, 4096, 1, 1, 0, 0), (2, 1 << 28, 2, 1, 1, 0), (1, 4096, 2, 0, 1, 0),
+                    (2, 1 << 28, 1, 1, 1, 1), (2, 4096, 0, 1, 0, 1)):
                 with P.State(n, "c128", world=world, rank=rank) as st:
+                    st.set_option(ps.OPT_FUSED_EXCHANGE, fused)
                     st.set_option(ps.OPT_OVERLAP, ovl)
                     st.set_option(ps.OPT_FUSION, fusion)
                     st.set_option(ps.OPT_TILE_BITS, 6)
@@ -83,7 +85,8 @@ def main():
                     got = st.get_amplitudes()
                     stats = st.stats()
                 if rank == 0:
-                    tag = f"n={n} fusion={fusion} chunk={chunk} layout={layout} transport={transport} overlap={ovl}"
+                    tag = (f"n={n} fusion={fusion} chunk={chunk} layout={layout} transport={transport} overlap={ovl} "
+                           f"fused={fused}")
                     check(f"oracle {tag} exch={stats['exchanges']} perm={stats['launches']['permute']}",
                           np.max(np.abs(got - want)), 1e-10)
                     check(f"mid-call norm {tag}", abs(nrm_mid - oracle.norm(n, oracle.random_state(SEED, n))) /

@@ -59,10 +59,9 @@ def test_large_n_default_options(n, count, kind, dtype):
 @pytest.mark.parametrize("dtype", ["c128", "c64"])
 @pytest.mark.parametrize("kind", ["R10", "R4", "S8"])
 @pytest.mark.parametrize("n,cap", [(14, 1), (16, 3), (18, 7)])
-@pytest.mark.parametrize("tune", [0, 5632])
+@pytest.mark.parametrize("tune", [0, 1536])
 def test_grid_cap_many_tiles_per_cta(n, cap, kind, dtype, tune):
-    """Many tiles per CTA; tune 5632 = the next tile prefetched by TMA bulk copies (mbarrier phases
-    alternate per tile)."""
+    """Many tiles per CTA, with (default fp64) and without (tune 1536) the next-tile prefetch."""
     codes, ang, want = _want(n, kind, 300, 32)
     opts = dict(grid_cap=cap)
     if tune:

@@ -83,12 +83,11 @@ def test_specialised_kernel_identical(dtype, kind, n, count, tb):
 def test_param_block_records_identical(dtype, kind, n, count, tb):
     """Records read from the launch's parameter block (PS_OPT_TILE_TUNE bit 10, the default) and
     from global memory (bit 10 clear), with or without the shared-memory prefetch of the next
-    tile by LDGSTS (bit 11) or by TMA bulk copies (bit 12), drive the same arithmetic:
-    bitwise-identical results."""
+    tile (bit 11), drive the same arithmetic: bitwise-identical results."""
     codes, ang, want = _want(n, kind, count, 11)
     x, z = P.pauli_encode_codes(codes)
     outs = []
-    for tune in (512, 1536, 512 | 2048, 1536 | 2048, 1536 | 4096, 512 | 4096):
+    for tune in (512, 1536, 512 | 2048, 1536 | 2048):
         with P.State(n, dtype) as st:
             st.set_option(ps.OPT_TILE_BITS, tb)
             st.set_option(ps.OPT_TILE_TUNE, tune)

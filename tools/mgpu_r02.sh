@@ -20,4 +20,4 @@ for L in ${LS-1 10 100}; do
   run SUFFIX_L${L}_layout1_fused0 --kind SUFFIX --group $L --layout 1 --fused 0 --layer 1000 --qubits 30
 done
 run JW_32 --kind JW --qubits 32
-run JW_32_fused0 --kind JW --qubits 32 --fused 0
+run JW_32_fused1 --kind JW --qubits 32 --fused 1
