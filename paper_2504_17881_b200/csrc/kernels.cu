@@ -430,6 +430,120 @@ __device__ __forceinline__ void cform_sub(T (&vr)[kSubAmps], T (&vi)[kSubAmps], 
 #define PS_UC8(R, XI) PS_UC(R, XI, 0) PS_UC(R, XI, 1) PS_UC(R, XI, 2) PS_UC(R, XI, 3) PS_UC(R, XI, 4) \
     PS_UC(R, XI, 5) PS_UC(R, XI, 6) PS_UC(R, XI, 7)
 
+#ifdef PS_DISPATCH2
+// two-level dispatch (A/B build): 16-way inner switches
+template <typename T>
+__device__ __forceinline__ void unit_dispatch(T (&vr)[kSubAmps], T (&vi)[kSubAmps], uint32_t ucase, T t) {
+    switch (ucase >> 4) {
+    case 0:
+        switch (ucase & 15u) {
+        case 0: cform_sub<0, 0, 0, T>(vr, vi, t); break;
+        case 1: cform_sub<0, 0, 1, T>(vr, vi, t); break;
+        case 2: cform_sub<0, 0, 2, T>(vr, vi, t); break;
+        case 3: cform_sub<0, 0, 3, T>(vr, vi, t); break;
+        case 4: cform_sub<0, 0, 4, T>(vr, vi, t); break;
+        case 5: cform_sub<0, 0, 5, T>(vr, vi, t); break;
+        case 6: cform_sub<0, 0, 6, T>(vr, vi, t); break;
+        case 7: cform_sub<0, 0, 7, T>(vr, vi, t); break;
+        case 8: cform_sub<0, 0, 8, T>(vr, vi, t); break;
+        case 9: cform_sub<0, 0, 9, T>(vr, vi, t); break;
+        case 10: cform_sub<0, 0, 10, T>(vr, vi, t); break;
+        case 11: cform_sub<0, 0, 11, T>(vr, vi, t); break;
+        case 12: cform_sub<0, 0, 12, T>(vr, vi, t); break;
+        case 13: cform_sub<0, 0, 13, T>(vr, vi, t); break;
+        case 14: cform_sub<0, 0, 14, T>(vr, vi, t); break;
+        case 15: cform_sub<0, 0, 15, T>(vr, vi, t); break;
+        default: break;
+        }
+        break;
+    case 1:
+        switch (ucase & 15u) {
+        case 0: cform_sub<0, (1 << 0), tu_dz(0, 0), T>(vr, vi, t); break;
+        case 1: cform_sub<0, (1 << 0), tu_dz(0, 1), T>(vr, vi, t); break;
+        case 2: cform_sub<0, (1 << 0), tu_dz(0, 2), T>(vr, vi, t); break;
+        case 3: cform_sub<0, (1 << 0), tu_dz(0, 3), T>(vr, vi, t); break;
+        case 4: cform_sub<0, (1 << 0), tu_dz(0, 4), T>(vr, vi, t); break;
+        case 5: cform_sub<0, (1 << 0), tu_dz(0, 5), T>(vr, vi, t); break;
+        case 6: cform_sub<0, (1 << 0), tu_dz(0, 6), T>(vr, vi, t); break;
+        case 7: cform_sub<0, (1 << 0), tu_dz(0, 7), T>(vr, vi, t); break;
+        case 8: cform_sub<0, (1 << 1), tu_dz(1, 0), T>(vr, vi, t); break;
+        case 9: cform_sub<0, (1 << 1), tu_dz(1, 1), T>(vr, vi, t); break;
+        case 10: cform_sub<0, (1 << 1), tu_dz(1, 2), T>(vr, vi, t); break;
+        case 11: cform_sub<0, (1 << 1), tu_dz(1, 3), T>(vr, vi, t); break;
+        case 12: cform_sub<0, (1 << 1), tu_dz(1, 4), T>(vr, vi, t); break;
+        case 13: cform_sub<0, (1 << 1), tu_dz(1, 5), T>(vr, vi, t); break;
+        case 14: cform_sub<0, (1 << 1), tu_dz(1, 6), T>(vr, vi, t); break;
+        case 15: cform_sub<0, (1 << 1), tu_dz(1, 7), T>(vr, vi, t); break;
+        default: break;
+        }
+        break;
+    case 2:
+        switch (ucase & 15u) {
+        case 0: cform_sub<0, (1 << 2), tu_dz(2, 0), T>(vr, vi, t); break;
+        case 1: cform_sub<0, (1 << 2), tu_dz(2, 1), T>(vr, vi, t); break;
+        case 2: cform_sub<0, (1 << 2), tu_dz(2, 2), T>(vr, vi, t); break;
+        case 3: cform_sub<0, (1 << 2), tu_dz(2, 3), T>(vr, vi, t); break;
+        case 4: cform_sub<0, (1 << 2), tu_dz(2, 4), T>(vr, vi, t); break;
+        case 5: cform_sub<0, (1 << 2), tu_dz(2, 5), T>(vr, vi, t); break;
+        case 6: cform_sub<0, (1 << 2), tu_dz(2, 6), T>(vr, vi, t); break;
+        case 7: cform_sub<0, (1 << 2), tu_dz(2, 7), T>(vr, vi, t); break;
+        case 8: cform_sub<0, (1 << 3), tu_dz(3, 0), T>(vr, vi, t); break;
+        case 9: cform_sub<0, (1 << 3), tu_dz(3, 1), T>(vr, vi, t); break;
+        case 10: cform_sub<0, (1 << 3), tu_dz(3, 2), T>(vr, vi, t); break;
+        case 11: cform_sub<0, (1 << 3), tu_dz(3, 3), T>(vr, vi, t); break;
+        case 12: cform_sub<0, (1 << 3), tu_dz(3, 4), T>(vr, vi, t); break;
+        case 13: cform_sub<0, (1 << 3), tu_dz(3, 5), T>(vr, vi, t); break;
+        case 14: cform_sub<0, (1 << 3), tu_dz(3, 6), T>(vr, vi, t); break;
+        case 15: cform_sub<0, (1 << 3), tu_dz(3, 7), T>(vr, vi, t); break;
+        default: break;
+        }
+        break;
+    case 3:
+        switch (ucase & 15u) {
+        case 0: cform_sub<1, (1 << 0), tu_dz(0, 0), T>(vr, vi, t); break;
+        case 1: cform_sub<1, (1 << 0), tu_dz(0, 1), T>(vr, vi, t); break;
+        case 2: cform_sub<1, (1 << 0), tu_dz(0, 2), T>(vr, vi, t); break;
+        case 3: cform_sub<1, (1 << 0), tu_dz(0, 3), T>(vr, vi, t); break;
+        case 4: cform_sub<1, (1 << 0), tu_dz(0, 4), T>(vr, vi, t); break;
+        case 5: cform_sub<1, (1 << 0), tu_dz(0, 5), T>(vr, vi, t); break;
+        case 6: cform_sub<1, (1 << 0), tu_dz(0, 6), T>(vr, vi, t); break;
+        case 7: cform_sub<1, (1 << 0), tu_dz(0, 7), T>(vr, vi, t); break;
+        case 8: cform_sub<1, (1 << 1), tu_dz(1, 0), T>(vr, vi, t); break;
+        case 9: cform_sub<1, (1 << 1), tu_dz(1, 1), T>(vr, vi, t); break;
+        case 10: cform_sub<1, (1 << 1), tu_dz(1, 2), T>(vr, vi, t); break;
+        case 11: cform_sub<1, (1 << 1), tu_dz(1, 3), T>(vr, vi, t); break;
+        case 12: cform_sub<1, (1 << 1), tu_dz(1, 4), T>(vr, vi, t); break;
+        case 13: cform_sub<1, (1 << 1), tu_dz(1, 5), T>(vr, vi, t); break;
+        case 14: cform_sub<1, (1 << 1), tu_dz(1, 6), T>(vr, vi, t); break;
+        case 15: cform_sub<1, (1 << 1), tu_dz(1, 7), T>(vr, vi, t); break;
+        default: break;
+        }
+        break;
+    case 4:
+        switch (ucase & 15u) {
+        case 0: cform_sub<1, (1 << 2), tu_dz(2, 0), T>(vr, vi, t); break;
+        case 1: cform_sub<1, (1 << 2), tu_dz(2, 1), T>(vr, vi, t); break;
+        case 2: cform_sub<1, (1 << 2), tu_dz(2, 2), T>(vr, vi, t); break;
+        case 3: cform_sub<1, (1 << 2), tu_dz(2, 3), T>(vr, vi, t); break;
+        case 4: cform_sub<1, (1 << 2), tu_dz(2, 4), T>(vr, vi, t); break;
+        case 5: cform_sub<1, (1 << 2), tu_dz(2, 5), T>(vr, vi, t); break;
+        case 6: cform_sub<1, (1 << 2), tu_dz(2, 6), T>(vr, vi, t); break;
+        case 7: cform_sub<1, (1 << 2), tu_dz(2, 7), T>(vr, vi, t); break;
+        case 8: cform_sub<1, (1 << 3), tu_dz(3, 0), T>(vr, vi, t); break;
+        case 9: cform_sub<1, (1 << 3), tu_dz(3, 1), T>(vr, vi, t); break;
+        case 10: cform_sub<1, (1 << 3), tu_dz(3, 2), T>(vr, vi, t); break;
+        case 11: cform_sub<1, (1 << 3), tu_dz(3, 3), T>(vr, vi, t); break;
+        case 12: cform_sub<1, (1 << 3), tu_dz(3, 4), T>(vr, vi, t); break;
+        case 13: cform_sub<1, (1 << 3), tu_dz(3, 5), T>(vr, vi, t); break;
+        case 14: cform_sub<1, (1 << 3), tu_dz(3, 6), T>(vr, vi, t); break;
+        case 15: cform_sub<1, (1 << 3), tu_dz(3, 7), T>(vr, vi, t); break;
+        default: break;
+        }
+        break;
+    default: break;
+    }
+}
+#else
 template <typename T>
 __device__ __forceinline__ void unit_dispatch(T (&vr)[kSubAmps], T (&vi)[kSubAmps], uint32_t ucase, T t) {
     switch (ucase) {
@@ -443,6 +557,7 @@ __device__ __forceinline__ void unit_dispatch(T (&vr)[kSubAmps], T (&vi)[kSubAmp
     default: break;
     }
 }
+#endif
 
 // applies the rotations [rb, rb + nr) of a sub-group to the thread's 16 registers; the next
 // record is fetched while the current one is applied.  SPEC = 0: generic (one switch on dx, the
