@@ -430,8 +430,9 @@ __device__ __forceinline__ void cform_sub(T (&vr)[kSubAmps], T (&vi)[kSubAmps], 
 #define PS_UC8(R, XI) PS_UC(R, XI, 0) PS_UC(R, XI, 1) PS_UC(R, XI, 2) PS_UC(R, XI, 3) PS_UC(R, XI, 4) \
     PS_UC(R, XI, 5) PS_UC(R, XI, 6) PS_UC(R, XI, 7)
 
-#ifdef PS_DISPATCH2
-// two-level dispatch (A/B build): 16-way inner switches
+#ifndef PS_DISPATCH1
+// two-level dispatch (default: +0.9 % R10, +1.9 % JW, +1.7 % gates over one 80-way switch,
+// profiles/r02/kernel_ab.md section 7): by case id / 16, then 16-way inner switches
 template <typename T>
 __device__ __forceinline__ void unit_dispatch(T (&vr)[kSubAmps], T (&vi)[kSubAmps], uint32_t ucase, T t) {
     switch (ucase >> 4) {
