@@ -199,6 +199,21 @@ class ClockSampler:
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def fma_roofline(stats, fam, args, world, clk):
+    kms = stats["kernel_ms"][fam]
+    rot = stats["rotations_by"][fam]
+    if kms <= 0 or rot <= 0:
+        return None
+    nl = args.n - (world.bit_length() - 1)
+    fma = 2.0 * rot * float(1 << nl)  # per rank (rank 0's stats)
+    achieved = fma / (kms / 1e3)
+    lanes = 64 if args.dtype == "c128" else 128
+    mhz = (clk or {}).get("sm_max_mhz") or 1965.0
+    peak = 148 * lanes * mhz * 1e6
+    return {"bound": "alu", "unit": "FMA/s", "achieved": achieved, "peak": peak, "frac": achieved / peak,
+            "algorithmic_fma_per_rotation": 2.0 * float(1 << nl)}
+
+
 def peaks():
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -529,6 +544,10 @@ def run_ours(args):
                          "algorithmic_bytes_per_launch": bytes_per_launch,
                          "avg_launch_ms": kms / launches,
                          "traffic": traffic_for(fam, bytes_per_launch, args.dtype)},
+            # the fp64/fp32 FMA pipe roofline of the same kernel family: the deferred-scale pair update
+            # costs 2 FMA per amplitude and rotation (4 per pair); peak = 148 SMs x 64 fp64 (128 fp32)
+            # FMA lanes x the max SM clock (B200_PROFILING.md: 148 SMs, 1965 MHz)
+            "roofline_fma": fma_roofline(stats, fam, args, world, clk),
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": gpu_launches,
