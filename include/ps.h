@@ -128,7 +128,10 @@ enum {
     PS_OPT_TRANSPORT = 10,    /* world > 1: 1 = NVLink P2P swap kernel on CUDA-IPC peer pointers when
                                  available (default); 0 = NCCL send/recv with staging */
     PS_OPT_OVERLAP = 11,      /* world > 1, P2P: 1 = overlap each swap with the following tile pass
-                                 on a second stream (default); 0 = serialise */
+                                 on a second stream (default); 2 = also with the tile pass before it
+                                 (both split into pieces; a piece is swapped as soon as both ranks
+                                 finished it); 0 = serialise; > 2: on, bits 0-15 = swap CTAs,
+                                 bits 16-18 = piece bits + 1 */
     PS_OPT_SPECIALIZE = 12    /* tile-kernel variant: 2 = specialised (default for C128): CFORM
                                  rotations whose sub-group xor mask dx is a unit vector or 0 run
                                  through one of 80 compile-time cases (per-pair signs and pairing

@@ -646,8 +646,8 @@ static int set_option_rank(ps_state* h, int option, int64_t value) {
     case PS_OPT_OVERLAP: {
         // 0: off; 1: on; > 1: on, bits 0-15 = swap CTAs (if > 1), bits 16-18 = piece bits + 1
         const int pb = (int)((value >> 16) & 7);
-        h->overlap = (value && h->xstream) ? 1 : 0;
-        if ((value & 0xffff) > 1) h->swap_ctas = (int)(value & 0xffff);
+        h->overlap = (value && h->xstream) ? ((value & 0xffff) == 2 ? 2 : 1) : 0;
+        if ((value & 0xffff) > 2) h->swap_ctas = (int)(value & 0xffff);
         if (pb) h->piece_bits = pb - 1;
         break;
     }
@@ -1028,6 +1028,96 @@ static int exchange_overlap(ps_state* h, const Pass& ex, const Pass& np) {
     return PS_OK;
 }
 
+// the previous tile pass, the swap E(gx, ell) and the next tile pass as one pipeline (overlap mode
+// 2): both passes split into P = 2^B pieces by B free bits outside both tile spaces (and not ell);
+// the second stream swaps piece j as soon as both ranks finished the previous pass's piece j
+// (event + barrier), and the next pass's piece j starts when its swap landed.  The swap then
+// overlaps the previous pass as well as the next one.
+static uint64_t split_bits2(const Pass& a, const Pass& b, int ell) {
+    return split_bits(a) & split_bits(b) & ~(1ull << ell);
+}
+
+static bool can_overlap3(const ps_state* h, const Pass& pa, const Pass* ex, const Pass* np) {
+    return ex && np && (pa.kind == PASS_TILE || pa.kind == PASS_COSET) && can_overlap(h, *ex, np) &&
+           h->overlap >= 2 && split_bits2(pa, *np, ex->ell) != 0;
+}
+
+static int exchange_overlap3(ps_state* h, const Pass& pa, const Pass& ex, const Pass& np) {
+    const int partner = h->rank ^ (int)ex.gx;
+    const uint64_t rows = 1ull << (h->nl - 1 - ex.ell);
+    const uint64_t row_amps = 1ull << ex.ell, total = rows * row_amps;
+    const uint64_t my_off = (uint64_t)(1 - ex.keep) * row_amps, peer_off = (uint64_t)ex.keep * row_amps;
+    const uint64_t sb = split_bits2(pa, np, ex.ell);
+    uint64_t pbits = 0;
+    int B = 0;
+    for (int b = 63; b >= 0 && B < std::min(h->piece_bits, 2); --b)
+        if ((sb >> b) & 1) {
+            pbits |= 1ull << b;
+            ++B;
+        }
+    const int P = 1 << B;  // <= 4: events xev[1..P] (previous pass) and xev[1+P..2P] (swap)
+    auto elem_bits = [&](uint64_t m) {
+        uint64_t r = 0;
+        for (; m; m &= m - 1) {
+            const int f = __builtin_ctzll(m);
+            r |= 1ull << (f < ex.ell ? f : f - 1);
+        }
+        return r;
+    };
+    auto deposit = [](uint64_t v, uint64_t mask) {
+        uint64_t r = 0;
+        for (; mask; mask &= mask - 1, v >>= 1)
+            if (v & 1) r |= mask & (~mask + 1);
+        return r;
+    };
+    const uint64_t emask = elem_bits(pbits);
+    const uint64_t piece = total >> B;
+    const uint64_t t0 = ex.keep ? piece / 2 : 0, t1 = ex.keep ? piece : piece / 2;
+    auto run_piece = [&](const Pass& q0, int j) -> int {
+        Pass q = q0;
+        q.free_mask = q0.free_mask & ~pbits;
+        q.or_mask = q0.or_mask | deposit((uint64_t)j, pbits);
+        Timed t(h, q0.kind);
+        CUDA_TRY(h, launch_tile(h->dtype, h->d_state, h->nl, q, h->d_subs, h->d_trots, h->d_offs, h->tile_tma,
+                                h->tile_tune, h->stream, h->cur_plan->subs.data(), h->cur_plan->trots.data(),
+                                h->grid_cap));
+        return PS_OK;
+    };
+    int rc = PS_OK;
+    for (int j = 0; j < P; ++j) {
+        if ((rc = run_piece(pa, j))) return rc;
+        CUDA_TRY(h, cudaEventRecord(h->xev[1 + j], h->stream));
+    }
+    {
+        Timed t(h, PS_K_EXCHANGE, h->xstream);
+        for (int j = 0; j < P; ++j) {
+            CUDA_TRY(h, cudaStreamWaitEvent(h->xstream, h->xev[1 + j], 0));
+            if ((rc = barrier_on(h, h->xstream, 1))) return rc;  // both ranks finished piece j
+            CUDA_TRY(h, launch_p2p_swap(h->dtype, h->d_state, h->peers[partner], rows, row_amps, my_off, peer_off, t0,
+                                        t1, emask, deposit((uint64_t)j, emask), h->xstream, h->swap_ctas));
+            if ((rc = barrier_on(h, h->xstream, 2))) return rc;  // both halves of piece j landed
+            CUDA_TRY(h, cudaEventRecord(h->xev[1 + P + j], h->xstream));
+        }
+    }
+    for (int j = 0; j < P; ++j) {
+        CUDA_TRY(h, cudaStreamWaitEvent(h->stream, h->xev[1 + P + j], 0));
+        if ((rc = run_piece(np, j))) return rc;
+    }
+    const double pass_bytes = 2.0 * (double)h->amp_bytes * (double)local_amps(h);
+    for (const Pass* q : {&pa, &np}) {
+        h->stats.launches[q->kind] += 1;
+        h->stats.rotations_by[q->kind] += (uint64_t)q->rot_count;
+        h->stats.algo_bytes[q->kind] += pass_bytes;
+        h->stats.passes += 1;
+    }
+    const double region = (double)(rows * row_amps * h->amp_bytes);
+    h->stats.nvlink_bytes += region;
+    h->stats.exchanges += 1;
+    h->stats.launches[PS_K_EXCHANGE] += 1;
+    h->stats.algo_bytes[PS_K_EXCHANGE] += region * 2.0;
+    return PS_OK;
+}
+
 // single-rotation full exchange (no free pivot): chunk pairs {t, t^delta}
 static int exchange_full(ps_state* h, const Pass& p, const DevRot* d_rec, const DevRot& rec) {
     const int partner = h->rank ^ (int)p.gx;
@@ -1343,6 +1433,11 @@ static int execute_plans(const RankSet& rs, const std::vector<Plan*>& plans) {
         if (p0.kind == PASS_EXCHANGE && G <= 8 && can_fuse(rs[0], p0, next)) {
             rc = exchange_fused(rs, plans, pi);
             ++pi;  // the next pass ran inside the fused kernel
+            continue;
+        }
+        if (G == 1 && pi + 2 < np && can_overlap3(rs[0], p0, next, &plans[0]->passes[pi + 2])) {
+            rc = exchange_overlap3(rs[0], p0, *next, plans[0]->passes[pi + 2]);
+            pi += 2;  // the exchange and the pass after it ran inside the pipeline
             continue;
         }
         if (G == 1 && p0.kind == PASS_EXCHANGE && can_overlap(rs[0], p0, next)) {

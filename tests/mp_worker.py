@@ -67,7 +67,7 @@ def main():
             for fusion, chunk, layout, transport, ovl, fused in (
                     (0, 4096, 0, 0, 1, 0), (1, 1 << 28, 0, 1, 1, 0), (2, 4096, 0, 0, 1, 0), (2, 1 << 28, 1, 1, 1, 0),
                     (0, 1 << 28, 1, 0, 1, 0), (2, 4096, 1, 1, 0, 0), (2, 1 << 28, 2, 1, 1, 0), (1, 4096, 2, 0, 1, 0),
-                    (2, 1 << 28, 1, 1, 1, 1), (2, 4096, 0, 1, 0, 1)):
+                    (2, 1 << 28, 1, 1, 1, 1), (2, 4096, 0, 1, 0, 1), (2, 1 << 28, 1, 1, 2, 0), (2, 1 << 28, 0, 1, 2, 0)):
                 with P.State(n, "c128", world=world, rank=rank) as st:
                     st.set_option(ps.OPT_FUSED_EXCHANGE, fused)
                     st.set_option(ps.OPT_OVERLAP, ovl)
