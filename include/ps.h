@@ -130,8 +130,7 @@ enum {
     PS_OPT_OVERLAP = 11,      /* world > 1, P2P: 1 = overlap each swap with the following tile pass
                                  on a second stream (default); 2 = also with the tile pass before it
                                  (both split into pieces; a piece is swapped as soon as both ranks
-                                 finished it); 0 = serialise; > 2: on, bits 0-15 = swap CTAs,
-                                 bits 16-18 = piece bits + 1 */
+                                 finished it); 0 = serialise; bits 16-18 = piece bits + 1 */
     PS_OPT_SPECIALIZE = 12    /* tile-kernel variant: 2 = specialised (default for C128): CFORM
                                  rotations whose sub-group xor mask dx is a unit vector or 0 run
                                  through one of 80 compile-time cases (per-pair signs and pairing
@@ -148,7 +147,11 @@ enum {
                                  new layout, with per-tile release/acquire flags instead of a swap;
                                  0 = swap, then the pass, overlapped on two streams (default: the
                                  fused kernel measured slower, profiles/r02/multi_gpu.md)
-                                  */
+                                  */,
+    PS_OPT_SWAP_CTAS = 15     /* overlapped swap pieces (PS_OPT_OVERLAP): 0 = the slim swap kernel
+                                 (128 threads, <= 64 registers) with one CTA per SM, which fits next
+                                 to the tile kernel's resident CTAs (default); -k = k slim CTAs;
+                                 k > 0 = k full-size CTAs (512 threads: they wait for whole SMs) */
 };
 
 /* ------------------------------------------------------------------------------------------ */

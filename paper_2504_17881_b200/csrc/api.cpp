@@ -123,7 +123,8 @@ struct ps_state {
     static constexpr int kXev = 2 + (1 << kMaxPieceBits);
     cudaEvent_t xev[kXev] = {};
     int overlap = 1;
-    int swap_ctas = 32;   // CTAs of an overlapped swap (NVLink-bound; leaves SMs to the pass)
+    int swap_ctas = -1;   // overlapped swap pieces: < 0 the slim kernel that co-resides with the
+                          // tile kernel (-1: one CTA per SM), > 0 that many full-size CTAs
     int piece_bits = 2;   // an overlapped swap/pass pair runs in up to 2^piece_bits pieces
     const Plan* cur_plan = nullptr;  // the plan being executed (host copies of its records)
     int layout = 1, transport = 1;
@@ -610,8 +611,12 @@ static int check_option(const ps_state* h, int option, int64_t value) {
     case PS_OPT_MAX_PASS_ROTS: return value < 1 ? fail(PS_EINVAL, "max pass rotations must be >= 1") : PS_OK;
     case PS_OPT_LAYOUT: return (value < 0 || value > 2) ? fail(PS_EINVAL, "layout must be 0, 1 or 2") : PS_OK;
     case PS_OPT_OVERLAP:
+        if ((value & 0xffff) > 2) return fail(PS_EINVAL, "overlap mode must be 0, 1 or 2");
         return (((value >> 16) & 7) > ps_state::kMaxPieceBits + 1) ? fail(PS_EINVAL, "overlap piece bits must be <= 3")
                                                                     : PS_OK;
+    case PS_OPT_SWAP_CTAS:
+        return (value < -(1 << 16) || value > (1 << 16)) ? fail(PS_EINVAL, "swap CTAs must be in [-65536, 65536]")
+                                                         : PS_OK;
     case PS_OPT_CHUNK_BITS:
         return (value < 0 || value > 12) ? fail(PS_EINVAL, "chunk bits must be 0..12 (0 = default)") : PS_OK;
     case PS_OPT_SPECIALIZE: return (value < 0 || value > 2) ? fail(PS_EINVAL, "specialize must be 0, 1 or 2") : PS_OK;
@@ -644,13 +649,13 @@ static int set_option_rank(ps_state* h, int option, int64_t value) {
         break;
     case PS_OPT_TRANSPORT: h->transport = (value || h->emulated) ? 1 : 0; break;
     case PS_OPT_OVERLAP: {
-        // 0: off; 1: on; > 1: on, bits 0-15 = swap CTAs (if > 1), bits 16-18 = piece bits + 1
+        // 0: off; 1: with the next pass; 2: with the passes before and after; bits 16-18 = piece bits + 1
         const int pb = (int)((value >> 16) & 7);
         h->overlap = (value && h->xstream) ? ((value & 0xffff) == 2 ? 2 : 1) : 0;
-        if ((value & 0xffff) > 2) h->swap_ctas = (int)(value & 0xffff);
         if (pb) h->piece_bits = pb - 1;
         break;
     }
+    case PS_OPT_SWAP_CTAS: h->swap_ctas = value == 0 ? -1 : (int)value; break;
     case PS_OPT_CHUNK_BITS: h->chunk_bits = (int)value; break;
     case PS_OPT_SPECIALIZE: h->specialize = (int)value; break;
     case PS_OPT_GRID_CAP: h->grid_cap = (int)value; break;

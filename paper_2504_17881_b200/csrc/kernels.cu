@@ -392,16 +392,30 @@ __device__ __forceinline__ void sub_rotation(T (&vr)[kSubAmps], T (&vi)[kSubAmps
 __host__ __device__ constexpr int par4(int v) { return (v ^ (v >> 1) ^ (v >> 2) ^ (v >> 3)) & 1; }
 
 // one CFORM rotation with a compile-time pair pattern (dx = DX) and sign pattern parity(DZ & d):
-// four fused multiply-adds per pair, the signs ride on the FMA operands
+// four fused multiply-adds per pair, the signs ride on the FMA operands.  PS_SHEAR: every
+// two-cycle of components (x, y) is rotated in place by three shears, x -= tau y; y += sg x;
+// x -= tau y (tau = tan(theta/2), sg = sin(theta), ps_internal.h kTrUnit): six FMAs per pair and
+// no register moves (the 4-FMA form must park one member of each two-cycle in a temporary)
+template <typename T>
+__device__ __forceinline__ void shear3(T& x, T& y, T tau, T sg) {
+    x = pfma(-tau, y, x);
+    y = pfma(sg, x, y);
+    x = pfma(-tau, y, x);
+}
+
 template <int REAL, int DX, int DZ, typename T>
-__device__ __forceinline__ void cform_sub(T (&vr)[kSubAmps], T (&vi)[kSubAmps], T t) {
+__device__ __forceinline__ void cform_sub(T (&vr)[kSubAmps], T (&vi)[kSubAmps], T t, T sg) {
     if constexpr (DX == 0) {
 #pragma unroll
         for (int d = 0; d < kSubAmps; ++d) {
             const T b = par4(DZ & d) ? -t : t;
+#if PS_SHEAR
+            shear3(vr[d], vi[d], b, par4(DZ & d) ? -sg : sg);
+#else
             const T nr = pfma(-b, vi[d], vr[d]), ni = pfma(b, vr[d], vi[d]);
             vr[d] = nr;
             vi[d] = ni;
+#endif
         }
     } else if constexpr (DX < kSubAmps) {
         constexpr int piv = hibit(DX);
@@ -410,6 +424,16 @@ __device__ __forceinline__ void cform_sub(T (&vr)[kSubAmps], T (&vi)[kSubAmps], 
             if ((d >> piv) & 1) continue;
             const int e = d ^ DX;
             const T b = par4(DZ & d) ? -t : t;
+#if PS_SHEAR
+            const T g = par4(DZ & d) ? -sg : sg;
+            if (REAL) {
+                shear3(vr[d], vr[e], b, g);
+                shear3(vi[d], vi[e], b, g);
+            } else {
+                shear3(vr[d], vi[e], b, g);
+                shear3(vr[e], vi[d], b, g);
+            }
+#else
             if (REAL) {
                 const T nir = pfma(-b, vr[e], vr[d]), nii = pfma(-b, vi[e], vi[d]);
                 const T njr = pfma(b, vr[d], vr[e]), nji = pfma(b, vi[d], vi[e]);
@@ -419,14 +443,59 @@ __device__ __forceinline__ void cform_sub(T (&vr)[kSubAmps], T (&vi)[kSubAmps], 
                 const T njr = pfma(-b, vi[d], vr[e]), nji = pfma(b, vr[d], vi[e]);
                 vr[d] = nir; vi[d] = nii; vr[e] = njr; vi[e] = nji;
             }
+#endif
         }
     }
 }
 
+#if PS_SHEAR
+// the generic kernel's form of the same shear rotation (unit dx, run-time per-pair signs Ms)
+template <int REAL, int DX, typename T>
+__device__ __forceinline__ void shear_pairs(T (&vr)[kSubAmps], T (&vi)[kSubAmps], uint32_t Ms, T t, T sg) {
+#pragma unroll
+    for (int d = 0; d < kSubAmps; ++d) {
+        const int ng = (int)((Ms >> d) & 1u);
+        const T b = flip(t, ng), g = flip(sg, ng);
+        if constexpr (DX == 0) {
+            shear3(vr[d], vi[d], b, g);
+        } else {
+            if ((d >> hibit(DX)) & 1) continue;
+            const int e = d ^ DX;
+            if (REAL) {
+                shear3(vr[d], vr[e], b, g);
+                shear3(vi[d], vi[e], b, g);
+            } else {
+                shear3(vr[d], vi[e], b, g);
+                shear3(vr[e], vi[d], b, g);
+            }
+        }
+    }
+}
+
+template <typename T>
+__device__ __forceinline__ void shear_rotation(T (&vr)[kSubAmps], T (&vi)[kSubAmps], uint32_t dx, int real,
+                                               uint32_t Ms, T t, T sg) {
+    switch (dx | (real ? 16u : 0u)) {
+    case 0: shear_pairs<0, 0>(vr, vi, Ms, t, sg); break;
+    case 1: shear_pairs<0, 1>(vr, vi, Ms, t, sg); break;
+    case 2: shear_pairs<0, 2>(vr, vi, Ms, t, sg); break;
+    case 4: shear_pairs<0, 4>(vr, vi, Ms, t, sg); break;
+    case 17: shear_pairs<1, 1>(vr, vi, Ms, t, sg); break;
+    case 18: shear_pairs<1, 2>(vr, vi, Ms, t, sg); break;
+    case 20: shear_pairs<1, 4>(vr, vi, Ms, t, sg); break;
+#if PS_SUBDIM >= 4
+    case 8: shear_pairs<0, 8>(vr, vi, Ms, t, sg); break;
+    case 24: shear_pairs<1, 8>(vr, vi, Ms, t, sg); break;
+#endif
+    default: break;
+    }
+}
+#endif
+
 // unit cases (ps_internal.h tu_case): diagonal by its 4-bit Dz, unit dx by (real, log2 dx, the three
 // Dz bits other than the pivot's); signs and the pair pattern are compile-time
-#define PS_UD(Z) case Z: cform_sub<0, 0, Z, T>(vr, vi, t); break;
-#define PS_UC(R, XI, Z3) case tu_case(R, XI, tu_dz(XI, Z3)): cform_sub<R, (1 << XI), tu_dz(XI, Z3), T>(vr, vi, t); break;
+#define PS_UD(Z) case Z: cform_sub<0, 0, Z, T>(vr, vi, t, sg); break;
+#define PS_UC(R, XI, Z3) case tu_case(R, XI, tu_dz(XI, Z3)): cform_sub<R, (1 << XI), tu_dz(XI, Z3), T>(vr, vi, t, sg); break;
 #define PS_UC8(R, XI) PS_UC(R, XI, 0) PS_UC(R, XI, 1) PS_UC(R, XI, 2) PS_UC(R, XI, 3) PS_UC(R, XI, 4) \
     PS_UC(R, XI, 5) PS_UC(R, XI, 6) PS_UC(R, XI, 7)
 
@@ -434,110 +503,110 @@ __device__ __forceinline__ void cform_sub(T (&vr)[kSubAmps], T (&vi)[kSubAmps], 
 // two-level dispatch (default: +0.9 % R10, +1.9 % JW, +1.7 % gates over one 80-way switch,
 // profiles/r02/kernel_ab.md section 7): by case id / 16, then 16-way inner switches
 template <typename T>
-__device__ __forceinline__ void unit_dispatch(T (&vr)[kSubAmps], T (&vi)[kSubAmps], uint32_t ucase, T t) {
+__device__ __forceinline__ void unit_dispatch(T (&vr)[kSubAmps], T (&vi)[kSubAmps], uint32_t ucase, T t, T sg) {
     switch (ucase >> 4) {
     case 0:
         switch (ucase & 15u) {
-        case 0: cform_sub<0, 0, 0, T>(vr, vi, t); break;
-        case 1: cform_sub<0, 0, 1, T>(vr, vi, t); break;
-        case 2: cform_sub<0, 0, 2, T>(vr, vi, t); break;
-        case 3: cform_sub<0, 0, 3, T>(vr, vi, t); break;
-        case 4: cform_sub<0, 0, 4, T>(vr, vi, t); break;
-        case 5: cform_sub<0, 0, 5, T>(vr, vi, t); break;
-        case 6: cform_sub<0, 0, 6, T>(vr, vi, t); break;
-        case 7: cform_sub<0, 0, 7, T>(vr, vi, t); break;
-        case 8: cform_sub<0, 0, 8, T>(vr, vi, t); break;
-        case 9: cform_sub<0, 0, 9, T>(vr, vi, t); break;
-        case 10: cform_sub<0, 0, 10, T>(vr, vi, t); break;
-        case 11: cform_sub<0, 0, 11, T>(vr, vi, t); break;
-        case 12: cform_sub<0, 0, 12, T>(vr, vi, t); break;
-        case 13: cform_sub<0, 0, 13, T>(vr, vi, t); break;
-        case 14: cform_sub<0, 0, 14, T>(vr, vi, t); break;
-        case 15: cform_sub<0, 0, 15, T>(vr, vi, t); break;
+        case 0: cform_sub<0, 0, 0, T>(vr, vi, t, sg); break;
+        case 1: cform_sub<0, 0, 1, T>(vr, vi, t, sg); break;
+        case 2: cform_sub<0, 0, 2, T>(vr, vi, t, sg); break;
+        case 3: cform_sub<0, 0, 3, T>(vr, vi, t, sg); break;
+        case 4: cform_sub<0, 0, 4, T>(vr, vi, t, sg); break;
+        case 5: cform_sub<0, 0, 5, T>(vr, vi, t, sg); break;
+        case 6: cform_sub<0, 0, 6, T>(vr, vi, t, sg); break;
+        case 7: cform_sub<0, 0, 7, T>(vr, vi, t, sg); break;
+        case 8: cform_sub<0, 0, 8, T>(vr, vi, t, sg); break;
+        case 9: cform_sub<0, 0, 9, T>(vr, vi, t, sg); break;
+        case 10: cform_sub<0, 0, 10, T>(vr, vi, t, sg); break;
+        case 11: cform_sub<0, 0, 11, T>(vr, vi, t, sg); break;
+        case 12: cform_sub<0, 0, 12, T>(vr, vi, t, sg); break;
+        case 13: cform_sub<0, 0, 13, T>(vr, vi, t, sg); break;
+        case 14: cform_sub<0, 0, 14, T>(vr, vi, t, sg); break;
+        case 15: cform_sub<0, 0, 15, T>(vr, vi, t, sg); break;
         default: break;
         }
         break;
     case 1:
         switch (ucase & 15u) {
-        case 0: cform_sub<0, (1 << 0), tu_dz(0, 0), T>(vr, vi, t); break;
-        case 1: cform_sub<0, (1 << 0), tu_dz(0, 1), T>(vr, vi, t); break;
-        case 2: cform_sub<0, (1 << 0), tu_dz(0, 2), T>(vr, vi, t); break;
-        case 3: cform_sub<0, (1 << 0), tu_dz(0, 3), T>(vr, vi, t); break;
-        case 4: cform_sub<0, (1 << 0), tu_dz(0, 4), T>(vr, vi, t); break;
-        case 5: cform_sub<0, (1 << 0), tu_dz(0, 5), T>(vr, vi, t); break;
-        case 6: cform_sub<0, (1 << 0), tu_dz(0, 6), T>(vr, vi, t); break;
-        case 7: cform_sub<0, (1 << 0), tu_dz(0, 7), T>(vr, vi, t); break;
-        case 8: cform_sub<0, (1 << 1), tu_dz(1, 0), T>(vr, vi, t); break;
-        case 9: cform_sub<0, (1 << 1), tu_dz(1, 1), T>(vr, vi, t); break;
-        case 10: cform_sub<0, (1 << 1), tu_dz(1, 2), T>(vr, vi, t); break;
-        case 11: cform_sub<0, (1 << 1), tu_dz(1, 3), T>(vr, vi, t); break;
-        case 12: cform_sub<0, (1 << 1), tu_dz(1, 4), T>(vr, vi, t); break;
-        case 13: cform_sub<0, (1 << 1), tu_dz(1, 5), T>(vr, vi, t); break;
-        case 14: cform_sub<0, (1 << 1), tu_dz(1, 6), T>(vr, vi, t); break;
-        case 15: cform_sub<0, (1 << 1), tu_dz(1, 7), T>(vr, vi, t); break;
+        case 0: cform_sub<0, (1 << 0), tu_dz(0, 0), T>(vr, vi, t, sg); break;
+        case 1: cform_sub<0, (1 << 0), tu_dz(0, 1), T>(vr, vi, t, sg); break;
+        case 2: cform_sub<0, (1 << 0), tu_dz(0, 2), T>(vr, vi, t, sg); break;
+        case 3: cform_sub<0, (1 << 0), tu_dz(0, 3), T>(vr, vi, t, sg); break;
+        case 4: cform_sub<0, (1 << 0), tu_dz(0, 4), T>(vr, vi, t, sg); break;
+        case 5: cform_sub<0, (1 << 0), tu_dz(0, 5), T>(vr, vi, t, sg); break;
+        case 6: cform_sub<0, (1 << 0), tu_dz(0, 6), T>(vr, vi, t, sg); break;
+        case 7: cform_sub<0, (1 << 0), tu_dz(0, 7), T>(vr, vi, t, sg); break;
+        case 8: cform_sub<0, (1 << 1), tu_dz(1, 0), T>(vr, vi, t, sg); break;
+        case 9: cform_sub<0, (1 << 1), tu_dz(1, 1), T>(vr, vi, t, sg); break;
+        case 10: cform_sub<0, (1 << 1), tu_dz(1, 2), T>(vr, vi, t, sg); break;
+        case 11: cform_sub<0, (1 << 1), tu_dz(1, 3), T>(vr, vi, t, sg); break;
+        case 12: cform_sub<0, (1 << 1), tu_dz(1, 4), T>(vr, vi, t, sg); break;
+        case 13: cform_sub<0, (1 << 1), tu_dz(1, 5), T>(vr, vi, t, sg); break;
+        case 14: cform_sub<0, (1 << 1), tu_dz(1, 6), T>(vr, vi, t, sg); break;
+        case 15: cform_sub<0, (1 << 1), tu_dz(1, 7), T>(vr, vi, t, sg); break;
         default: break;
         }
         break;
     case 2:
         switch (ucase & 15u) {
-        case 0: cform_sub<0, (1 << 2), tu_dz(2, 0), T>(vr, vi, t); break;
-        case 1: cform_sub<0, (1 << 2), tu_dz(2, 1), T>(vr, vi, t); break;
-        case 2: cform_sub<0, (1 << 2), tu_dz(2, 2), T>(vr, vi, t); break;
-        case 3: cform_sub<0, (1 << 2), tu_dz(2, 3), T>(vr, vi, t); break;
-        case 4: cform_sub<0, (1 << 2), tu_dz(2, 4), T>(vr, vi, t); break;
-        case 5: cform_sub<0, (1 << 2), tu_dz(2, 5), T>(vr, vi, t); break;
-        case 6: cform_sub<0, (1 << 2), tu_dz(2, 6), T>(vr, vi, t); break;
-        case 7: cform_sub<0, (1 << 2), tu_dz(2, 7), T>(vr, vi, t); break;
-        case 8: cform_sub<0, (1 << 3), tu_dz(3, 0), T>(vr, vi, t); break;
-        case 9: cform_sub<0, (1 << 3), tu_dz(3, 1), T>(vr, vi, t); break;
-        case 10: cform_sub<0, (1 << 3), tu_dz(3, 2), T>(vr, vi, t); break;
-        case 11: cform_sub<0, (1 << 3), tu_dz(3, 3), T>(vr, vi, t); break;
-        case 12: cform_sub<0, (1 << 3), tu_dz(3, 4), T>(vr, vi, t); break;
-        case 13: cform_sub<0, (1 << 3), tu_dz(3, 5), T>(vr, vi, t); break;
-        case 14: cform_sub<0, (1 << 3), tu_dz(3, 6), T>(vr, vi, t); break;
-        case 15: cform_sub<0, (1 << 3), tu_dz(3, 7), T>(vr, vi, t); break;
+        case 0: cform_sub<0, (1 << 2), tu_dz(2, 0), T>(vr, vi, t, sg); break;
+        case 1: cform_sub<0, (1 << 2), tu_dz(2, 1), T>(vr, vi, t, sg); break;
+        case 2: cform_sub<0, (1 << 2), tu_dz(2, 2), T>(vr, vi, t, sg); break;
+        case 3: cform_sub<0, (1 << 2), tu_dz(2, 3), T>(vr, vi, t, sg); break;
+        case 4: cform_sub<0, (1 << 2), tu_dz(2, 4), T>(vr, vi, t, sg); break;
+        case 5: cform_sub<0, (1 << 2), tu_dz(2, 5), T>(vr, vi, t, sg); break;
+        case 6: cform_sub<0, (1 << 2), tu_dz(2, 6), T>(vr, vi, t, sg); break;
+        case 7: cform_sub<0, (1 << 2), tu_dz(2, 7), T>(vr, vi, t, sg); break;
+        case 8: cform_sub<0, (1 << 3), tu_dz(3, 0), T>(vr, vi, t, sg); break;
+        case 9: cform_sub<0, (1 << 3), tu_dz(3, 1), T>(vr, vi, t, sg); break;
+        case 10: cform_sub<0, (1 << 3), tu_dz(3, 2), T>(vr, vi, t, sg); break;
+        case 11: cform_sub<0, (1 << 3), tu_dz(3, 3), T>(vr, vi, t, sg); break;
+        case 12: cform_sub<0, (1 << 3), tu_dz(3, 4), T>(vr, vi, t, sg); break;
+        case 13: cform_sub<0, (1 << 3), tu_dz(3, 5), T>(vr, vi, t, sg); break;
+        case 14: cform_sub<0, (1 << 3), tu_dz(3, 6), T>(vr, vi, t, sg); break;
+        case 15: cform_sub<0, (1 << 3), tu_dz(3, 7), T>(vr, vi, t, sg); break;
         default: break;
         }
         break;
     case 3:
         switch (ucase & 15u) {
-        case 0: cform_sub<1, (1 << 0), tu_dz(0, 0), T>(vr, vi, t); break;
-        case 1: cform_sub<1, (1 << 0), tu_dz(0, 1), T>(vr, vi, t); break;
-        case 2: cform_sub<1, (1 << 0), tu_dz(0, 2), T>(vr, vi, t); break;
-        case 3: cform_sub<1, (1 << 0), tu_dz(0, 3), T>(vr, vi, t); break;
-        case 4: cform_sub<1, (1 << 0), tu_dz(0, 4), T>(vr, vi, t); break;
-        case 5: cform_sub<1, (1 << 0), tu_dz(0, 5), T>(vr, vi, t); break;
-        case 6: cform_sub<1, (1 << 0), tu_dz(0, 6), T>(vr, vi, t); break;
-        case 7: cform_sub<1, (1 << 0), tu_dz(0, 7), T>(vr, vi, t); break;
-        case 8: cform_sub<1, (1 << 1), tu_dz(1, 0), T>(vr, vi, t); break;
-        case 9: cform_sub<1, (1 << 1), tu_dz(1, 1), T>(vr, vi, t); break;
-        case 10: cform_sub<1, (1 << 1), tu_dz(1, 2), T>(vr, vi, t); break;
-        case 11: cform_sub<1, (1 << 1), tu_dz(1, 3), T>(vr, vi, t); break;
-        case 12: cform_sub<1, (1 << 1), tu_dz(1, 4), T>(vr, vi, t); break;
-        case 13: cform_sub<1, (1 << 1), tu_dz(1, 5), T>(vr, vi, t); break;
-        case 14: cform_sub<1, (1 << 1), tu_dz(1, 6), T>(vr, vi, t); break;
-        case 15: cform_sub<1, (1 << 1), tu_dz(1, 7), T>(vr, vi, t); break;
+        case 0: cform_sub<1, (1 << 0), tu_dz(0, 0), T>(vr, vi, t, sg); break;
+        case 1: cform_sub<1, (1 << 0), tu_dz(0, 1), T>(vr, vi, t, sg); break;
+        case 2: cform_sub<1, (1 << 0), tu_dz(0, 2), T>(vr, vi, t, sg); break;
+        case 3: cform_sub<1, (1 << 0), tu_dz(0, 3), T>(vr, vi, t, sg); break;
+        case 4: cform_sub<1, (1 << 0), tu_dz(0, 4), T>(vr, vi, t, sg); break;
+        case 5: cform_sub<1, (1 << 0), tu_dz(0, 5), T>(vr, vi, t, sg); break;
+        case 6: cform_sub<1, (1 << 0), tu_dz(0, 6), T>(vr, vi, t, sg); break;
+        case 7: cform_sub<1, (1 << 0), tu_dz(0, 7), T>(vr, vi, t, sg); break;
+        case 8: cform_sub<1, (1 << 1), tu_dz(1, 0), T>(vr, vi, t, sg); break;
+        case 9: cform_sub<1, (1 << 1), tu_dz(1, 1), T>(vr, vi, t, sg); break;
+        case 10: cform_sub<1, (1 << 1), tu_dz(1, 2), T>(vr, vi, t, sg); break;
+        case 11: cform_sub<1, (1 << 1), tu_dz(1, 3), T>(vr, vi, t, sg); break;
+        case 12: cform_sub<1, (1 << 1), tu_dz(1, 4), T>(vr, vi, t, sg); break;
+        case 13: cform_sub<1, (1 << 1), tu_dz(1, 5), T>(vr, vi, t, sg); break;
+        case 14: cform_sub<1, (1 << 1), tu_dz(1, 6), T>(vr, vi, t, sg); break;
+        case 15: cform_sub<1, (1 << 1), tu_dz(1, 7), T>(vr, vi, t, sg); break;
         default: break;
         }
         break;
     case 4:
         switch (ucase & 15u) {
-        case 0: cform_sub<1, (1 << 2), tu_dz(2, 0), T>(vr, vi, t); break;
-        case 1: cform_sub<1, (1 << 2), tu_dz(2, 1), T>(vr, vi, t); break;
-        case 2: cform_sub<1, (1 << 2), tu_dz(2, 2), T>(vr, vi, t); break;
-        case 3: cform_sub<1, (1 << 2), tu_dz(2, 3), T>(vr, vi, t); break;
-        case 4: cform_sub<1, (1 << 2), tu_dz(2, 4), T>(vr, vi, t); break;
-        case 5: cform_sub<1, (1 << 2), tu_dz(2, 5), T>(vr, vi, t); break;
-        case 6: cform_sub<1, (1 << 2), tu_dz(2, 6), T>(vr, vi, t); break;
-        case 7: cform_sub<1, (1 << 2), tu_dz(2, 7), T>(vr, vi, t); break;
-        case 8: cform_sub<1, (1 << 3), tu_dz(3, 0), T>(vr, vi, t); break;
-        case 9: cform_sub<1, (1 << 3), tu_dz(3, 1), T>(vr, vi, t); break;
-        case 10: cform_sub<1, (1 << 3), tu_dz(3, 2), T>(vr, vi, t); break;
-        case 11: cform_sub<1, (1 << 3), tu_dz(3, 3), T>(vr, vi, t); break;
-        case 12: cform_sub<1, (1 << 3), tu_dz(3, 4), T>(vr, vi, t); break;
-        case 13: cform_sub<1, (1 << 3), tu_dz(3, 5), T>(vr, vi, t); break;
-        case 14: cform_sub<1, (1 << 3), tu_dz(3, 6), T>(vr, vi, t); break;
-        case 15: cform_sub<1, (1 << 3), tu_dz(3, 7), T>(vr, vi, t); break;
+        case 0: cform_sub<1, (1 << 2), tu_dz(2, 0), T>(vr, vi, t, sg); break;
+        case 1: cform_sub<1, (1 << 2), tu_dz(2, 1), T>(vr, vi, t, sg); break;
+        case 2: cform_sub<1, (1 << 2), tu_dz(2, 2), T>(vr, vi, t, sg); break;
+        case 3: cform_sub<1, (1 << 2), tu_dz(2, 3), T>(vr, vi, t, sg); break;
+        case 4: cform_sub<1, (1 << 2), tu_dz(2, 4), T>(vr, vi, t, sg); break;
+        case 5: cform_sub<1, (1 << 2), tu_dz(2, 5), T>(vr, vi, t, sg); break;
+        case 6: cform_sub<1, (1 << 2), tu_dz(2, 6), T>(vr, vi, t, sg); break;
+        case 7: cform_sub<1, (1 << 2), tu_dz(2, 7), T>(vr, vi, t, sg); break;
+        case 8: cform_sub<1, (1 << 3), tu_dz(3, 0), T>(vr, vi, t, sg); break;
+        case 9: cform_sub<1, (1 << 3), tu_dz(3, 1), T>(vr, vi, t, sg); break;
+        case 10: cform_sub<1, (1 << 3), tu_dz(3, 2), T>(vr, vi, t, sg); break;
+        case 11: cform_sub<1, (1 << 3), tu_dz(3, 3), T>(vr, vi, t, sg); break;
+        case 12: cform_sub<1, (1 << 3), tu_dz(3, 4), T>(vr, vi, t, sg); break;
+        case 13: cform_sub<1, (1 << 3), tu_dz(3, 5), T>(vr, vi, t, sg); break;
+        case 14: cform_sub<1, (1 << 3), tu_dz(3, 6), T>(vr, vi, t, sg); break;
+        case 15: cform_sub<1, (1 << 3), tu_dz(3, 7), T>(vr, vi, t, sg); break;
         default: break;
         }
         break;
@@ -546,7 +615,7 @@ __device__ __forceinline__ void unit_dispatch(T (&vr)[kSubAmps], T (&vi)[kSubAmp
 }
 #else
 template <typename T>
-__device__ __forceinline__ void unit_dispatch(T (&vr)[kSubAmps], T (&vi)[kSubAmps], uint32_t ucase, T t) {
+__device__ __forceinline__ void unit_dispatch(T (&vr)[kSubAmps], T (&vi)[kSubAmps], uint32_t ucase, T t, T sg) {
     switch (ucase) {
         PS_UD(0) PS_UD(1) PS_UD(2) PS_UD(3) PS_UD(4) PS_UD(5) PS_UD(6) PS_UD(7)
         PS_UD(8) PS_UD(9) PS_UD(10) PS_UD(11) PS_UD(12) PS_UD(13) PS_UD(14) PS_UD(15)
@@ -575,23 +644,37 @@ __device__ __forceinline__ void sub_apply(T (&vr)[kSubAmps], T (&vi)[kSubAmps], 
     const DevTRot* tr = trots + rb;
     uint4 h = ldr<PARAM>(reinterpret_cast<const uint4*>(tr));
     double pn = ldr<PARAM>(&tr->p);
+#if PS_SHEAR
+    double sn = ldr<PARAM>(&tr->s);
+#else
+    constexpr double sn = 0.0;
+#endif
     for (int q = 0; q < nr; ++q) {
         const uint32_t code = h.x, zr = h.y;
         const uint64_t zt_c = ((uint64_t)h.w << 32) | h.z;
-        const double pc = pn;
+        const double pc = pn, sc = sn;
         if (q + 1 < nr) {
             const DevTRot* tn = trots + rb + q + 1;
             h = ldr<PARAM>(reinterpret_cast<const uint4*>(tn));
             pn = ldr<PARAM>(&tn->p);
+#if PS_SHEAR
+            sn = ldr<PARAM>(&tn->s);
+#endif
         }
         const int s0 = par32(zr & r) ^ par64(zt_c & i0);
         if (SPEC && (code & kTrUnit)) {
             // the thread-wide sign flips t once; the per-pair signs are static
-            unit_dispatch<T>(vr, vi, code & 0x7fu, flip((T)pc, s0));
+            unit_dispatch<T>(vr, vi, code & 0x7fu, flip((T)pc, s0), flip((T)sc, s0));
         } else {
             uint32_t Ms = (code >> 16) ^ (s0 ? 0xffffu : 0u);
             if (code & kTrNeg) Ms ^= 0xffffu;
             const uint32_t dx = (code >> 8) & 15u;
+#if PS_SHEAR
+            if (code & kTrUnit) {
+                shear_rotation<T>(vr, vi, dx, (code & kTrReal) ? 1 : 0, Ms, (T)pc, (T)sc);
+                continue;
+            }
+#endif
             switch (((code & kTrReal) ? 1u : 0u) | ((code & kTrSform) ? 2u : 0u)) {
             case 0: sub_rotation<0, 0, T>(vr, vi, dx, Ms, (T)pc); break;
             case 1: sub_rotation<1, 0, T>(vr, vi, dx, Ms, (T)pc); break;
@@ -1502,41 +1585,53 @@ __global__ void k_permute(T* __restrict__ a, uint64_t quarter, int b1, int b2) {
 }
 
 // NVLink P2P half swap: local region element e (row, col) <-> the partner's matching element.
-// Elements are enumerated as e = t (fb < 0) or e = t with bit fb of e forced to fv (one half of
-// the region, for the swap/compute overlap), t in [t0, t1).
+// Elements are enumerated as e = t with the filter bits (fmask, fval) inserted (fmask = 0: every
+// element; else one piece of the region, for the swap/compute overlap), t in [t0, t1).
 template <typename T>
-__global__ void k_p2p_swap(T* __restrict__ local, T* __restrict__ peer, uint64_t row_amps, uint64_t my_off,
-                           uint64_t peer_off, uint64_t t0, uint64_t t1, uint64_t fmask, uint64_t fval) {
+__device__ __forceinline__ void swap_index(uint64_t tq, uint64_t row_amps, uint64_t my_off, uint64_t peer_off,
+                                           uint64_t fmask, uint64_t fval, uint64_t& li, uint64_t& ri) {
+    uint64_t e = tq;
+    for (uint64_t m = fmask; m; m &= m - 1) {
+        const int b = __ffsll((long long)m) - 1;
+        e = insert0(e, b) | (fval & (1ull << b));
+    }
+    const uint64_t row = e / row_amps, col = e - row * row_amps;
+    li = row * 2 * row_amps + my_off + col;
+    ri = row * 2 * row_amps + peer_off + col;
+}
+
+// U elements in flight per thread (NVLink latency ~2 us).  The full-GPU form (512 threads, U = 8)
+// runs alone; the overlap form (128 threads, U = 4, <= 64 registers) fits next to the tile kernel's
+// two resident CTAs on every SM (their 2 x 256 x 112 registers leave 8192 = 128 x 64), so the swap
+// really runs while the pass runs instead of waiting for whole SMs to drain.
+template <typename T, int U, int THREADS, int MINB>
+__global__ void __launch_bounds__(THREADS, MINB)
+k_p2p_swap(T* __restrict__ local, T* __restrict__ peer, uint64_t row_amps, uint64_t my_off,
+           uint64_t peer_off, uint64_t t0, uint64_t t1, uint64_t fmask, uint64_t fval) {
     using V2 = typename SmemAmp<T>::V;
-    constexpr int U = 8;  // elements in flight per thread (NVLink latency ~2 us)
     V2* L = reinterpret_cast<V2*>(local);
     V2* R = reinterpret_cast<V2*>(peer);
-    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    for (uint64_t t = t0 + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < t1; t += U * stride) {
-        uint64_t li[U], ri[U];
+    const uint64_t stride = (uint64_t)gridDim.x * THREADS;
+    for (uint64_t t = t0 + (uint64_t)blockIdx.x * THREADS + threadIdx.x; t < t1; t += U * stride) {
         V2 u[U], v[U];
 #pragma unroll
         for (int q = 0; q < U; ++q) {
             const uint64_t tq = t + (uint64_t)q * stride;
-            // element index: tq with the filter bits (fmask, fval) inserted, lowest first
-            uint64_t e = tq;
-            for (uint64_t m = fmask; m; m &= m - 1) {
-                const int b = __ffsll((long long)m) - 1;
-                e = insert0(e, b) | (fval & (1ull << b));
-            }
-            const uint64_t row = e / row_amps, col = e - row * row_amps;
-            li[q] = row * 2 * row_amps + my_off + col;
-            ri[q] = row * 2 * row_amps + peer_off + col;
             if (tq < t1) {
-                u[q] = L[li[q]];
-                v[q] = __ldcv(&R[ri[q]]);
+                uint64_t li, ri;
+                swap_index<T>(tq, row_amps, my_off, peer_off, fmask, fval, li, ri);
+                u[q] = L[li];
+                v[q] = __ldcv(&R[ri]);
             }
         }
 #pragma unroll
         for (int q = 0; q < U; ++q) {
-            if (t + (uint64_t)q * stride < t1) {
-                L[li[q]] = v[q];
-                __stcg(&R[ri[q]], u[q]);
+            const uint64_t tq = t + (uint64_t)q * stride;
+            if (tq < t1) {
+                uint64_t li, ri;
+                swap_index<T>(tq, row_amps, my_off, peer_off, fmask, fval, li, ri);
+                L[li] = v[q];
+                __stcg(&R[ri], u[q]);
             }
         }
     }
@@ -2014,11 +2109,25 @@ cudaError_t launch_p2p_swap(int dtype, void* local, void* peer, uint64_t rows, u
                             int ctas) {
     (void)rows;
     if (t1 <= t0) return cudaSuccess;
-    const unsigned grid = ctas > 0 ? (unsigned)ctas : (unsigned)num_sms();
-    if (dtype == PS_C128)
-        k_p2p_swap<double><<<grid, 512, 0, s>>>((double*)local, (double*)peer, row_amps, my_off, peer_off, t0, t1, fmask, fval);
-    else
-        k_p2p_swap<float><<<grid, 512, 0, s>>>((float*)local, (float*)peer, row_amps, my_off, peer_off, t0, t1, fmask, fval);
+    // ctas > 0: that many full-size CTAs; 0: one full-size CTA per SM; < 0: the overlap form,
+    // -ctas CTAs (-1: one per SM)
+    if (ctas >= 0) {
+        const unsigned grid = ctas > 0 ? (unsigned)ctas : (unsigned)num_sms();
+        if (dtype == PS_C128)
+            k_p2p_swap<double, 8, 512, 1><<<grid, 512, 0, s>>>((double*)local, (double*)peer, row_amps, my_off,
+                                                                peer_off, t0, t1, fmask, fval);
+        else
+            k_p2p_swap<float, 8, 512, 1><<<grid, 512, 0, s>>>((float*)local, (float*)peer, row_amps, my_off, peer_off,
+                                                               t0, t1, fmask, fval);
+    } else {
+        const unsigned grid = ctas == -1 ? (unsigned)num_sms() : (unsigned)(-ctas);
+        if (dtype == PS_C128)
+            k_p2p_swap<double, 4, 128, 8><<<grid, 128, 0, s>>>((double*)local, (double*)peer, row_amps, my_off,
+                                                                peer_off, t0, t1, fmask, fval);
+        else
+            k_p2p_swap<float, 4, 128, 8><<<grid, 128, 0, s>>>((float*)local, (float*)peer, row_amps, my_off, peer_off,
+                                                               t0, t1, fmask, fval);
+    }
     return cudaGetLastError();
 }
 

@@ -260,6 +260,24 @@ static void make_subgroups(const std::vector<LocalRot>& lr, int k, int phase_bit
                     tr.code |= kTrUnit | (uint32_t)tu_case(real, dx ? __builtin_ctz(dx) : -1, (int)dz);
                 tr.p = ph * (s0 / c);
                 tr.s = 0.0;
+#if PS_SHEAR
+                if (tr.code & kTrUnit) {
+                    // the pair update c * [[1, -t], [t, 1]] is the exact rotation by theta with
+                    // cos theta = c, sin theta = ph * s0: three shears, no deferred factor;
+                    // |theta| > pi/2 runs as -R(theta -+ pi) (the -1 joins F)
+                    const double sg = ph * s0;
+                    if (c >= 0.0) {
+                        tr.p = sg / (1.0 + c);
+                        tr.s = sg;
+                    } else {
+                        tr.p = -sg / (1.0 - c);
+                        tr.s = -sg;
+                        F = -F;
+                    }
+                    plan->trots.push_back(tr);
+                    continue;
+                }
+#endif
                 F *= c;
             } else {
                 // SFORM: keeps phi = pi/2 exact (R8)

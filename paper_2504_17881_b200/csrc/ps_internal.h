@@ -50,6 +50,9 @@ static_assert(sizeof(DevRot) == 48, "DevRot layout");
 // sub-groups while it stays within [2^-40, 2^40]).  CFORM's per-pair sign pattern parity(Dz & d)
 // is a compile-time case of the kernel's switch (code bits 0-8), so its pairs carry no sign
 // flips; only the thread-wide sign (the representative's parity) flips t once per rotation.
+#ifndef PS_SHEAR
+#define PS_SHEAR 0  // 1: unit-case CFORM rotations as three in-place shears (DevTRot p = tau, s = sin)
+#endif
 #ifndef PS_SUBDIM
 #define PS_SUBDIM 4
 #endif
@@ -98,8 +101,9 @@ struct DevTRot {
     uint32_t code;
     uint32_t zr;   // tile-local phase mask (parity with the coset representative r)
     uint64_t zt;   // phase mask on the tile-enumeration bits (parity with the tile base i0)
-    double p;      // CFORM: t (B/f = +-t or +-i t); SFORM: t = cos/f (B/f = +-1 or +-i)
-    double s;      // unused (keeps the record 32 B)
+    double p;      // CFORM: t (B/f = +-t or +-i t); SFORM: t = cos/f (B/f = +-1 or +-i);
+                   // PS_SHEAR unit case: tau = tan(theta / 2) of the exact rotation (no factor)
+    double s;      // PS_SHEAR unit case: sin(theta); otherwise unused (keeps the record 32 B)
 };
 static_assert(sizeof(DevTRot) == 32, "DevTRot layout");
 
