@@ -369,7 +369,8 @@ def test_rpe_eigenstate_signal():
 def test_option_validation_and_restore():
     with P.State(10, "c128") as st:
         for opt, bad in ((ps.OPT_FUSION, 5), (ps.OPT_TILE_BITS, 14), (ps.OPT_TILE_BITS, 3), (ps.OPT_CHUNK_BYTES, 1000),
-                         (ps.OPT_MAX_PASS_ROTS, 0), (ps.OPT_TILE_TMA, 7), (ps.OPT_LAYOUT, 3), (ps.OPT_SPECIALIZE, 3), (99, 1)):
+                         (ps.OPT_MAX_PASS_ROTS, 0), (ps.OPT_TILE_TMA, 7), (ps.OPT_LAYOUT, 3), (ps.OPT_SPECIALIZE, 3), (ps.OPT_OVERLAP, 3),
+                         (ps.OPT_OVERLAP, 5 << 16), (ps.OPT_SWAP_CTAS, 1 << 20), (99, 1)):
             with pytest.raises(P.PsError) as ei:
                 st.set_option(opt, bad)
             assert ei.value.code == -1
