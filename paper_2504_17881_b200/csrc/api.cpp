@@ -49,6 +49,7 @@ cudaError_t launch_permute(int dtype, void* a, int nl, int b1, int b2, cudaStrea
 cudaError_t launch_butterfly(int dtype, void* A, void* B, uint64_t n, int wr, int wi, cudaStream_t s);
 cudaError_t launch_recombine(int dtype, void* A, const void* B, uint64_t n, cudaStream_t s);
 cudaError_t launch_p2p_copy(int dtype, void* dst, const void* src, uint64_t n, cudaStream_t s);
+cudaError_t launch_pair_barrier(const uint32_t* mine, uint32_t* theirs, uint32_t epoch, cudaStream_t s);
 cudaError_t launch_p2p_swap(int dtype, void* local, void* peer, uint64_t rows, uint64_t row_amps, uint64_t my_off,
                             uint64_t peer_off, uint64_t t0, uint64_t t1, uint64_t fmask, uint64_t fval,
                             cudaStream_t s, int ctas);
@@ -116,6 +117,10 @@ struct ps_state {
     size_t flags_cap = 0;
     std::vector<uint32_t*> peer_flags;
     uint32_t epoch = 0;
+    // pairwise P2P barriers (overlapped swaps): words [flag_words + src * kBarSlots + slot] of a
+    // rank's d_flags are raised by rank src; bar_epoch[partner * kBarSlots + slot] counts the uses
+    static constexpr int kBarSlots = 4;
+    std::vector<uint32_t> bar_epoch;
     int fused = 0;  // off by default: measured slower than swap + overlap (profiles/r02/multi_gpu.md)
     void* d_mirror = nullptr;  // PS_OPT_LAYOUT=2 mirror buffer B_k
     cudaStream_t xstream = nullptr;  // second stream: swaps overlapped with the next pass
@@ -321,6 +326,7 @@ static bool ipc_export(void* ptr, cudaIpcMemHandle_t* handle, uint64_t* offset) 
 // handshake flags of the fused exchange + tile pass: one 32-bit word per tile of the smallest
 // tiles a pass can have (2^4 amplitudes), so every pass's tile index has a word
 static size_t flag_words(const ps_state* h) { return (size_t)1 << std::max(0, h->nl - 4); }
+static size_t bar_words(const ps_state* h) { return (size_t)h->world * ps_state::kBarSlots; }
 
 static void setup_p2p(ps_state* h) {
     h->p2p = false;
@@ -457,10 +463,12 @@ static int make_state(int n_qubits, int dtype, void* dev_buf, size_t bytes, void
     for (int q = 0; q < n_qubits; ++q) h->perm[q] = q;
     if (world > 1) {
         // handshake flags of the fused exchange + tile pass (0 = no epoch raised yet)
-        if ((e = cudaMalloc(&h->d_flags, sizeof(uint32_t) * flag_words(h))) != cudaSuccess)
+        if ((e = cudaMalloc(&h->d_flags, sizeof(uint32_t) * (flag_words(h) + bar_words(h)))) != cudaSuccess)
             return bail(PS_ENOMEM, std::string("flags: ") + cudaGetErrorString(e));
         h->flags_cap = flag_words(h);
-        if ((e = cudaMemsetAsync(h->d_flags, 0, sizeof(uint32_t) * h->flags_cap, h->stream)) != cudaSuccess)
+        h->bar_epoch.assign(bar_words(h), 0);
+        if ((e = cudaMemsetAsync(h->d_flags, 0, sizeof(uint32_t) * (h->flags_cap + bar_words(h)), h->stream)) !=
+            cudaSuccess)
             return bail(PS_ECUDA, std::string("flags: ") + cudaGetErrorString(e));
     }
     if (world > 1 && !emulated) {
@@ -700,6 +708,19 @@ static int barrier(ps_state* h) {
 static int barrier_on(ps_state* h, cudaStream_t st, int slot) {
     if (h->emulated || h->world == 1) return PS_OK;
     NCCL_TRY(h, ncclAllReduce(h->d_barrier + slot, h->d_barrier + slot, 1, ncclInt32, ncclSum, h->comm, st));
+    return PS_OK;
+}
+
+// pairwise barrier with `partner` on stream st (P2P flags; NCCL barrier without peer access)
+static int pair_barrier(ps_state* h, cudaStream_t st, int partner, int slot) {
+    if (h->emulated || h->world == 1) return PS_OK;
+    if (!h->p2p || !h->peer_flags[partner]) return barrier_on(h, st, slot);
+    uint32_t& ep = h->bar_epoch[(size_t)partner * ps_state::kBarSlots + slot];
+    ep += 1;
+    const size_t fw = flag_words(h);
+    CUDA_TRY(h, launch_pair_barrier(h->d_flags + fw + (size_t)partner * ps_state::kBarSlots + slot,
+                                    h->peer_flags[partner] + fw + (size_t)h->rank * ps_state::kBarSlots + slot, ep,
+                                    st));
     return PS_OK;
 }
 
@@ -1003,7 +1024,7 @@ static int exchange_overlap(ps_state* h, const Pass& ex, const Pass& np) {
         Timed t(h, PS_K_EXCHANGE, h->xstream);
         for (int j = first; j < P; ++j) {
             CUDA_TRY(h, swap_piece(j, h->xstream, h->swap_ctas));
-            rc = barrier_on(h, h->xstream, 1);
+            rc = pair_barrier(h, h->xstream, partner, 1);
             if (rc) return rc;
             CUDA_TRY(h, cudaEventRecord(h->xev[1 + j], h->xstream));
         }
@@ -1097,10 +1118,10 @@ static int exchange_overlap3(ps_state* h, const Pass& pa, const Pass& ex, const 
         Timed t(h, PS_K_EXCHANGE, h->xstream);
         for (int j = 0; j < P; ++j) {
             CUDA_TRY(h, cudaStreamWaitEvent(h->xstream, h->xev[1 + j], 0));
-            if ((rc = barrier_on(h, h->xstream, 1))) return rc;  // both ranks finished piece j
+            if ((rc = pair_barrier(h, h->xstream, partner, 1))) return rc;  // both ranks finished piece j
             CUDA_TRY(h, launch_p2p_swap(h->dtype, h->d_state, h->peers[partner], rows, row_amps, my_off, peer_off, t0,
                                         t1, emask, deposit((uint64_t)j, emask), h->xstream, h->swap_ctas));
-            if ((rc = barrier_on(h, h->xstream, 2))) return rc;  // both halves of piece j landed
+            if ((rc = pair_barrier(h, h->xstream, partner, 2))) return rc;  // both halves of piece j landed
             CUDA_TRY(h, cudaEventRecord(h->xev[1 + P + j], h->xstream));
         }
     }

@@ -1640,6 +1640,28 @@ k_p2p_swap(T* __restrict__ local, T* __restrict__ peer, uint64_t row_amps, uint6
     __threadfence_system();
 }
 
+// pairwise barrier between two ranks over peer memory (the overlapped swap's "both ranks finished
+// piece j" / "both halves landed" points): one thread raises the partner's word to `epoch` (system-
+// scope release, after this stream's earlier kernels completed) and spins until its own word from
+// the partner reaches `epoch` (acquire).  One warp with a few registers: it fits on an SM next to the
+// tile kernel's resident CTAs, where an NCCL collective kernel would wait for a whole SM to drain.
+// A partner that never arrives traps after ~60 s instead of hanging the GPU.
+__global__ void k_pair_barrier(const uint32_t* mine, uint32_t* theirs, uint32_t epoch) {
+    if (threadIdx.x != 0) return;
+    flag_release(theirs, epoch);
+    uint64_t t0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    uint32_t spins = 0;
+    while ((int32_t)(flag_acquire(mine) - epoch) < 0) {
+        __nanosleep(256);
+        if ((++spins & 1023u) == 0) {
+            uint64_t t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            if (t - t0 > 60ull * 1000000000ull) __trap();
+        }
+    }
+}
+
 // Eq. (core_state) helpers (PS_OPT_LAYOUT=2)
 // butterfly: b = w B (w = conj(w_k) in {+-1, +-i}); A <- (A + b)/sqrt2, B <- (A - b)/sqrt2
 template <typename T>
@@ -2128,6 +2150,11 @@ cudaError_t launch_p2p_swap(int dtype, void* local, void* peer, uint64_t rows, u
             k_p2p_swap<float, 4, 128, 8><<<grid, 128, 0, s>>>((float*)local, (float*)peer, row_amps, my_off, peer_off,
                                                                t0, t1, fmask, fval);
     }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_pair_barrier(const uint32_t* mine, uint32_t* theirs, uint32_t epoch, cudaStream_t s) {
+    k_pair_barrier<<<1, 32, 0, s>>>(mine, theirs, epoch);
     return cudaGetLastError();
 }
 
