@@ -125,7 +125,7 @@ struct ps_state {
     void* d_mirror = nullptr;  // PS_OPT_LAYOUT=2 mirror buffer B_k
     cudaStream_t xstream = nullptr;  // second stream: swaps overlapped with the next pass
     static constexpr int kMaxPieceBits = 3;
-    static constexpr int kXev = 2 + (1 << kMaxPieceBits);
+    static constexpr int kXev = 2 + 2 * (1 << kMaxPieceBits);  // overlap mode 2 uses 1 + 2P events
     cudaEvent_t xev[kXev] = {};
     int overlap = 1;
     int swap_ctas = -1;   // overlapped swap pieces: < 0 the slim kernel that co-resides with the
@@ -1076,12 +1076,12 @@ static int exchange_overlap3(ps_state* h, const Pass& pa, const Pass& ex, const 
     const uint64_t sb = split_bits2(pa, np, ex.ell);
     uint64_t pbits = 0;
     int B = 0;
-    for (int b = 63; b >= 0 && B < std::min(h->piece_bits, 2); --b)
+    for (int b = 63; b >= 0 && B < std::min(h->piece_bits, (int)ps_state::kMaxPieceBits); --b)
         if ((sb >> b) & 1) {
             pbits |= 1ull << b;
             ++B;
         }
-    const int P = 1 << B;  // <= 4: events xev[1..P] (previous pass) and xev[1+P..2P] (swap)
+    const int P = 1 << B;  // <= 8: events xev[1..P] (previous pass) and xev[1+P..2P] (swap)
     auto elem_bits = [&](uint64_t m) {
         uint64_t r = 0;
         for (; m; m &= m - 1) {
