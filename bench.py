@@ -58,8 +58,8 @@ def parse():
     ap.add_argument("--tile-tune", type=int, default=-1)
     ap.add_argument("--layout", type=int, default=1, help="world > 1: 1 lazy qubit swaps, 0 runs + swap-back")
     ap.add_argument("--transport", type=int, default=1, help="world > 1: 1 NVLink P2P, 0 NCCL send/recv")
-    ap.add_argument("--overlap", type=int, default=1, help="world > 1: overlap swaps with the next pass (2: and the previous one)")
-    ap.add_argument("--swap-ctas", type=int, default=0, help="overlapped swap pieces: 0 slim kernel, one CTA per SM; -k slim; k full-size")
+    ap.add_argument("--overlap", type=int, default=2, help="world > 1: overlap swaps with the next pass (2: and the previous one)")
+    ap.add_argument("--swap-ctas", type=int, default=0, help="overlapped swap pieces: 0 default (slim kernel, 2 per SM); -k slim (per SM if k <= 8); k full-size")
     ap.add_argument("--specialize", type=int, default=-1,
                     help="tile-kernel variant: -1 library default (fp64 2, fp32 0), 0 generic, 2 unit-dx specialised, "
                          "1 planner's per-pass choice")

@@ -127,10 +127,12 @@ enum {
                                  recombine -- kept for A/B */
     PS_OPT_TRANSPORT = 10,    /* world > 1: 1 = NVLink P2P swap kernel on CUDA-IPC peer pointers when
                                  available (default); 0 = NCCL send/recv with staging */
-    PS_OPT_OVERLAP = 11,      /* world > 1, P2P: 1 = overlap each swap with the following tile pass
-                                 on a second stream (default); 2 = also with the tile pass before it
-                                 (both split into pieces; a piece is swapped as soon as both ranks
-                                 finished it); 0 = serialise; bits 16-18 = piece bits + 1 */
+    PS_OPT_OVERLAP = 11,      /* world > 1, P2P: 2 = each swap overlaps the tile passes before and
+                                 after it (default): both passes run in 2^B pieces split by free
+                                 bits outside their tiles, a piece is swapped as soon as both ranks
+                                 finished it (pairwise P2P flag barrier) and the next pass's piece
+                                 runs as soon as it landed; 1 = only with the pass after it;
+                                 0 = serialise; bits 16-18 = B + 1 (default B = 2) */
     PS_OPT_SPECIALIZE = 12    /* tile-kernel variant: 2 = specialised (default for C128): CFORM
                                  rotations whose sub-group xor mask dx is a unit vector or 0 run
                                  through one of 80 compile-time cases (per-pair signs and pairing
@@ -148,10 +150,11 @@ enum {
                                  0 = swap, then the pass, overlapped on two streams (default: the
                                  fused kernel measured slower, profiles/r02/multi_gpu.md)
                                   */,
-    PS_OPT_SWAP_CTAS = 15     /* overlapped swap pieces (PS_OPT_OVERLAP): 0 = the slim swap kernel
-                                 (128 threads, <= 64 registers) with one CTA per SM, which fits next
-                                 to the tile kernel's resident CTAs (default); -k = k slim CTAs;
-                                 k > 0 = k full-size CTAs (512 threads: they wait for whole SMs) */
+    PS_OPT_SWAP_CTAS = 15     /* overlapped swap pieces: the slim swap kernel (128 threads, <= 64
+                                 registers, fits next to the tile kernel's resident CTAs) with
+                                 -k CTAs per SM for -8 <= -k < 0 or k CTAs for -k < -8; 0 = default
+                                 (2 per SM); k > 0 = k full-size CTAs (512 threads: wait for whole
+                                 SMs) */
 };
 
 /* ------------------------------------------------------------------------------------------ */

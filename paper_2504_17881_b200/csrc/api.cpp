@@ -127,9 +127,9 @@ struct ps_state {
     static constexpr int kMaxPieceBits = 3;
     static constexpr int kXev = 2 + 2 * (1 << kMaxPieceBits);  // overlap mode 2 uses 1 + 2P events
     cudaEvent_t xev[kXev] = {};
-    int overlap = 1;
-    int swap_ctas = -1;   // overlapped swap pieces: < 0 the slim kernel that co-resides with the
-                          // tile kernel (-1: one CTA per SM), > 0 that many full-size CTAs
+    int overlap = 2;      // PS_OPT_OVERLAP (2: the swap overlaps the passes before and after it)
+    int swap_ctas = -2;   // overlapped swap pieces: < 0 the slim kernel that co-resides with the
+                          // tile kernel (-k: k per SM if k <= 8, else k CTAs), > 0 full-size CTAs
     int piece_bits = 2;   // an overlapped swap/pass pair runs in up to 2^piece_bits pieces
     const Plan* cur_plan = nullptr;  // the plan being executed (host copies of its records)
     int layout = 1, transport = 1;
@@ -663,7 +663,7 @@ static int set_option_rank(ps_state* h, int option, int64_t value) {
         if (pb) h->piece_bits = pb - 1;
         break;
     }
-    case PS_OPT_SWAP_CTAS: h->swap_ctas = value == 0 ? -1 : (int)value; break;
+    case PS_OPT_SWAP_CTAS: h->swap_ctas = value == 0 ? -2 : (int)value; break;
     case PS_OPT_CHUNK_BITS: h->chunk_bits = (int)value; break;
     case PS_OPT_SPECIALIZE: h->specialize = (int)value; break;
     case PS_OPT_GRID_CAP: h->grid_cap = (int)value; break;

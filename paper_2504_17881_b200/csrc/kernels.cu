@@ -2132,7 +2132,7 @@ cudaError_t launch_p2p_swap(int dtype, void* local, void* peer, uint64_t rows, u
     (void)rows;
     if (t1 <= t0) return cudaSuccess;
     // ctas > 0: that many full-size CTAs; 0: one full-size CTA per SM; < 0: the overlap form,
-    // -ctas CTAs (-1: one per SM)
+    // -ctas CTAs per SM if -ctas <= 8, else -ctas CTAs
     if (ctas >= 0) {
         const unsigned grid = ctas > 0 ? (unsigned)ctas : (unsigned)num_sms();
         if (dtype == PS_C128)
@@ -2142,7 +2142,7 @@ cudaError_t launch_p2p_swap(int dtype, void* local, void* peer, uint64_t rows, u
             k_p2p_swap<float, 8, 512, 1><<<grid, 512, 0, s>>>((float*)local, (float*)peer, row_amps, my_off, peer_off,
                                                                t0, t1, fmask, fval);
     } else {
-        const unsigned grid = ctas == -1 ? (unsigned)num_sms() : (unsigned)(-ctas);
+        const unsigned grid = -ctas <= 8 ? (unsigned)(-ctas * num_sms()) : (unsigned)(-ctas);
         if (dtype == PS_C128)
             k_p2p_swap<double, 4, 128, 8><<<grid, 128, 0, s>>>((double*)local, (double*)peer, row_amps, my_off,
                                                                 peer_off, t0, t1, fmask, fval);
