@@ -59,6 +59,7 @@ def parse():
     ap.add_argument("--layout", type=int, default=1, help="world > 1: 1 lazy qubit swaps, 0 runs + swap-back")
     ap.add_argument("--transport", type=int, default=1, help="world > 1: 1 NVLink P2P, 0 NCCL send/recv")
     ap.add_argument("--overlap", type=int, default=2, help="world > 1: overlap swaps with the next pass (2: and the previous one)")
+    ap.add_argument("--swap-tma", type=int, default=1, help="overlapped swap pieces through the TMA swap kernel (1) or the register kernel (0)")
     ap.add_argument("--swap-ctas", type=int, default=0, help="overlapped swap pieces: 0 default (slim kernel, 2 per SM); -k slim (per SM if k <= 8); k full-size")
     ap.add_argument("--specialize", type=int, default=-1,
                     help="tile-kernel variant: -1 library default (fp64 2, fp32 0), 0 generic, 2 unit-dx specialised, "
@@ -424,6 +425,7 @@ def run_ours(args):
     st.set_option(ps.OPT_TRANSPORT, args.transport)
     st.set_option(ps.OPT_OVERLAP, args.overlap)
     st.set_option(ps.OPT_SWAP_CTAS, args.swap_ctas)
+    st.set_option(ps.OPT_SWAP_TMA, args.swap_tma)
     if args.specialize >= 0:
         st.set_option(ps.OPT_SPECIALIZE, args.specialize)
     st.set_option(ps.OPT_FUSED_EXCHANGE, args.fused)
@@ -521,7 +523,7 @@ def run_ours(args):
             "data": "synthetic",
             "config": {"workload": workload_name(args), "n_qubits": args.n, "rotations_per_step": rot_per_step,
                        "fusion": args.fusion, "tile_mode": args.tile_mode, "tile_bits": args.tile_bits or (12 if args.dtype == "c128" else 11),
-                       "layout": args.layout, "transport": args.transport, "overlap": args.overlap, "swap_ctas": args.swap_ctas, "specialize": args.specialize if args.specialize >= 0 else (2 if args.dtype == "c128" else 0),
+                       "layout": args.layout, "transport": args.transport, "overlap": args.overlap, "swap_ctas": args.swap_ctas, "swap_tma": args.swap_tma, "specialize": args.specialize if args.specialize >= 0 else (2 if args.dtype == "c128" else 0),
                        "parallelism": (f"state sharded over {args.emulate} virtual ranks on 1 GPU (emulation)"
                                        if args.emulate else f"state sharded over {world} GPU(s) by top qubits"),
                        "fused_exchange": args.fused, "group": args.group if args.kind == "SUFFIX" else None,

@@ -154,7 +154,12 @@ enum {
                                  registers, fits next to the tile kernel's resident CTAs) with
                                  -k CTAs per SM for -8 <= -k < 0 or k CTAs for -k < -8; 0 = default
                                  (2 per SM); k > 0 = k full-size CTAs (512 threads: wait for whole
-                                 SMs) */
+                                 SMs) */,
+    PS_OPT_SWAP_TMA = 16      /* overlapped swap pieces: 1 = the TMA swap kernel (one thread per CTA
+                                 moves 4 KB chunks through a 4-stage shared-memory ring with
+                                 cp.async.bulk loads of the partner's and its own chunk and crosswise
+                                 bulk stores; default) where the piece's contiguous runs are >= 1 KB,
+                                 else the slim register kernel; 0 = always the register kernel */
 };
 
 /* ------------------------------------------------------------------------------------------ */

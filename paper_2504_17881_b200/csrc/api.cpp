@@ -52,7 +52,7 @@ cudaError_t launch_p2p_copy(int dtype, void* dst, const void* src, uint64_t n, c
 cudaError_t launch_pair_barrier(const uint32_t* mine, uint32_t* theirs, uint32_t epoch, cudaStream_t s);
 cudaError_t launch_p2p_swap(int dtype, void* local, void* peer, uint64_t rows, uint64_t row_amps, uint64_t my_off,
                             uint64_t peer_off, uint64_t t0, uint64_t t1, uint64_t fmask, uint64_t fval,
-                            cudaStream_t s, int ctas);
+                            cudaStream_t s, int ctas, int tma_chunk = 0);
 cudaError_t launch_xtile(int dtype, const XTileRank* ranks, int nranks, const Pass& p, const uint64_t* d_offs,
                          const uint64_t* h_offs, int ell, uint32_t epoch, cudaStream_t s, int grid_cap);
 
@@ -128,6 +128,7 @@ struct ps_state {
     static constexpr int kXev = 2 + 2 * (1 << kMaxPieceBits);  // overlap mode 2 uses 1 + 2P events
     cudaEvent_t xev[kXev] = {};
     int overlap = 2;      // PS_OPT_OVERLAP (2: the swap overlaps the passes before and after it)
+    int swap_tma = 1;     // PS_OPT_SWAP_TMA: overlapped swap pieces through the TMA swap kernel
     int swap_ctas = -2;   // overlapped swap pieces: < 0 the slim kernel that co-resides with the
                           // tile kernel (-k: k per SM if k <= 8, else k CTAs), > 0 full-size CTAs
     int piece_bits = 2;   // an overlapped swap/pass pair runs in up to 2^piece_bits pieces
@@ -622,6 +623,7 @@ static int check_option(const ps_state* h, int option, int64_t value) {
         if ((value & 0xffff) > 2) return fail(PS_EINVAL, "overlap mode must be 0, 1 or 2");
         return (((value >> 16) & 7) > ps_state::kMaxPieceBits + 1) ? fail(PS_EINVAL, "overlap piece bits must be <= 3")
                                                                     : PS_OK;
+    case PS_OPT_SWAP_TMA: return PS_OK;
     case PS_OPT_SWAP_CTAS:
         return (value < -(1 << 16) || value > (1 << 16)) ? fail(PS_EINVAL, "swap CTAs must be in [-65536, 65536]")
                                                          : PS_OK;
@@ -664,6 +666,7 @@ static int set_option_rank(ps_state* h, int option, int64_t value) {
         break;
     }
     case PS_OPT_SWAP_CTAS: h->swap_ctas = value == 0 ? -2 : (int)value; break;
+    case PS_OPT_SWAP_TMA: h->swap_tma = value ? 1 : 0; break;
     case PS_OPT_CHUNK_BITS: h->chunk_bits = (int)value; break;
     case PS_OPT_SPECIALIZE: h->specialize = (int)value; break;
     case PS_OPT_GRID_CAP: h->grid_cap = (int)value; break;
@@ -943,6 +946,19 @@ static int exchange_half(ps_state* h, const Pass& p) {
     return PS_OK;
 }
 
+// contiguous elements per chunk of the TMA swap kernel for a piece of E(gx, ell) enumerated with
+// element filter mask emask (runs end at a region row or at the lowest filter bit); 0 = use the
+// register kernel (runs shorter than 1 KB, or the TMA form switched off)
+static int swap_tma_chunk(const ps_state* h, uint64_t row_amps, uint64_t emask, uint64_t t0, uint64_t t1) {
+    if (!h->swap_tma || t1 <= t0) return 0;
+    uint64_t run = row_amps;
+    if (emask) run = std::min<uint64_t>(run, 1ull << __builtin_ctzll(emask));
+    uint64_t c = std::min<uint64_t>(4096 / h->amp_bytes, run);
+    c = std::min<uint64_t>(c, t1 - t0);
+    while (c > 1 && ((t1 - t0) % c || t0 % c)) c >>= 1;
+    return c * h->amp_bytes >= 1024 ? (int)c : 0;
+}
+
 // a bit that splits the next pass's tiles into two halves whose elements all have that bit
 // fixed: a free (tile-enumeration) bit in which no two elements of one tile differ
 static uint64_t split_bits(const Pass& np) { return np.free_mask & ~np.touch_mask; }
@@ -994,7 +1010,8 @@ static int exchange_overlap(ps_state* h, const Pass& ex, const Pass& np) {
     const uint64_t t0 = ex.keep ? piece / 2 : 0, t1 = ex.keep ? piece : piece / 2;
     auto swap_piece = [&](int j, cudaStream_t st, int ctas) {
         return launch_p2p_swap(h->dtype, h->d_state, h->peers[partner], rows, row_amps, my_off, peer_off, t0, t1,
-                               emask, deposit((uint64_t)j, emask), st, ctas);
+                               emask, deposit((uint64_t)j, emask), st, ctas,
+                               ctas < 0 ? swap_tma_chunk(h, row_amps, emask, t0, t1) : 0);
     };
     auto run_pass = [&](uint64_t fixed_mask, uint64_t fixed_val) -> int {
         Pass q = np;
@@ -1120,7 +1137,8 @@ static int exchange_overlap3(ps_state* h, const Pass& pa, const Pass& ex, const 
             CUDA_TRY(h, cudaStreamWaitEvent(h->xstream, h->xev[1 + j], 0));
             if ((rc = pair_barrier(h, h->xstream, partner, 1))) return rc;  // both ranks finished piece j
             CUDA_TRY(h, launch_p2p_swap(h->dtype, h->d_state, h->peers[partner], rows, row_amps, my_off, peer_off, t0,
-                                        t1, emask, deposit((uint64_t)j, emask), h->xstream, h->swap_ctas));
+                                        t1, emask, deposit((uint64_t)j, emask), h->xstream, h->swap_ctas,
+                                        h->swap_ctas < 0 ? swap_tma_chunk(h, row_amps, emask, t0, t1) : 0));
             if ((rc = pair_barrier(h, h->xstream, partner, 2))) return rc;  // both halves of piece j landed
             CUDA_TRY(h, cudaEventRecord(h->xev[1 + P + j], h->xstream));
         }

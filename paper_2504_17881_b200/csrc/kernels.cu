@@ -1640,6 +1640,83 @@ k_p2p_swap(T* __restrict__ local, T* __restrict__ peer, uint64_t row_amps, uint6
     __threadfence_system();
 }
 
+// TMA form of the overlapped swap: one warp per CTA, lane 0 moves chunks of `chunk_amps`
+// contiguous elements (a run inside one region row and one piece) through a kSwapStages ring of
+// shared memory: bulk-load the partner's chunk and the own chunk (cp.async.bulk, mbarrier
+// complete_tx), then bulk-store them crosswise (bulk_group).  Loads run kSwapStages - 2 chunks
+// ahead of the stores; a stage is refilled once its stores have read it.  No data passes through
+// registers, so 24 KB per CTA are in flight with one thread and ~32 KB of shared memory -- it fits
+// on an SM next to the tile kernel's two resident CTAs.
+constexpr int kSwapStages = 4;
+
+template <typename T>
+__global__ void __launch_bounds__(32, 1)
+k_p2p_swap_tma(T* __restrict__ local, T* __restrict__ peer, uint64_t row_amps, uint64_t my_off, uint64_t peer_off,
+               uint64_t t0, uint64_t t1, uint64_t fmask, uint64_t fval, uint32_t chunk_amps) {
+    using V2 = typename SmemAmp<T>::V;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    __shared__ __align__(8) uint64_t mbar[kSwapStages];
+    if (threadIdx.x != 0) return;
+    const uint32_t cbytes = chunk_amps * (uint32_t)sizeof(V2);
+    for (int st = 0; st < kSwapStages; ++st)
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&mbar[st])));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    V2* L = reinterpret_cast<V2*>(local);
+    V2* R = reinterpret_cast<V2*>(peer);
+    const uint64_t nch = (t1 - t0) / chunk_amps;
+    const uint64_t mine = nch > blockIdx.x ? (nch - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+    auto addr = [&](uint64_t m, V2*& lp, V2*& rp) {
+        uint64_t li, ri;
+        swap_index<T>(t0 + (blockIdx.x + m * gridDim.x) * (uint64_t)chunk_amps, row_amps, my_off, peer_off, fmask,
+                      fval, li, ri);
+        lp = L + li;
+        rp = R + ri;
+    };
+    // stage st: [partner's chunk | own chunk]
+    auto sbuf = [&](int st, int w) { return smem_raw + ((size_t)(2 * st + w)) * cbytes; };
+    constexpr int D = kSwapStages - 2;  // loads ahead of stores
+    for (uint64_t m = 0; m < mine + D; ++m) {
+        if (m < mine) {
+            const int st = (int)(m % kSwapStages);
+            // stage st last held chunk m - kSwapStages, whose stores were committed two iterations
+            // ago: at most one newer store group may still be reading shared memory
+            asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+            V2 *lp, *rp;
+            addr(m, lp, rp);
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&mbar[st])),
+                         "r"(2 * cbytes)
+                         : "memory");
+            asm volatile(
+                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                    smem_u32(sbuf(st, 0))),
+                "l"(rp), "r"(cbytes), "r"(smem_u32(&mbar[st]))
+                : "memory");
+            asm volatile(
+                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                    smem_u32(sbuf(st, 1))),
+                "l"(lp), "r"(cbytes), "r"(smem_u32(&mbar[st]))
+                : "memory");
+        }
+        if (m >= (uint64_t)D) {
+            const uint64_t j = m - D;
+            const int st = (int)(j % kSwapStages);
+            mbar_wait(&mbar[st], (uint32_t)((j / kSwapStages) & 1));
+            V2 *lp, *rp;
+            addr(j, lp, rp);
+            asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(lp),
+                         "r"(smem_u32(sbuf(st, 0))), "r"(cbytes)
+                         : "memory");
+            asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(rp),
+                         "r"(smem_u32(sbuf(st, 1))), "r"(cbytes)
+                         : "memory");
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+    }
+    // every store complete (not only read out of shared memory), then system scope for the partner
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    __threadfence_system();
+}
+
 // pairwise barrier between two ranks over peer memory (the overlapped swap's "both ranks finished
 // piece j" / "both halves landed" points): one thread raises the partner's word to `epoch` (system-
 // scope release, after this stream's earlier kernels completed) and spins until its own word from
@@ -2128,7 +2205,7 @@ cudaError_t launch_permute(int dtype, void* a, int nl, int b1, int b2, cudaStrea
 
 cudaError_t launch_p2p_swap(int dtype, void* local, void* peer, uint64_t rows, uint64_t row_amps, uint64_t my_off,
                             uint64_t peer_off, uint64_t t0, uint64_t t1, uint64_t fmask, uint64_t fval, cudaStream_t s,
-                            int ctas) {
+                            int ctas, int tma_chunk) {
     (void)rows;
     if (t1 <= t0) return cudaSuccess;
     // ctas > 0: that many full-size CTAs; 0: one full-size CTA per SM; < 0: the overlap form,
@@ -2141,6 +2218,17 @@ cudaError_t launch_p2p_swap(int dtype, void* local, void* peer, uint64_t rows, u
         else
             k_p2p_swap<float, 8, 512, 1><<<grid, 512, 0, s>>>((float*)local, (float*)peer, row_amps, my_off, peer_off,
                                                                t0, t1, fmask, fval);
+    } else if (tma_chunk > 0) {
+        // TMA form: chunk_amps contiguous elements per chunk, one 32-thread CTA per SM x (-ctas)
+        const unsigned grid = -ctas <= 8 ? (unsigned)(-ctas * num_sms()) : (unsigned)(-ctas);
+        const size_t amp = dtype == PS_C128 ? 16 : 8;
+        const size_t smem = (size_t)2 * kSwapStages * (size_t)tma_chunk * amp;
+        if (dtype == PS_C128)
+            k_p2p_swap_tma<double><<<grid, 32, smem, s>>>((double*)local, (double*)peer, row_amps, my_off, peer_off,
+                                                           t0, t1, fmask, fval, (uint32_t)tma_chunk);
+        else
+            k_p2p_swap_tma<float><<<grid, 32, smem, s>>>((float*)local, (float*)peer, row_amps, my_off, peer_off, t0,
+                                                          t1, fmask, fval, (uint32_t)tma_chunk);
     } else {
         const unsigned grid = -ctas <= 8 ? (unsigned)(-ctas * num_sms()) : (unsigned)(-ctas);
         if (dtype == PS_C128)

@@ -19,7 +19,7 @@ K_STREAM, K_TILE, K_COSET, K_REDUCE, K_INIT, K_EXCHANGE, K_PERMUTE, K_MIRROR, K_
 KERNEL_NAMES = ["stream", "tile", "coset", "reduce", "init", "exchange", "permute", "mirror", "xtile"]
 NK = len(KERNEL_NAMES)
 OP_MIRROR_BEGIN, OP_MIRROR_SWITCH, OP_MIRROR_END = 16, 17, 18
-OPT_PROFILE, OPT_FUSION, OPT_TILE_BITS, OPT_CHUNK_BYTES, OPT_MAX_PASS_ROTS, OPT_VEC256, OPT_TILE_TMA, OPT_CHUNK_BITS, OPT_TILE_TUNE, OPT_LAYOUT, OPT_TRANSPORT, OPT_OVERLAP, OPT_SPECIALIZE, OPT_GRID_CAP, OPT_FUSED_EXCHANGE, OPT_SWAP_CTAS = range(16)
+OPT_PROFILE, OPT_FUSION, OPT_TILE_BITS, OPT_CHUNK_BYTES, OPT_MAX_PASS_ROTS, OPT_VEC256, OPT_TILE_TMA, OPT_CHUNK_BITS, OPT_TILE_TUNE, OPT_LAYOUT, OPT_TRANSPORT, OPT_OVERLAP, OPT_SPECIALIZE, OPT_GRID_CAP, OPT_FUSED_EXCHANGE, OPT_SWAP_CTAS, OPT_SWAP_TMA = range(17)
 
 
 class PsError(RuntimeError):

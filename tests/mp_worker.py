@@ -94,6 +94,28 @@ def main():
                           np.max(np.abs(got - want)), 1e-10)
                     check(f"mid-call norm {tag}", abs(nrm_mid - oracle.norm(n, oracle.random_state(SEED, n))) /
                           oracle.norm(n, oracle.random_state(SEED, n)), 1e-12)
+        # (a2) 18 qubits with default tiles: overlapped swap pieces whose runs reach 1 KB go through the
+        # TMA swap kernel; the register kernels must give bitwise the same state
+        for n in (() if only_large else (18,)):
+            codes, ang = layer_with_global(n, 200, n, world)
+            x, z = P.pauli_encode_codes(codes)
+            want = oracle.apply(n, oracle.random_state(SEED, n), codes, ang) if rank == 0 else None
+            ref = None
+            for ovl, swap_tma, swap_ctas in ((2, 1, 0), (1, 1, 0), (2, 0, 0), (2, 1, -1), (1, 0, 32), (0, 1, 0)):
+                with P.State(n, "c128", world=world, rank=rank) as st:
+                    st.set_option(ps.OPT_OVERLAP, ovl)
+                    st.set_option(ps.OPT_SWAP_TMA, swap_tma)
+                    st.set_option(ps.OPT_SWAP_CTAS, swap_ctas)
+                    st.init_random(SEED)
+                    st.apply_rotations(x, z, ang)
+                    got = st.get_amplitudes()
+                    stats = st.stats()
+                if rank == 0:
+                    tag = f"n={n} overlap={ovl} swap_tma={swap_tma} swap_ctas={swap_ctas} exch={stats['exchanges']}"
+                    check(f"oracle {tag}", np.max(np.abs(got - want)), 1e-10)
+                    if ref is None:
+                        ref = got
+                    check(f"swap kernels bitwise {tag}", 0.0 if np.array_equal(got, ref) else 1.0, 0.0)
         if only_large:
             raise _SkipSmall()
         # (b) full-exchange fallback: local X-part covering every local bit
