@@ -1071,94 +1071,120 @@ static int exchange_overlap(ps_state* h, const Pass& ex, const Pass& np) {
     return PS_OK;
 }
 
-// the previous tile pass, the swap E(gx, ell) and the next tile pass as one pipeline (overlap mode
-// 2): both passes split into P = 2^B pieces by B free bits outside both tile spaces (and not ell);
-// the second stream swaps piece j as soon as both ranks finished the previous pass's piece j
-// (event + barrier), and the next pass's piece j starts when its swap landed.  The swap then
-// overlaps the previous pass as well as the next one.
-static uint64_t split_bits2(const Pass& a, const Pass& b, int ell) {
-    return split_bits(a) & split_bits(b) & ~(1ull << ell);
+// overlap mode 2: a chain  pass, E, pass, E, ..., pass  (tile passes and P2P half exchanges,
+// consecutive exchanges allowed) as one pipeline.  Every pass and every swap region splits into
+// P = 2^B pieces by B local bits that are free bits outside every pass's tile space and are no
+// exchange's ell, so piece j of each step touches only elements whose piece bits equal j.  The
+// main stream runs the passes piece by piece, a pass's piece j waiting for the preceding swap's
+// piece j; the second stream swaps piece j of an exchange as soon as this rank finished the
+// preceding step's piece j and the partner arrived at the same point (pairwise barrier).  A swap
+// then overlaps the passes on both sides of it, and an exchange right after another one (4 and more
+// ranks) still overlaps.
+static bool chain_pass(const Pass& q) { return q.kind == PASS_TILE || q.kind == PASS_COSET; }
+static bool chain_exchange(const ps_state* h, const Pass& q) {
+    return q.kind == PASS_EXCHANGE && !q.full && h->overlap >= 2 && h->xstream && h->p2p && h->transport &&
+           h->tile_tma == 2;
 }
 
-static bool can_overlap3(const ps_state* h, const Pass& pa, const Pass* ex, const Pass* np) {
-    return ex && np && (pa.kind == PASS_TILE || pa.kind == PASS_COSET) && can_overlap(h, *ex, np) &&
-           h->overlap >= 2 && split_bits2(pa, *np, ex->ell) != 0;
-}
-
-static int exchange_overlap3(ps_state* h, const Pass& pa, const Pass& ex, const Pass& np) {
-    const int partner = h->rank ^ (int)ex.gx;
-    const uint64_t rows = 1ull << (h->nl - 1 - ex.ell);
-    const uint64_t row_amps = 1ull << ex.ell, total = rows * row_amps;
-    const uint64_t my_off = (uint64_t)(1 - ex.keep) * row_amps, peer_off = (uint64_t)ex.keep * row_amps;
-    const uint64_t sb = split_bits2(pa, np, ex.ell);
+// end (exclusive) of the longest chain starting at tile pass passes[b], or 0 if there is none;
+// *pbits_out = the piece bits (the highest common split bits, at most piece_bits of them)
+static size_t overlap_chain_end(const ps_state* h, const std::vector<Pass>& passes, size_t b, uint64_t* pbits_out) {
+    if (h->overlap < 2 || !chain_pass(passes[b])) return 0;
+    uint64_t sb = split_bits(passes[b]);
+    int want = 0;  // split bits the first segment keeps; later segments must keep as many
+    size_t end = 0, k = b + 1;
+    while (k < passes.size()) {
+        uint64_t ells = 0;
+        size_t m = k;
+        while (m < passes.size() && chain_exchange(h, passes[m])) ells |= 1ull << passes[m++].ell;
+        if (m == k || m >= passes.size() || !chain_pass(passes[m])) break;
+        const uint64_t nsb = sb & ~ells & split_bits(passes[m]);
+        const int have = __builtin_popcountll(nsb);
+        if (have == 0 || (end && have < want)) break;
+        if (!end) want = std::min(have, std::min(h->piece_bits, (int)ps_state::kMaxPieceBits));
+        sb = nsb;
+        end = m + 1;
+        k = m + 1;
+    }
+    if (!end) return 0;
     uint64_t pbits = 0;
     int B = 0;
-    for (int b = 63; b >= 0 && B < std::min(h->piece_bits, (int)ps_state::kMaxPieceBits); --b)
-        if ((sb >> b) & 1) {
-            pbits |= 1ull << b;
+    for (int q = 63; q >= 0 && B < want; --q)
+        if ((sb >> q) & 1) {
+            pbits |= 1ull << q;
             ++B;
         }
-    const int P = 1 << B;  // <= 8: events xev[1..P] (previous pass) and xev[1+P..2P] (swap)
-    auto elem_bits = [&](uint64_t m) {
-        uint64_t r = 0;
-        for (; m; m &= m - 1) {
-            const int f = __builtin_ctzll(m);
-            r |= 1ull << (f < ex.ell ? f : f - 1);
-        }
-        return r;
-    };
+    *pbits_out = pbits;
+    return end;
+}
+
+static int overlap_chain(ps_state* h, const std::vector<Pass>& passes, size_t b, size_t e, uint64_t pbits) {
+    const int P = 1 << __builtin_popcountll(pbits);  // <= 8: events xev[1..P] (passes), xev[1+P..2P] (swaps)
     auto deposit = [](uint64_t v, uint64_t mask) {
         uint64_t r = 0;
         for (; mask; mask &= mask - 1, v >>= 1)
             if (v & 1) r |= mask & (~mask + 1);
         return r;
     };
-    const uint64_t emask = elem_bits(pbits);
-    const uint64_t piece = total >> B;
-    const uint64_t t0 = ex.keep ? piece / 2 : 0, t1 = ex.keep ? piece : piece / 2;
-    auto run_piece = [&](const Pass& q0, int j) -> int {
-        Pass q = q0;
-        q.free_mask = q0.free_mask & ~pbits;
-        q.or_mask = q0.or_mask | deposit((uint64_t)j, pbits);
-        Timed t(h, q0.kind);
-        CUDA_TRY(h, launch_tile(h->dtype, h->d_state, h->nl, q, h->d_subs, h->d_trots, h->d_offs, h->tile_tma,
-                                h->tile_tune, h->stream, h->cur_plan->subs.data(), h->cur_plan->trots.data(),
-                                h->grid_cap));
-        return PS_OK;
-    };
-    int rc = PS_OK;
-    for (int j = 0; j < P; ++j) {
-        if ((rc = run_piece(pa, j))) return rc;
-        CUDA_TRY(h, cudaEventRecord(h->xev[1 + j], h->stream));
-    }
-    {
-        Timed t(h, PS_K_EXCHANGE, h->xstream);
-        for (int j = 0; j < P; ++j) {
-            CUDA_TRY(h, cudaStreamWaitEvent(h->xstream, h->xev[1 + j], 0));
-            if ((rc = pair_barrier(h, h->xstream, partner, 1))) return rc;  // both ranks finished piece j
-            CUDA_TRY(h, launch_p2p_swap(h->dtype, h->d_state, h->peers[partner], rows, row_amps, my_off, peer_off, t0,
-                                        t1, emask, deposit((uint64_t)j, emask), h->xstream, h->swap_ctas,
-                                        h->swap_ctas < 0 ? swap_tma_chunk(h, row_amps, emask, t0, t1) : 0));
-            if ((rc = pair_barrier(h, h->xstream, partner, 2))) return rc;  // both halves of piece j landed
-            CUDA_TRY(h, cudaEventRecord(h->xev[1 + P + j], h->xstream));
-        }
-    }
-    for (int j = 0; j < P; ++j) {
-        CUDA_TRY(h, cudaStreamWaitEvent(h->stream, h->xev[1 + P + j], 0));
-        if ((rc = run_piece(np, j))) return rc;
-    }
     const double pass_bytes = 2.0 * (double)h->amp_bytes * (double)local_amps(h);
-    for (const Pass* q : {&pa, &np}) {
-        h->stats.launches[q->kind] += 1;
-        h->stats.rotations_by[q->kind] += (uint64_t)q->rot_count;
-        h->stats.algo_bytes[q->kind] += pass_bytes;
-        h->stats.passes += 1;
+    int rc = PS_OK;
+    bool after_swap = false;
+    for (size_t k = b; k < e; ++k) {
+        const Pass& st = passes[k];
+        if (chain_pass(st)) {
+            for (int j = 0; j < P; ++j) {
+                if (after_swap) CUDA_TRY(h, cudaStreamWaitEvent(h->stream, h->xev[1 + P + j], 0));
+                Pass q = st;
+                q.free_mask = st.free_mask & ~pbits;
+                q.or_mask = st.or_mask | deposit((uint64_t)j, pbits);
+                {
+                    Timed t(h, st.kind);
+                    CUDA_TRY(h, launch_tile(h->dtype, h->d_state, h->nl, q, h->d_subs, h->d_trots, h->d_offs,
+                                            h->tile_tma, h->tile_tune, h->stream, h->cur_plan->subs.data(),
+                                            h->cur_plan->trots.data(), h->grid_cap));
+                }
+                CUDA_TRY(h, cudaEventRecord(h->xev[1 + j], h->stream));
+            }
+            after_swap = false;
+            h->stats.launches[st.kind] += 1;  // the pieces are one logical pass over the local state
+            h->stats.rotations_by[st.kind] += (uint64_t)st.rot_count;
+            h->stats.algo_bytes[st.kind] += pass_bytes;
+            h->stats.passes += 1;
+            continue;
+        }
+        // a half exchange E(gx, ell), swapped piece by piece on the second stream
+        const int partner = h->rank ^ (int)st.gx;
+        const uint64_t rows = 1ull << (h->nl - 1 - st.ell);
+        const uint64_t row_amps = 1ull << st.ell, total = rows * row_amps;
+        const uint64_t my_off = (uint64_t)(1 - st.keep) * row_amps, peer_off = (uint64_t)st.keep * row_amps;
+        uint64_t emask = 0;  // piece bits in region-element positions (bit ell removed)
+        for (uint64_t m = pbits; m; m &= m - 1) {
+            const int f = __builtin_ctzll(m);
+            emask |= 1ull << (f < st.ell ? f : f - 1);
+        }
+        const uint64_t piece = total / (uint64_t)P;
+        const uint64_t t0 = st.keep ? piece / 2 : 0, t1 = st.keep ? piece : piece / 2;
+        {
+            Timed t(h, PS_K_EXCHANGE, h->xstream);
+            for (int j = 0; j < P; ++j) {
+                // after a pass: this rank finished its piece j (event); after a swap the stream order
+                // already holds.  Then the partner reached the same point (pair barrier).
+                if (!after_swap) CUDA_TRY(h, cudaStreamWaitEvent(h->xstream, h->xev[1 + j], 0));
+                if ((rc = pair_barrier(h, h->xstream, partner, 1))) return rc;
+                CUDA_TRY(h, launch_p2p_swap(h->dtype, h->d_state, h->peers[partner], rows, row_amps, my_off, peer_off,
+                                            t0, t1, emask, deposit((uint64_t)j, emask), h->xstream, h->swap_ctas,
+                                            h->swap_ctas < 0 ? swap_tma_chunk(h, row_amps, emask, t0, t1) : 0));
+                if ((rc = pair_barrier(h, h->xstream, partner, 2))) return rc;  // both halves of piece j landed
+                CUDA_TRY(h, cudaEventRecord(h->xev[1 + P + j], h->xstream));
+            }
+        }
+        after_swap = true;
+        const double region = (double)(total * h->amp_bytes);
+        h->stats.nvlink_bytes += region;
+        h->stats.exchanges += 1;
+        h->stats.launches[PS_K_EXCHANGE] += 1;
+        h->stats.algo_bytes[PS_K_EXCHANGE] += region * 2.0;
     }
-    const double region = (double)(rows * row_amps * h->amp_bytes);
-    h->stats.nvlink_bytes += region;
-    h->stats.exchanges += 1;
-    h->stats.launches[PS_K_EXCHANGE] += 1;
-    h->stats.algo_bytes[PS_K_EXCHANGE] += region * 2.0;
     return PS_OK;
 }
 
@@ -1479,10 +1505,14 @@ static int execute_plans(const RankSet& rs, const std::vector<Plan*>& plans) {
             ++pi;  // the next pass ran inside the fused kernel
             continue;
         }
-        if (G == 1 && pi + 2 < np && can_overlap3(rs[0], p0, next, &plans[0]->passes[pi + 2])) {
-            rc = exchange_overlap3(rs[0], p0, *next, plans[0]->passes[pi + 2]);
-            pi += 2;  // the exchange and the pass after it ran inside the pipeline
-            continue;
+        if (G == 1 && rs[0]->overlap >= 2) {
+            uint64_t pbits = 0;
+            const size_t ce = overlap_chain_end(rs[0], plans[0]->passes, pi, &pbits);
+            if (ce) {
+                rc = overlap_chain(rs[0], plans[0]->passes, pi, ce, pbits);
+                pi = ce - 1;  // the whole chain ran inside the pipeline
+                continue;
+            }
         }
         if (G == 1 && p0.kind == PASS_EXCHANGE && can_overlap(rs[0], p0, next)) {
             rc = exchange_overlap(rs[0], p0, *next);
