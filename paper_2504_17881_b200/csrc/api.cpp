@@ -1089,7 +1089,8 @@ static bool chain_exchange(const ps_state* h, const Pass& q) {
 // end (exclusive) of the longest chain starting at tile pass passes[b], or 0 if there is none;
 // *pbits_out = the piece bits (the highest common split bits, at most piece_bits of them)
 static size_t overlap_chain_end(const ps_state* h, const std::vector<Pass>& passes, size_t b, uint64_t* pbits_out) {
-    if (h->overlap < 2 || !chain_pass(passes[b])) return 0;
+    // with the fused exchange + tile kernel on, every fusable exchange runs fused instead
+    if (h->overlap < 2 || h->fused || !chain_pass(passes[b])) return 0;
     uint64_t sb = split_bits(passes[b]);
     int want = 0;  // split bits the first segment keeps; later segments must keep as many
     size_t end = 0, k = b + 1;
