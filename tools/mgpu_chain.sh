@@ -13,3 +13,4 @@ run R10_chain_pb3 --overlap $(( (4 << 16) | 2 ))
 nw=$((30 + $(python -c "print(($N).bit_length()-1)")))
 run R10_${nw}_weak --qubits $nw
 run JW_32 --kind JW --qubits 32
+run R10_fused --fused 1
