@@ -128,11 +128,12 @@ enum {
     PS_OPT_TRANSPORT = 10,    /* world > 1: 1 = NVLink P2P swap kernel on CUDA-IPC peer pointers when
                                  available (default); 0 = NCCL send/recv with staging */
     PS_OPT_OVERLAP = 11,      /* world > 1, P2P: 2 = each swap overlaps the tile passes before and
-                                 after it (default): both passes run in 2^B pieces split by free
-                                 bits outside their tiles, a piece is swapped as soon as both ranks
-                                 finished it (pairwise P2P flag barrier) and the next pass's piece
-                                 runs as soon as it landed; 1 = only with the pass after it;
-                                 0 = serialise; bits 16-18 = B + 1 (default B = 2) */
+                                 after it (default): a chain pass, E, pass, ..., pass runs in 2^B
+                                 pieces split by free bits outside every tile, a piece is swapped as
+                                 soon as both ranks finished it (pairwise P2P flag barrier) and the
+                                 next pass's piece runs as soon as it landed; 1 = only with the pass
+                                 after it; 0 = serialise; bits 16-18 = B + 1 (default B = 2).  Like
+                                 every option, it must be set identically on all ranks */
     PS_OPT_SPECIALIZE = 12    /* tile-kernel variant: 2 = specialised (default for C128): CFORM
                                  rotations whose sub-group xor mask dx is a unit vector or 0 run
                                  through one of 80 compile-time cases (per-pair signs and pairing
