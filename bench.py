@@ -536,9 +536,13 @@ def run_ours(args):
             "exchanges": stats["exchanges"],
             "exchange_ms": stats["kernel_ms"]["exchange"],
             # per direction per GPU: swap exchanges over their own (CUDA-event) time; fused exchange +
-            # tile passes over theirs (NVLink 5: 900 GB/s per direction nominal, 770 measured peer copy)
+            # tile passes over theirs (NVLink 5: 900 GB/s per direction nominal, 770 measured peer copy).
+            # With overlap (modes 1, 2) a swap's time runs on its stream from the first piece to the last
+            # and includes the waits for pass pieces, so this is a lower bound on the link rate; the
+            # serialised rate is the --overlap 0 line (profiles/r02/multi_gpu.md)
             "nvlink_gbs": (stats["nvlink_bytes"] / (stats["kernel_ms"]["exchange"] / 1e3) / 1e9
                            if stats["kernel_ms"]["exchange"] > 0 and stats["nvlink_bytes"] > 0 else None),
+            "nvlink_gbs_includes_overlap_waits": bool(world > 1 and args.overlap > 0),
             "nvlink_fused_gbs": (stats["nvlink_fused_bytes"] / (stats["kernel_ms"]["xtile"] / 1e3) / 1e9
                                  if stats["kernel_ms"]["xtile"] > 0 else None),
             "best_step_ms": min(step_ms) if step_ms else None,
