@@ -1943,6 +1943,10 @@ cudaError_t launch_coset_param(T* a, int nl, const Pass& p, const DevSub* h_subs
         if (occ_sel == 0 && threads <= 128)
             return narrow ? launch_coset_param_k<T, 128, 8, 0, 1>(a, p, recs, d_offs, l2_prefetch, grid_mult, s)
                           : launch_coset_param_k<T, 128, 8>(a, p, recs, d_offs, l2_prefetch, grid_mult, s);
+    if constexpr (sizeof(T) == 4)
+        if (occ_sel == 3 && threads == 256)  // fp32 2^12 tiles: 4 CTAs per SM at 64 registers (A/B)
+            return narrow ? launch_coset_param_k<T, 256, 4, 0, 1>(a, p, recs, d_offs, l2_prefetch, grid_mult, s)
+                          : launch_coset_param_k<T, 256, 4>(a, p, recs, d_offs, l2_prefetch, grid_mult, s);
     if (threads == 512) return launch_coset_param_k<T, 512, 1>(a, p, recs, d_offs, l2_prefetch, grid_mult, s);
     if constexpr (sizeof(T) == 4)
         if (threads == 1024) return launch_coset_param_k<T, 1024, 1>(a, p, recs, d_offs, l2_prefetch, grid_mult, s);
