@@ -522,7 +522,7 @@ def run_ours(args):
             "scaling": "strong", "vs_baseline": None, "dtype": "f64" if args.dtype == "c128" else "f32",
             "data": "synthetic",
             "config": {"workload": workload_name(args), "n_qubits": args.n, "rotations_per_step": rot_per_step,
-                       "fusion": args.fusion, "tile_mode": args.tile_mode, "tile_bits": args.tile_bits or (12 if args.dtype == "c128" else 11),
+                       "fusion": args.fusion, "tile_mode": args.tile_mode, "tile_bits": args.tile_bits or 12,
                        "layout": args.layout, "transport": args.transport, "overlap": args.overlap, "swap_ctas": args.swap_ctas, "swap_tma": args.swap_tma, "specialize": args.specialize if args.specialize >= 0 else (2 if args.dtype == "c128" else 0),
                        "parallelism": (f"state sharded over {args.emulate} virtual ranks on 1 GPU (emulation)"
                                        if args.emulate else f"state sharded over {world} GPU(s) by top qubits"),

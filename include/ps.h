@@ -98,7 +98,7 @@ enum {
     PS_OPT_PROFILE = 0,       /* 1: time every launch with CUDA events on the handle's stream (default 0) */
     PS_OPT_FUSION = 1,        /* 0: one rotation per pass (K1 only); 1: same-x runs; 2: + tiles (default 2) */
     PS_OPT_TILE_BITS = 2,     /* log2 amplitudes per fused tile, 4..13 for C128 (default 12),
-                                 4..14 for C64 (default 11); 2^13 / 2^14 tiles run one CTA of
+                                 4..14 for C64 (default 12); 2^13 / 2^14 tiles run one CTA of
                                  512 / 1024 threads per SM */
     PS_OPT_CHUNK_BYTES = 3,   /* exchange chunk size in bytes (default 256 MiB) */
     PS_OPT_MAX_PASS_ROTS = 4, /* cap on rotations fused into one tile pass (default: no cap) */

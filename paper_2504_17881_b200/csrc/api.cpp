@@ -418,7 +418,9 @@ static int make_state(int n_qubits, int dtype, void* dev_buf, size_t bytes, void
     // per-dtype defaults (profiles/r01/kernel_ab.md): fp64 2^12 tiles with the next tile's first
     // sub-group prefetched into shared memory (tune bit 11); fp32 2^11 tiles at 8 CTAs per SM,
     // where the prefetch costs more occupancy than it hides
-    h->tile_bits = dtype == PS_C128 ? 12 : 11;
+    // 2^12-amplitude tiles for both dtypes (fp32 on 256 threads x 4 CTAs per SM: R10 +5.7 % over
+    // 2^11 tiles, JW -1.6 %; profiles/r02/kernel_ab.md section 10)
+    h->tile_bits = 12;
     h->tile_tune = dtype == PS_C128 ? (1536 | 2048) : 1536;
     // fp64: unit-dx CFORM rotations with compile-time signs (+6 % R10, +9 % JW, +15 % gates;
     // profiles/r02/kernel_ab.md); fp32 keeps the generic kernel (its 64-register 8-CTA build spills)

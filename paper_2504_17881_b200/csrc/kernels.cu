@@ -1854,6 +1854,9 @@ cudaError_t launch_coset_t(T* a, int nl, const Pass& p, const DevSub* d_subs, co
     if (occ_sel == 0 && sizeof(T) == 4 && !p.spec) occ_sel = 3;
     if (threads <= 128 && !p.spec && occ_sel == 3)
         return launch_coset_k<T, 128, 8, 0>(a, nl, p, d_subs, d_trots, d_offs, l2_prefetch, grid_mult, s);
+    if constexpr (sizeof(T) == 4)
+        if (threads == 256 && !p.spec && occ_sel == 3)  // fp32 2^12 tiles (default): 4 CTAs x 64 registers
+            return launch_coset_k<T, 256, 4, 0>(a, nl, p, d_subs, d_trots, d_offs, l2_prefetch, grid_mult, s);
     // tiles of 2^13 (fp64) / 2^13..2^14 (fp32) amplitudes: one CTA of 512 / 1024 threads per SM
     if (threads == 512)
         return launch_coset_k<T, 512, 1, 0>(a, nl, p, d_subs, d_trots, d_offs, l2_prefetch, grid_mult, s);
@@ -1944,7 +1947,7 @@ cudaError_t launch_coset_param(T* a, int nl, const Pass& p, const DevSub* h_subs
             return narrow ? launch_coset_param_k<T, 128, 8, 0, 1>(a, p, recs, d_offs, l2_prefetch, grid_mult, s)
                           : launch_coset_param_k<T, 128, 8>(a, p, recs, d_offs, l2_prefetch, grid_mult, s);
     if constexpr (sizeof(T) == 4)
-        if (occ_sel == 3 && threads == 256)  // fp32 2^12 tiles: 4 CTAs per SM at 64 registers (A/B)
+        if ((occ_sel == 0 || occ_sel == 3) && threads == 256)  // fp32 2^12 tiles (default): 4 CTAs x 64 registers
             return narrow ? launch_coset_param_k<T, 256, 4, 0, 1>(a, p, recs, d_offs, l2_prefetch, grid_mult, s)
                           : launch_coset_param_k<T, 256, 4>(a, p, recs, d_offs, l2_prefetch, grid_mult, s);
     if (threads == 512) return launch_coset_param_k<T, 512, 1>(a, p, recs, d_offs, l2_prefetch, grid_mult, s);

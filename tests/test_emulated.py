@@ -171,7 +171,7 @@ def test_expectation_without_free_pivot(world):
 @pytest.mark.parametrize("dtype", ["c128", "c64"])
 @pytest.mark.parametrize("kind", ["R10", "R4", "S8"])
 def test_emulated_large_default_options(world, dtype, kind):
-    """22 qubits, default options (2^12 / 2^11 tiles, fused exchange, lazy layout): the bench's
+    """22 qubits, default options (2^12 tiles, fused exchange, lazy layout): the bench's
     launch configuration on the multi-rank path, full-state oracle comparison."""
     n = 22
     codes, ang = workloads.random_layer(n, 150, seed=44, kind=kind)

@@ -2,7 +2,7 @@
 
 * large-n sweeps (22 and 24 qubits, default options): full-state comparison with the CPU oracle
   for every random-layer kind, fp64 and fp32.  At 24 qubits both dtypes run several tiles per CTA
-  of the persistent grid (2^12 fp64 tiles on a 1184-CTA grid, 2^11 fp32 tiles on a 4736-CTA grid),
+  of the persistent grid (2^12 fp64 tiles on a 1184-CTA grid, 2^12 fp32 tiles on a 2368-CTA grid),
   so the incremental tile bases and the next-tile prefetch run exactly as in the 30-qubit bench;
 * a grid cap (PS_OPT_GRID_CAP) forces many tiles per CTA at 14-18 qubits;
 * 2^13 / 2^14-amplitude tiles (one CTA of 512 / 1024 threads per SM);
