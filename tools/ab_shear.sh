@@ -1,5 +1,6 @@
 #!/bin/bash
 # A/B: unit-case rotations as three in-place shears (libps_shear.so, -DPS_SHEAR=1) vs the 4-FMA
+# build the A/B library first: python -m paper_2504_17881_b200.build --force -DPS_SHEAR=1 --out=paper_2504_17881_b200/libps_shear.so
 # deferred-scale form (default build), same box
 D=gpurun_out/shear; mkdir -p $D
 export PS_LIB_PATH=$PWD/paper_2504_17881_b200/libps_shear.so
