@@ -1,7 +1,7 @@
 #!/bin/bash
 # A/B: unit-case rotations as three in-place shears (libps_shear.so, -DPS_SHEAR=1) vs the 4-FMA
-# build the A/B library first: python -m paper_2504_17881_b200.build --force -DPS_SHEAR=1 --out=paper_2504_17881_b200/libps_shear.so
 # deferred-scale form (default build), same box
+# build the A/B library first: python -m paper_2504_17881_b200.build --force -DPS_SHEAR=1 --out=paper_2504_17881_b200/libps_shear.so
 D=gpurun_out/shear; mkdir -p $D
 export PS_LIB_PATH=$PWD/paper_2504_17881_b200/libps_shear.so
 timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_workloads.py tests/test_emulated.py -q -x > $D/tests_shear.log 2>&1
