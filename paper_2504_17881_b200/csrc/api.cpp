@@ -1508,7 +1508,9 @@ static int execute_plans(const RankSet& rs, const std::vector<Plan*>& plans) {
             ++pi;  // the next pass ran inside the fused kernel
             continue;
         }
-        if (G == 1 && rs[0]->overlap >= 2) {
+        // the overlap pipelines run their passes on the state itself: not inside a mirror section
+        const bool on_state = target[0] == rs[0]->d_state;
+        if (G == 1 && on_state && rs[0]->overlap >= 2) {
             uint64_t pbits = 0;
             const size_t ce = overlap_chain_end(rs[0], plans[0]->passes, pi, &pbits);
             if (ce) {
@@ -1517,7 +1519,7 @@ static int execute_plans(const RankSet& rs, const std::vector<Plan*>& plans) {
                 continue;
             }
         }
-        if (G == 1 && p0.kind == PASS_EXCHANGE && can_overlap(rs[0], p0, next)) {
+        if (G == 1 && on_state && p0.kind == PASS_EXCHANGE && can_overlap(rs[0], p0, next)) {
             rc = exchange_overlap(rs[0], p0, *next);
             ++pi;  // the next pass ran inside the overlap
             continue;

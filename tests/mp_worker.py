@@ -68,7 +68,8 @@ def main():
                     (0, 4096, 0, 0, 1, 0), (1, 1 << 28, 0, 1, 1, 0), (2, 4096, 0, 0, 1, 0), (2, 1 << 28, 1, 1, 1, 0),
                     (0, 1 << 28, 1, 0, 1, 0), (2, 4096, 1, 1, 0, 0), (2, 1 << 28, 2, 1, 1, 0), (1, 4096, 2, 0, 1, 0),
                     (2, 1 << 28, 1, 1, 1, 1), (2, 4096, 0, 1, 0, 1), (2, 1 << 28, 1, 1, 2, 0), (2, 1 << 28, 0, 1, 2, 0),
-                    (2, 1 << 28, 1, 1, 11, 0), (2, 1 << 28, 1, 1, 12, 0)):
+                    (2, 1 << 28, 1, 1, 11, 0), (2, 1 << 28, 1, 1, 12, 0), (2, 1 << 28, 2, 1, 2, 0),
+                    (1, 4096, 2, 1, 2, 0)):
                 # ovl >= 10: overlap mode ovl - 10 with 32 full-size swap CTAs (else the slim kernel)
                 with P.State(n, "c128", world=world, rank=rank) as st:
                     st.set_option(ps.OPT_FUSED_EXCHANGE, fused)
