@@ -556,6 +556,17 @@ def run_ours(args):
             # costs 2 FMA per amplitude and rotation (4 per pair); peak = 148 SMs x 64 fp64 (128 fp32)
             # FMA lanes x the max SM clock (B200_PROFILING.md: 148 SMs, 1965 MHz)
             "roofline_fma": fma_roofline(stats, fam, args, world, clk),
+            # exchange rotations (world > 1): swap NVLink rate per direction per GPU against NVLink 5's
+            # nominal 900 GB/s per direction (770 GB/s = our measured peer copy, DESIGN.md section 5
+            # K3); with overlap the swap time includes waits (a lower bound)
+            "roofline_nvlink": ({"bound": "nvlink", "unit": "GB/s",
+                                 "achieved": stats["nvlink_bytes"] / (stats["kernel_ms"]["exchange"] / 1e3) / 1e9,
+                                 "peak": 900.0, "peak_source": "NVLink 5 nominal per direction",
+                                 "frac": stats["nvlink_bytes"] / (stats["kernel_ms"]["exchange"] / 1e3) / 1e9 / 900.0,
+                                 "measured_peer_copy_gbs": 770.0,
+                                 "includes_overlap_waits": bool(args.overlap > 0)}
+                                if world > 1 and stats["kernel_ms"]["exchange"] > 0 and stats["nvlink_bytes"] > 0
+                                else None),
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": gpu_launches,
